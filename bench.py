@@ -1,0 +1,402 @@
+#!/usr/bin/env python3
+"""xorgensGP throughput on B200: RN/s (32-bit, device-timed), % of HBM roofline.
+
+Default workload (BASELINE.json configs[1]): fill of 2^30 uint32 per GPU,
+P = 2^14 streams x 2^16 words, base_seed 1, block-major, bit-exact with the
+reference.  A "step" is one BlockEnsemble::generate(2^16) pass over the
+persistent ensemble (streams continue across steps, exactly like repeated
+generate() calls in the reference, proj/src/parallel.cpp:97-135 and
+proj/src/bench.cpp:95-112) -- one fill_kernel launch.
+
+Other workloads (--workload): fill_f32, fill_f64 (config 3), fill_2p34
+(config 4: 2^34 words over N GPUs, strong scaling), mc_pi (config 5: 2^40
+samples over N GPUs, one NCCL all-reduce of the uint64 hit count).
+
+  python bench.py [--gpus N --steps K --warmup W] [--workload W] [--impl reference]
+Multi-GPU: launched by torchrun, one rank per GPU; each rank owns a disjoint
+stream range; timing = max over ranks of CUDA-event time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_BYTES = 126 * 2**20
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(workload: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                parts = [x.strip() for x in out.strip().split(",")]
+                if len(parts) >= 7:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_setup():
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    elif world == 1:
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# --------------------------------------------------------------------------
+# CPU baseline / reference arm: the reference's own code (oracle/_ref),
+# BlockEnsemble(p, 1, P, 63).generate(per_block) on all host threads,
+# wall-clocked around generate() as measure_ensemble_throughput does.
+# --------------------------------------------------------------------------
+
+def reference_rate(streams: int, per_block: int, trials: int, warmup: int = 1, budget_s: float = 30.0):
+    from oracle import REF_SO, Oracle, Reference
+
+    threads = os.cpu_count() or 1
+    if os.path.exists(REF_SO):
+        ref = Reference()
+        p = Oracle().gp32()
+        h = ref.ensemble(p, 1, streams, 63)
+        rates = []
+        t0 = time.perf_counter()
+        for i in range(warmup + trials):
+            secs, _ = ref.generate_timed(h, per_block, threads)
+            if i >= warmup:
+                rates.append(streams * per_block / secs)
+            if time.perf_counter() - t0 > budget_s and len(rates) >= 1:
+                break
+        ref.destroy(h)
+        kind = "reference"
+    else:  # the C restatement, when the reference could not be compiled
+        import numpy as np  # noqa: F401
+
+        o = Oracle()
+        e = o.ensemble(1, streams)
+        rates = []
+        for i in range(warmup + trials):
+            t = time.perf_counter()
+            e.fill_u32(per_block)
+            dt = time.perf_counter() - t
+            if i >= warmup:
+                rates.append(streams * per_block / dt)
+        kind = "port"
+    return {"value": statistics.mean(rates), "unit": "RN/s", "cores": threads, "kind": kind,
+            "sample": f"BlockEnsemble(xorgensgp32, base_seed=1, blocks={streams}, lanes=63)"
+                      f".generate({per_block}) = {streams * per_block} words per trial, "
+                      f"{len(rates)} trials after {warmup} warm-up, workers={threads}, "
+                      f"wall clock around generate() (proj/src/bench.cpp:95-112)",
+            "trials": len(rates), "min": min(rates), "max": max(rates)}
+
+
+def run_reference_arm(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    streams = 1 << 14
+    per_block = 1 << 13  # 2^27 words per step (8 B/word in the reference: 1 GiB of vectors)
+    base = reference_rate(streams, per_block, trials=max(1, args.steps), warmup=args.warmup,
+                          budget_s=120.0)
+    v = base["value"]
+    line = {
+        "impl": "reference", "metric": "RN/s (32-bit, device-timed) at 1/2/4/8 B200; % of HBM write BW",
+        "value": v, "unit": "RN/s", "n_gpus": world, "steps": base["trials"], "warmup": args.warmup,
+        "ms_per_step": streams * per_block / v * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "xorgensGP fill, xorgensgp32, base_seed 1, 2^14 streams "
+                               f"(reference BlockEnsemble::generate, {per_block} words/stream/step "
+                               "bounded sample of the 2^30-word config)",
+                   "streams": streams, "per_stream": per_block},
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": v, "unit": "RN/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+
+def timed_loop(fn, stream, steps, warmup, world, flush=None):
+    """W warm-ups, then K timed steps bracketed by barrier + synchronize;
+    per-step CUDA events on the launching stream.  Returns (total_ms, [step_ms])."""
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps)]
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for i in range(steps):
+        if flush is not None:
+            flush()
+        evs[2 * i].record(stream)
+        fn()
+        evs[2 * i + 1].record(stream)
+    end.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    step_ms = [evs[2 * i].elapsed_time(evs[2 * i + 1]) for i in range(steps)]
+    total = start.elapsed_time(end)
+    return total, step_ms
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="fill_u32",
+                    choices=["fill_u32", "fill_f32", "fill_f64", "fill_2p34", "mc_pi"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+
+    import paper_1108_0486_b200 as xg
+
+    world, rank, local = dist_setup()
+    stream = torch.cuda.current_stream()
+    p = xg.xorgensgp32_params()
+    wl = args.workload
+    hbm_peak, peak_src = load_peaks()
+
+    # workload geometry (per rank)
+    if wl in ("fill_u32", "fill_f32", "fill_f64"):
+        P, per = 1 << 14, 1 << 16                       # 2^30 values per GPU (weak scaling)
+        first, count = rank * P, P
+        scaling = "weak"
+    elif wl == "fill_2p34":
+        total_streams, per = 1 << 18, 1 << 16           # 2^34 words over the job (strong scaling)
+        first, count = xg.partition(total_streams, world, rank)
+        scaling = "strong"
+    else:  # mc_pi: 2^40 samples over the job
+        total_streams = 1 << 17
+        first, count = xg.partition(total_streams, world, rank)
+        per = (1 << 40) // total_streams               # samples per stream = 2^23
+        scaling = "strong"
+    ens = xg.BlockEnsemble(p, 1, count, 63, first_stream=first, device=local)
+
+    out = None
+    bytes_per_val = {"fill_u32": 4, "fill_f32": 4, "fill_f64": 8, "fill_2p34": 4, "mc_pi": 0}[wl]
+    words_per_val = 2 if wl in ("fill_f64", "mc_pi") else 1
+    if wl in ("fill_u32", "fill_2p34"):
+        out = torch.empty((count, per), dtype=torch.uint32, device="cuda")
+        fn = lambda: ens.fill_u32(per, out=out)  # noqa: E731
+    elif wl == "fill_f32":
+        out = torch.empty((count, per), dtype=torch.float32, device="cuda")
+        fn = lambda: ens.fill_f32(per, out=out)  # noqa: E731
+    elif wl == "fill_f64":
+        out = torch.empty((count, per), dtype=torch.float64, device="cuda")
+        fn = lambda: ens.fill_f64(per, out=out)  # noqa: E731
+    else:
+        hits = torch.zeros(1, dtype=torch.int64, device="cuda")
+        fn = lambda: ens.mc_pi(per, hits=hits)  # noqa: E731
+
+    vals_per_step = count * per
+    words_per_step = vals_per_step * words_per_val
+    launches0 = xg.kernel_launches()
+    with ClockSampler(local) as clk:
+        total_ms, step_ms = timed_loop(fn, stream, args.steps, args.warmup, world)
+    launches = xg.kernel_launches() - launches0 - args.warmup * (1 if wl != "mc_pi" else 1)
+    t_max = max_over_ranks(total_ms, world)
+    job_words = words_per_step * world if scaling == "weak" else (
+        (1 << 34) if wl == "fill_2p34" else (1 << 41))
+    value = job_words * args.steps / (t_max / 1e3)
+    kern_ms = statistics.mean(step_ms)
+    state_bytes = 2 * count * 129 * 4                     # window + weyl read and written back
+    alg_bytes = vals_per_step * bytes_per_val + state_bytes
+
+    result = {
+        "metric": "RN/s (32-bit, device-timed) at 1/2/4/8 B200; % of HBM write BW",
+        "value": value, "unit": "RN/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None,
+        "dtype": {"fill_f32": "u32->f32", "fill_f64": "u32->f64"}.get(wl, "u32"),
+        "data": "synthetic (seeded generator state; no input data)",
+        "config": {"workload": {
+            "fill_u32": "xorgensGP fill of 2^30 uint32 per GPU, bit-exact vs CPU per stream",
+            "fill_f32": "uniform float32 [0,1) fill of 2^30 values per GPU, fused conversion",
+            "fill_f64": "uniform float64 [0,1) fill of 2^30 values (2^31 words) per GPU, fused conversion",
+            "fill_2p34": "disjoint-stream fill of 2^34 uint32 across N GPUs",
+            "mc_pi": "fused in-register Monte Carlo pi, 2^40 samples across N GPUs"}[wl],
+            "params": "xorgensgp32 (128,65,15,14,12,17) w=32", "base_seed": 1,
+            "streams_per_gpu": count, "values_per_stream": per,
+            "layout": "block-major out[g*per_stream+k]",
+            "l2": "output per step >> 126 MB L2 (no flush needed)" if bytes_per_val else
+                  "no HBM traffic (in-register consumer)",
+            "parallelism": f"dp{world} (disjoint stream ranges, no data-path collective)"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if bytes_per_val:
+        achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+        result["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                              "frac": achieved / hbm_peak, "traffic": load_traffic(wl),
+                              "peak_source": peak_src,
+                              "alg_bytes_per_launch": alg_bytes,
+                              "kernel_ms_mean": kern_ms, "kernel_ms_min": min(step_ms)}
+        # write-only ceiling on the same buffer, same run (context for frac)
+        if out is not None:
+            def memset():
+                out.view(torch.uint8).fill_(0)
+            m_ms, m_steps = timed_loop(memset, stream, 5, 3, 1)
+            result["roofline"]["write_only_peak_gbs"] = out.numel() * out.element_size() / (
+                min(m_steps) / 1e3) / 1e9
+    else:
+        # in-register consumer: report integer-issue context
+        hits_v = int(hits.item())
+        if world > 1:
+            import torch.distributed as dist
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            dist.all_reduce(hits)  # the one NCCL collective of the workload (uint64 sum)
+            t1.record(stream)
+            torch.cuda.synchronize()
+            hits_v = int(hits.item())
+            result["allreduce_ms"] = t0.elapsed_time(t1)
+        samples = (args.steps + args.warmup) * (1 << 40)
+        result["mc"] = {"hits": hits_v, "samples": samples, "pi_estimate": 4.0 * hits_v / samples,
+                        "kernel_ms_mean": kern_ms}
+        result["roofline"] = {"bound": "int-issue", "achieved": value / world, "peak": None,
+                              "unit": "RN/s per GPU", "frac": None, "traffic": load_traffic(wl)}
+
+    # e2e through the public host API (generate into pinned host memory)
+    if not args.no_e2e and wl == "fill_u32":
+        host = torch.empty((count, per), dtype=torch.uint32, pin_memory=True)
+        e2e_steps = max(3, min(args.steps, 5))
+        for _ in range(1):
+            ens.generate_into_host(per, host)
+        barrier(world)
+        t = time.perf_counter()
+        for _ in range(e2e_steps):
+            ens.generate_into_host(per, host)
+        dt = max_over_ranks(time.perf_counter() - t, world)
+        result["e2e"] = {"value": words_per_step * world * e2e_steps / dt, "unit": "RN/s",
+                         "h2d_bytes_per_step": 0, "d2h_bytes_per_step": words_per_step * 4,
+                         "api": "BlockEnsemble.generate -> xg_generate_host (pinned host buffer)",
+                         "steps": e2e_steps}
+        del host
+    if rank == 0 and world == 1 and not args.no_cpu and wl in ("fill_u32", "fill_f32", "fill_f64"):
+        try:
+            result["cpu_baseline"] = reference_rate(1 << 14, 1 << 13, trials=5, budget_s=30.0)
+            for k in ("trials", "min", "max"):
+                result["cpu_baseline"].pop(k, None)
+        except Exception as e:  # noqa: BLE001
+            result["cpu_baseline"] = {"value": None, "unavailable": str(e)}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,169 @@
+/*
+ * xg_gpu.h -- C ABI of the B200-native xorgensGP generator (libxg_gpu.so).
+ *
+ * A drop-in for the reference CPU library's generation path.  Each entry point
+ * names the reference interface it replaces (paths relative to the reference
+ * tree).  Plain C types only: no C++, no CUDA or torch headers are needed to
+ * call it.  `xg_stream_t` is ABI-identical to `cudaStream_t`
+ * (`struct CUstream_st*`); NULL means the legacy default stream.
+ *
+ * All generation calls are asynchronous on the caller's stream and write to
+ * caller-owned device memory, except xg_generate_host / xg_next_* /
+ * xg_state_export / xg_state_import, which synchronise.
+ *
+ * Error model (no exceptions cross the ABI):
+ *   XG_OK                    success
+ *   1..6                     1 + ParamError ordinal, same check order as
+ *                            xg::check_params (proj/src/params.cpp:22-37)
+ *   XG_ERANGE                std::out_of_range in the reference (lanes outside
+ *                            [1, lane_bound], zero streams, stream index)
+ *   XG_EINVAL                std::invalid_argument (NULL / misaligned buffer,
+ *                            size overflow, wrong handle kind)
+ *   XG_EUNSUPPORTED          valid parameters the GPU path does not implement
+ *                            (it needs w = 32, r = 128, lane_bound >= 32)
+ *   XG_ECUDA / XG_ENOMEM     CUDA runtime failure / device allocation failure
+ */
+#ifndef XG_GPU_H
+#define XG_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* xg_stream_t;
+typedef struct xg_ensemble* xg_ensemble_t;
+
+enum {
+    XG_OK = 0,
+    XG_EPARAM_BAD_WORD_SIZE = 1,       /* ParamError::bad_word_size */
+    XG_EPARAM_S_OUT_OF_RANGE = 2,      /* ParamError::s_out_of_range */
+    XG_EPARAM_GCD_NOT_ONE = 3,         /* ParamError::gcd_not_one */
+    XG_EPARAM_SHIFT_OUT_OF_RANGE = 4,  /* ParamError::shift_out_of_range */
+    XG_EPARAM_GAMMA_OUT_OF_RANGE = 5,  /* ParamError::gamma_out_of_range */
+    XG_EPARAM_EVEN_WEYL_INCREMENT = 6, /* ParamError::even_weyl_increment */
+    XG_ERANGE = 16,
+    XG_EINVAL = 17,
+    XG_EUNSUPPORTED = 18,
+    XG_ECUDA = 19,
+    XG_ENOMEM = 20
+};
+
+/* GeneratorParams, same field order and meaning
+ * (proj/include/xg/params.hpp:17-29). */
+typedef struct {
+    unsigned r, s, a, b, c, d, w;
+    uint64_t omega;
+    unsigned gamma;
+} xg_params_t;
+
+/* ---- parameters (host only, no GPU needed) ------------------------------ */
+
+/* check_params (proj/include/xg/params.hpp:52, proj/src/params.cpp:22-37):
+ * XG_OK or 1 + ParamError. */
+int xg_params_check(const xg_params_t* p);
+/* to_string(ParamError) (proj/src/params.cpp:7-18) and the ABI codes. */
+const char* xg_strerror(int code);
+/* lane_bound (proj/include/xg/params.hpp:59-61): min(s, r - s). */
+unsigned xg_lane_bound(const xg_params_t* p);
+/* recommended_weyl_increment (proj/src/params.cpp:53-62); 0 for a bad w
+ * (the reference throws ParamValidationError(bad_word_size)). */
+uint64_t xg_recommended_weyl_increment(unsigned w);
+/* default_output_shift (proj/include/xg/params.hpp:77). */
+unsigned xg_default_output_shift(unsigned w);
+/* Shipped sets (proj/src/params.cpp:83-86). */
+xg_params_t xg_params_xorgensgp32(void);
+xg_params_t xg_params_tiny_r2w8(void);
+xg_params_t xg_params_tiny_r2w16(void);
+xg_params_t xg_params_tiny_r4w16(void);
+/* XG_OK when the GPU kernels implement `p`, else the check_params code or
+ * XG_EUNSUPPORTED. */
+int xg_gpu_supported(const xg_params_t* p);
+
+/* ---- ensembles ----------------------------------------------------------- */
+
+/* BlockEnsemble(params, base_seed, num_blocks, lanes)
+ * (proj/include/xg/parallel.hpp:35-40, proj/src/parallel.cpp:84-95) plus the
+ * seeding constructor XorgensState(params, seed) (proj/src/xorgens.cpp:19-32)
+ * for every block, run on the device.  Stream g of the handle is seeded with
+ * base_seed + first_stream + g (uint64 wrap); first_stream lets a multi-GPU
+ * job give each device a disjoint slice of one global ensemble.  `lanes` is
+ * validated like the reference (XG_ERANGE unless 1 <= lanes <= lane_bound);
+ * the output never depends on it. */
+int xg_ensemble_create(const xg_params_t* p, uint64_t base_seed, uint64_t first_stream,
+                       uint32_t num_streams, unsigned lanes, int device, xg_stream_t stream,
+                       xg_ensemble_t* out);
+/* XorgensState::from_raw (proj/include/xg/xorgens.hpp:33-35,
+ * proj/src/xorgens.cpp:34-38) for num_streams streams: buffers holds
+ * num_streams * r words, each stream's r most recent values oldest first;
+ * words are masked to w bits, no warm-up, no zero check. */
+int xg_ensemble_create_from_raw(const xg_params_t* p, uint32_t num_streams,
+                                const uint64_t* buffers, const uint64_t* weyls, int device,
+                                xg_stream_t stream, xg_ensemble_t* out);
+int xg_ensemble_destroy(xg_ensemble_t h);
+/* num_blocks() / base_seed() / lanes() (proj/include/xg/parallel.hpp:49-51). */
+int xg_ensemble_info(xg_ensemble_t h, uint32_t* num_streams, uint64_t* base_seed,
+                     uint64_t* first_stream, unsigned* lanes, int* device);
+
+/* ---- generation (device buffers, asynchronous) --------------------------- */
+
+/* BlockEnsemble::generate(per_block) (proj/src/parallel.cpp:97-135):
+ * dev_out[g * per_stream + k] = word k of stream g, continuing each stream
+ * from the handle's state (a second call continues where the first stopped).
+ * Byte-identical to `xgen gen --format raw-le --blocks`
+ * (proj/tools/xgen.cpp:51-57,94-98). */
+int xg_fill_u32(xg_ensemble_t h, uint64_t per_stream, uint32_t* dev_out, xg_stream_t stream);
+/* Two consecutive words per value, lo = first: value = w[2k] | w[2k+1] << 32
+ * (the raw-le stream read as little-endian uint64).  Not in the reference. */
+int xg_fill_u64(xg_ensemble_t h, uint64_t per_stream, uint64_t* dev_out, xg_stream_t stream);
+/* Uniform [0,1): f32 = (word >> 8) * 2^-24, one word per value.  Exact. */
+int xg_fill_f32(xg_ensemble_t h, uint64_t per_stream, float* dev_out, xg_stream_t stream);
+/* Uniform [0,1): f64 = (u64 >> 11) * 2^-53 with u64 as in xg_fill_u64. Exact. */
+int xg_fill_f64(xg_ensemble_t h, uint64_t per_stream, double* dev_out, xg_stream_t stream);
+/* Fused Monte Carlo pi: sample j of a stream uses words (2j, 2j+1) as
+ * x = w >> 8, y = w' >> 8 and hits iff x^2 + y^2 < 2^48.  The hit count over
+ * all streams is ADDED to *dev_hits (a device uint64).  No HBM traffic. */
+int xg_mc_pi(xg_ensemble_t h, uint64_t samples_per_stream, uint64_t* dev_hits,
+             xg_stream_t stream);
+/* Advance every stream by `words` without storing (discard). */
+int xg_skip(xg_ensemble_t h, uint64_t words, xg_stream_t stream);
+
+/* ---- host-facing calls (synchronise) -------------------------------------- */
+
+/* BlockEnsemble::generate into HOST memory: same layout as xg_fill_u32,
+ * generated in stream chunks and copied device->host with the copies
+ * overlapping generation.  host_out should be pinned for full speed. */
+int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,
+                     xg_stream_t stream);
+/* XorgensState::next_word (proj/include/xg/xorgens.hpp:58-62) on a
+ * one-stream handle, served from device-generated refills; interleaving with
+ * fills / exports keeps the exact serial stream. */
+int xg_next_u32(xg_ensemble_t h, uint32_t* out);
+/* Two next_u32 values, lo = first. */
+int xg_next_u64(xg_ensemble_t h, uint64_t* out);
+/* logical_buffer() + weyl_value() of stream `index`
+ * (proj/include/xg/xorgens.hpp:72-76): r words oldest first. */
+int xg_state_export(xg_ensemble_t h, uint32_t index, uint64_t* buffer, uint64_t* weyl);
+/* Replace stream `index` with from_raw(params, buffer, weyl). */
+int xg_state_import(xg_ensemble_t h, uint32_t index, const uint64_t* buffer, uint64_t weyl);
+
+/* ---- multi-GPU partitioner (host only) ----------------------------------- */
+
+/* Contiguous, balanced split of global streams [0, total) over `world`
+ * devices: rank k gets [floor(k*total/world), floor((k+1)*total/world)).
+ * Mirrors the block striping of proj/src/parallel.cpp:115-134 lifted to
+ * devices; the union of all ranks' fills is the single-device fill. */
+int xg_partition(uint64_t total_streams, uint32_t world, uint32_t rank, uint64_t* first,
+                 uint32_t* count);
+
+/* Launch bookkeeping: number of kernels this library has launched since load
+ * (bench.py reports it as gpu_launches). */
+uint64_t xg_kernel_launches(void);
+const char* xg_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XG_GPU_H */

@@ -1,0 +1,158 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A C entry layer over the UNMODIFIED reference sources
+// (proj/src/{params,xorgens,parallel}.cpp, compiled where they lie by
+// oracle/Makefile into oracle/_ref/libxgref.so).  Used (1) to pin the C
+// restatement in oracle/xg_oracle.c and to generate tests/golden fixtures, and
+// (2) as bench.py's reference arm / cpu_baseline (cpu_baseline.kind
+// "reference").  Nothing here re-implements generator arithmetic: every value
+// comes out of xg::XorgensState / xg::batch_step / xg::BlockEnsemble.
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <ctime>
+#include <exception>
+#include <stdexcept>
+#include <vector>
+
+#include "xg/params.hpp"
+#include "xg/parallel.hpp"
+#include "xg/xorgens.hpp"
+
+namespace {
+
+xg::GeneratorParams to_params(const unsigned* rsabcdw, std::uint64_t omega, unsigned gamma) {
+    xg::GeneratorParams p;
+    p.r = rsabcdw[0];
+    p.s = rsabcdw[1];
+    p.a = rsabcdw[2];
+    p.b = rsabcdw[3];
+    p.c = rsabcdw[4];
+    p.d = rsabcdw[5];
+    p.w = rsabcdw[6];
+    p.omega = omega;
+    p.gamma = gamma;
+    return p;
+}
+
+double thread_cpu_seconds() {
+    timespec ts;
+    clock_gettime(CLOCK_THREAD_CPUTIME_ID, &ts);
+    return static_cast<double>(ts.tv_sec) + static_cast<double>(ts.tv_nsec) * 1e-9;
+}
+
+} // namespace
+
+extern "C" {
+
+// check_params: 0 or 1 + ParamError ordinal.
+int xgref_check_params(const unsigned* rsabcdw, std::uint64_t omega, unsigned gamma) {
+    auto e = xg::check_params(to_params(rsabcdw, omega, gamma));
+    return e ? 1 + static_cast<int>(*e) : 0;
+}
+
+// XorgensState(params, seed).next_word() x n.
+int xgref_stream(const unsigned* rsabcdw, std::uint64_t omega, unsigned gamma,
+                 std::uint64_t seed, std::uint64_t n, std::uint64_t* out) {
+    try {
+        xg::XorgensState st(to_params(rsabcdw, omega, gamma), seed);
+        for (std::uint64_t k = 0; k < n; ++k)
+            out[k] = st.next_word();
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// State right after seeding: logical buffer (oldest first) + weyl.
+int xgref_seeded_state(const unsigned* rsabcdw, std::uint64_t omega, unsigned gamma,
+                       std::uint64_t seed, std::uint64_t* buffer, std::uint64_t* weyl) {
+    try {
+        xg::XorgensState st(to_params(rsabcdw, omega, gamma), seed);
+        auto lb = st.logical_buffer();
+        std::memcpy(buffer, lb.data(), lb.size() * sizeof(std::uint64_t));
+        *weyl = st.weyl_value();
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// from_raw(params, buffer, weyl).next_word() x n.
+int xgref_from_raw_stream(const unsigned* rsabcdw, std::uint64_t omega, unsigned gamma,
+                          const std::uint64_t* buffer, std::uint64_t weyl, std::uint64_t n,
+                          std::uint64_t* out) {
+    try {
+        auto p = to_params(rsabcdw, omega, gamma);
+        std::vector<std::uint64_t> buf(buffer, buffer + p.r);
+        auto st = xg::XorgensState::from_raw(p, buf, weyl);
+        for (std::uint64_t k = 0; k < n; ++k)
+            out[k] = st.next_word();
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// ---- BlockEnsemble handle (proj/src/parallel.cpp:84-135) -----------------
+
+void* xgref_ensemble_create(const unsigned* rsabcdw, std::uint64_t omega, unsigned gamma,
+                            std::uint64_t base_seed, unsigned num_blocks, unsigned lanes) {
+    try {
+        return new xg::BlockEnsemble(to_params(rsabcdw, omega, gamma), base_seed, num_blocks,
+                                     lanes);
+    } catch (const std::exception&) {
+        return nullptr;
+    }
+}
+
+void xgref_ensemble_destroy(void* h) { delete static_cast<xg::BlockEnsemble*>(h); }
+
+// generate(per_block, workers); the wall time of generate() alone is
+// returned in *seconds (measure_ensemble_throughput, proj/src/bench.cpp:95-112).
+// If out != nullptr the block-major words are copied out as uint32.
+int xgref_ensemble_generate(void* h, std::uint64_t per_block, unsigned workers,
+                            std::uint32_t* out, double* seconds, std::uint64_t* xor_sink) {
+    try {
+        auto* e = static_cast<xg::BlockEnsemble*>(h);
+        auto t0 = std::chrono::steady_clock::now();
+        auto blocks = e->generate(per_block, workers);
+        std::chrono::duration<double> dt = std::chrono::steady_clock::now() - t0;
+        if (seconds) *seconds = dt.count();
+        std::uint64_t sink = 0;
+        std::size_t pos = 0;
+        for (const auto& b : blocks)
+            for (std::uint64_t w : b) {
+                sink ^= w;
+                if (out) out[pos] = static_cast<std::uint32_t>(w);
+                ++pos;
+            }
+        if (xor_sink) *xor_sink = sink;
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// Serial next_word throughput, the measure_throughput method
+// (proj/src/bench.cpp:67-93): best chunk rate on thread CPU time.
+double xgref_serial_rate(std::uint64_t seed, std::uint64_t count, unsigned chunks,
+                         std::uint64_t* sink_out) {
+    xg::XorgensState st(xg::xorgensgp32_params(), seed);
+    std::uint64_t sink = 0, produced = 0;
+    const std::uint64_t chunk = count / chunks;
+    double best = 0.0;
+    for (unsigned c = 0; c < chunks; ++c) {
+        const std::uint64_t n = (c == chunks - 1) ? count - produced : chunk;
+        const double t0 = thread_cpu_seconds();
+        for (std::uint64_t i = 0; i < n; ++i)
+            sink ^= st.next_word();
+        const double dt = thread_cpu_seconds() - t0;
+        produced += n;
+        if (dt > 0.0 && static_cast<double>(n) / dt > best) best = static_cast<double>(n) / dt;
+    }
+    if (sink_out) *sink_out = sink;
+    return best;
+}
+
+} // extern "C"

@@ -1,0 +1,585 @@
+// xg_gpu.cu -- host side of libxg_gpu.so: the C ABI declared in
+// include/xg_gpu.h over the sm_100a kernels in xg_kernels.cuh.
+//
+// Host validation mirrors the reference exactly (check order and error
+// classes of proj/src/params.cpp:22-37 and proj/src/parallel.cpp:84-95); all
+// generator arithmetic runs on the device.  There is no CPU fallback: a call
+// without a usable CUDA device returns XG_ECUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <numeric>
+#include <vector>
+
+#include "xg_gpu.h"
+#include "xg_kernels.cuh"
+
+using namespace xgk;
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+
+constexpr uint32_t kMask32 = 0xffffffffu;
+constexpr size_t kNextBuf = 1u << 14;  // words per next_u32 refill
+
+enum Kind { kGP32 = 0, kRtJ1 = 1, kRtJ2 = 2 };
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+struct xg_ensemble {
+    xg_params_t params{};
+    Kind kind = kGP32;
+    int device = 0;
+    uint32_t num_streams = 0;
+    uint64_t base_seed = 0, first_stream = 0;
+    unsigned lanes = 0;
+    uint32_t* d_win = nullptr;   // [num_streams][128] logical window, oldest first
+    uint32_t* d_weyl = nullptr;  // [num_streams] Weyl accumulator
+    // next_u32 service (one-stream handles)
+    std::vector<uint32_t> nbuf;
+    size_t npos = 0;
+    uint32_t* d_snap = nullptr;  // 129-word state snapshot taken before a refill
+    uint32_t* d_scratch = nullptr;
+    // xg_generate_host staging
+    uint32_t* d_stage = nullptr;
+    size_t stage_words = 0;
+};
+
+namespace {
+
+int check_params_impl(const xg_params_t* p) {
+    if (!p) return XG_EINVAL;
+    if (p->w != 8 && p->w != 16 && p->w != 32 && p->w != 64) return XG_EPARAM_BAD_WORD_SIZE;
+    if (p->s == 0 || p->s >= p->r) return XG_EPARAM_S_OUT_OF_RANGE;
+    if (std::gcd(p->r, p->s) != 1u) return XG_EPARAM_GCD_NOT_ONE;
+    for (unsigned sh : {p->a, p->b, p->c, p->d})
+        if (sh == 0 || sh >= p->w) return XG_EPARAM_SHIFT_OUT_OF_RANGE;
+    if (p->gamma == 0 || p->gamma >= p->w) return XG_EPARAM_GAMMA_OUT_OF_RANGE;
+    if ((p->omega & 1u) == 0) return XG_EPARAM_EVEN_WEYL_INCREMENT;
+    return XG_OK;
+}
+
+unsigned lane_bound_impl(const xg_params_t* p) {
+    return p->s < p->r - p->s ? p->s : p->r - p->s;
+}
+
+bool is_gp32(const xg_params_t* p) {
+    return p->r == 128 && p->s == 65 && p->a == 15 && p->b == 14 && p->c == 12 &&
+           p->d == 17 && p->w == 32 && p->omega == 2654435769ull && p->gamma == 16;
+}
+
+int classify(const xg_params_t* p, Kind* kind) {
+    int e = check_params_impl(p);
+    if (e) return e;
+    if (p->w != 32 || p->r != kR || lane_bound_impl(p) < 32) return XG_EUNSUPPORTED;
+    if (is_gp32(p)) {
+        *kind = kGP32;
+    } else {
+        const unsigned q = p->r - p->s;  // odd, 33..95
+        *kind = (q / 32 == 1) ? kRtJ1 : kRtJ2;
+    }
+    return XG_OK;
+}
+
+template <int J>
+RtParams<J> rt_params(const xg_params_t& p) {
+    RtParams<J> r;
+    r.delta = (p.r - p.s) % 32;
+    r.a = p.a;
+    r.b = p.b;
+    r.c = p.c;
+    r.d = p.d;
+    r.gamma = p.gamma;
+    r.omega = static_cast<uint32_t>(p.omega & kMask32);
+    return r;
+}
+
+int cuda_rc(cudaError_t e) {
+    if (e == cudaSuccess) return XG_OK;
+    if (e == cudaErrorMemoryAllocation) return XG_ENOMEM;
+    return XG_ECUDA;
+}
+
+unsigned grid_for(uint32_t n) { return (n + kWarpsPerBlock - 1) / kWarpsPerBlock; }
+
+template <int MODE, class P>
+int launch_fill_p(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count,
+                  uint64_t words, void* out, unsigned long long* hits, cudaStream_t s) {
+    fill_kernel<P, MODE><<<grid_for(g_count), kThreads, 0, s>>>(p, h->d_win, h->d_weyl, g_begin,
+                                                                g_count, words, out, hits);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cuda_rc(cudaGetLastError());
+}
+
+template <int MODE>
+int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t words, void* out,
+                unsigned long long* hits, cudaStream_t s) {
+    if (words == 0 || g_count == 0) return XG_OK;
+    switch (h->kind) {
+    case kGP32: return launch_fill_p<MODE>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+    case kRtJ1: return launch_fill_p<MODE>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s);
+    default: return launch_fill_p<MODE>(rt_params<2>(h->params), h, g_begin, g_count, words, out, hits, s);
+    }
+}
+
+int launch_seed(xg_ensemble* h, uint64_t seed0, cudaStream_t s) {
+    const unsigned grid = grid_for(h->num_streams);
+    switch (h->kind) {
+    case kGP32:
+        seed_kernel<<<grid, kThreads, 0, s>>>(GP32{}, h->d_win, h->d_weyl, h->num_streams, seed0);
+        break;
+    case kRtJ1:
+        seed_kernel<<<grid, kThreads, 0, s>>>(rt_params<1>(h->params), h->d_win, h->d_weyl,
+                                             h->num_streams, seed0);
+        break;
+    default:
+        seed_kernel<<<grid, kThreads, 0, s>>>(rt_params<2>(h->params), h->d_win, h->d_weyl,
+                                             h->num_streams, seed0);
+        break;
+    }
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cuda_rc(cudaGetLastError());
+}
+
+int alloc_state(xg_ensemble* h) {
+    const size_t n = static_cast<size_t>(h->num_streams);
+    int rc = cuda_rc(cudaMalloc(&h->d_win, n * kR * sizeof(uint32_t)));
+    if (rc) return rc;
+    return cuda_rc(cudaMalloc(&h->d_weyl, n * sizeof(uint32_t)));
+}
+
+void free_handle(xg_ensemble* h) {
+    if (!h) return;
+    {
+        DeviceGuard dg(h->device);
+        cudaFree(h->d_win);
+        cudaFree(h->d_weyl);
+        cudaFree(h->d_snap);
+        cudaFree(h->d_scratch);
+        cudaFree(h->d_stage);
+    }
+    delete h;
+}
+
+// Buffered next_u32 words that were generated but not served are given back:
+// restore the pre-refill snapshot and re-advance by the served count, so the
+// device state is exactly "after the last word the caller saw".
+int settle_next(xg_ensemble* h, cudaStream_t s) {
+    if (h->nbuf.empty()) return XG_OK;
+    const size_t served = h->npos, held = h->nbuf.size();
+    h->nbuf.clear();
+    h->npos = 0;
+    if (served == held) return XG_OK;
+    int rc = cuda_rc(cudaMemcpyAsync(h->d_win, h->d_snap, kR * sizeof(uint32_t),
+                                     cudaMemcpyDeviceToDevice, s));
+    if (rc) return rc;
+    rc = cuda_rc(cudaMemcpyAsync(h->d_weyl, h->d_snap + kR, sizeof(uint32_t),
+                                 cudaMemcpyDeviceToDevice, s));
+    if (rc) return rc;
+    return launch_fill<kSkip>(h, 0, 1, served, nullptr, nullptr, s);
+}
+
+bool mul_overflows(uint64_t a, uint64_t b, uint64_t* out) {
+    return __builtin_mul_overflow(a, b, out);
+}
+
+int fill_common(xg_ensemble_t h, uint64_t per_stream, void* dev_out, size_t align, int mode,
+                xg_stream_t stream) {
+    if (!h) return XG_EINVAL;
+    uint64_t total;
+    if (mul_overflows(per_stream, h->num_streams, &total)) return XG_EINVAL;
+    if (per_stream == 0) return XG_OK;
+    if (!dev_out || (reinterpret_cast<uintptr_t>(dev_out) % align) != 0) return XG_EINVAL;
+    DeviceGuard dg(h->device);
+    if (!dg.ok) return XG_ECUDA;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = settle_next(h, s);
+    if (rc) return rc;
+    switch (mode) {
+    case kU32: return launch_fill<kU32>(h, 0, h->num_streams, per_stream, dev_out, nullptr, s);
+    case kF32: return launch_fill<kF32>(h, 0, h->num_streams, per_stream, dev_out, nullptr, s);
+    case kF64: {
+        uint64_t words;
+        if (mul_overflows(per_stream, 2, &words)) return XG_EINVAL;
+        return launch_fill<kF64>(h, 0, h->num_streams, words, dev_out, nullptr, s);
+    }
+    default: return XG_EINVAL;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int xg_params_check(const xg_params_t* p) { return check_params_impl(p); }
+
+const char* xg_strerror(int code) {
+    switch (code) {
+    case XG_OK: return "ok";
+    // proj/src/params.cpp:7-18
+    case XG_EPARAM_BAD_WORD_SIZE: return "word size must be 8, 16, 32 or 64";
+    case XG_EPARAM_S_OUT_OF_RANGE: return "tap offset s must satisfy 0 < s < r";
+    case XG_EPARAM_GCD_NOT_ONE: return "r and s must be coprime";
+    case XG_EPARAM_SHIFT_OUT_OF_RANGE: return "shifts a, b, c, d must lie in (0, w)";
+    case XG_EPARAM_GAMMA_OUT_OF_RANGE: return "output shift gamma must lie in (0, w)";
+    case XG_EPARAM_EVEN_WEYL_INCREMENT: return "Weyl increment omega must be odd";
+    case XG_ERANGE: return "argument out of range";
+    case XG_EINVAL: return "invalid argument";
+    case XG_EUNSUPPORTED: return "parameters not supported by the GPU path (needs w=32, r=128, lane_bound>=32)";
+    case XG_ECUDA: return "CUDA runtime error";
+    case XG_ENOMEM: return "device memory allocation failed";
+    default: return "unknown error";
+    }
+}
+
+unsigned xg_lane_bound(const xg_params_t* p) { return p ? lane_bound_impl(p) : 0u; }
+
+uint64_t xg_recommended_weyl_increment(unsigned w) {
+    switch (w) {
+    case 8: return 159u;
+    case 16: return 40503u;
+    case 32: return 2654435769ull;
+    case 64: return 11400714819323198485ull;
+    default: return 0;
+    }
+}
+
+unsigned xg_default_output_shift(unsigned w) { return w / 2; }
+
+static xg_params_t make_set(unsigned r, unsigned s, unsigned a, unsigned b, unsigned c, unsigned d,
+                            unsigned w) {
+    xg_params_t p;
+    p.r = r; p.s = s; p.a = a; p.b = b; p.c = c; p.d = d; p.w = w;
+    p.omega = xg_recommended_weyl_increment(w);
+    p.gamma = xg_default_output_shift(w);
+    return p;
+}
+
+xg_params_t xg_params_xorgensgp32(void) { return make_set(128, 65, 15, 14, 12, 17, 32); }
+xg_params_t xg_params_tiny_r2w8(void) { return make_set(2, 1, 1, 1, 5, 7, 8); }
+xg_params_t xg_params_tiny_r2w16(void) { return make_set(2, 1, 1, 1, 6, 11, 16); }
+xg_params_t xg_params_tiny_r4w16(void) { return make_set(4, 3, 1, 2, 5, 8, 16); }
+
+int xg_gpu_supported(const xg_params_t* p) {
+    Kind k;
+    return classify(p, &k);
+}
+
+int xg_ensemble_create(const xg_params_t* p, uint64_t base_seed, uint64_t first_stream,
+                       uint32_t num_streams, unsigned lanes, int device, xg_stream_t stream,
+                       xg_ensemble_t* out) {
+    if (!out) return XG_EINVAL;
+    *out = nullptr;
+    // proj/src/parallel.cpp:86-91: validate_params, then blocks, then lanes.
+    int e = check_params_impl(p);
+    if (e) return e;
+    if (num_streams == 0) return XG_ERANGE;
+    if (lanes == 0 || lanes > lane_bound_impl(p)) return XG_ERANGE;
+    Kind kind;
+    e = classify(p, &kind);
+    if (e) return e;
+    DeviceGuard dg(device);
+    if (!dg.ok) return XG_ECUDA;
+    auto* h = new (std::nothrow) xg_ensemble;
+    if (!h) return XG_ENOMEM;
+    h->params = *p;
+    h->kind = kind;
+    h->device = device;
+    h->num_streams = num_streams;
+    h->base_seed = base_seed;
+    h->first_stream = first_stream;
+    h->lanes = lanes;
+    int rc = alloc_state(h);
+    if (!rc) rc = launch_seed(h, base_seed + first_stream, reinterpret_cast<cudaStream_t>(stream));
+    if (rc) {
+        free_handle(h);
+        return rc;
+    }
+    *out = h;
+    return XG_OK;
+}
+
+int xg_ensemble_create_from_raw(const xg_params_t* p, uint32_t num_streams,
+                                const uint64_t* buffers, const uint64_t* weyls, int device,
+                                xg_stream_t stream, xg_ensemble_t* out) {
+    if (!out) return XG_EINVAL;
+    *out = nullptr;
+    int e = check_params_impl(p);
+    if (e) return e;
+    if (num_streams == 0) return XG_ERANGE;
+    if (!buffers || !weyls) return XG_EINVAL;
+    Kind kind;
+    e = classify(p, &kind);
+    if (e) return e;
+    DeviceGuard dg(device);
+    if (!dg.ok) return XG_ECUDA;
+    auto* h = new (std::nothrow) xg_ensemble;
+    if (!h) return XG_ENOMEM;
+    h->params = *p;
+    h->kind = kind;
+    h->device = device;
+    h->num_streams = num_streams;
+    h->lanes = lane_bound_impl(p);
+    int rc = alloc_state(h);
+    if (!rc) {
+        std::vector<uint32_t> win(static_cast<size_t>(num_streams) * kR), wy(num_streams);
+        for (size_t i = 0; i < win.size(); ++i) win[i] = static_cast<uint32_t>(buffers[i] & kMask32);
+        for (size_t i = 0; i < wy.size(); ++i) wy[i] = static_cast<uint32_t>(weyls[i] & kMask32);
+        cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+        rc = cuda_rc(cudaMemcpyAsync(h->d_win, win.data(), win.size() * 4, cudaMemcpyHostToDevice, s));
+        if (!rc) rc = cuda_rc(cudaMemcpyAsync(h->d_weyl, wy.data(), wy.size() * 4, cudaMemcpyHostToDevice, s));
+        if (!rc) rc = cuda_rc(cudaStreamSynchronize(s));
+    }
+    if (rc) {
+        free_handle(h);
+        return rc;
+    }
+    *out = h;
+    return XG_OK;
+}
+
+int xg_ensemble_destroy(xg_ensemble_t h) {
+    if (!h) return XG_EINVAL;
+    free_handle(h);
+    return XG_OK;
+}
+
+int xg_ensemble_info(xg_ensemble_t h, uint32_t* num_streams, uint64_t* base_seed,
+                     uint64_t* first_stream, unsigned* lanes, int* device) {
+    if (!h) return XG_EINVAL;
+    if (num_streams) *num_streams = h->num_streams;
+    if (base_seed) *base_seed = h->base_seed;
+    if (first_stream) *first_stream = h->first_stream;
+    if (lanes) *lanes = h->lanes;
+    if (device) *device = h->device;
+    return XG_OK;
+}
+
+int xg_fill_u32(xg_ensemble_t h, uint64_t per_stream, uint32_t* dev_out, xg_stream_t stream) {
+    return fill_common(h, per_stream, dev_out, 4, kU32, stream);
+}
+
+int xg_fill_u64(xg_ensemble_t h, uint64_t per_stream, uint64_t* dev_out, xg_stream_t stream) {
+    uint64_t words;
+    if (mul_overflows(per_stream, 2, &words)) return XG_EINVAL;
+    if (reinterpret_cast<uintptr_t>(dev_out) % 8 != 0) return XG_EINVAL;
+    // Little-endian: (lo, hi) word pairs are exactly the uint64 values.
+    return fill_common(h, words, dev_out, 8, kU32, stream);
+}
+
+int xg_fill_f32(xg_ensemble_t h, uint64_t per_stream, float* dev_out, xg_stream_t stream) {
+    return fill_common(h, per_stream, dev_out, 4, kF32, stream);
+}
+
+int xg_fill_f64(xg_ensemble_t h, uint64_t per_stream, double* dev_out, xg_stream_t stream) {
+    return fill_common(h, per_stream, dev_out, 8, kF64, stream);
+}
+
+int xg_mc_pi(xg_ensemble_t h, uint64_t samples_per_stream, uint64_t* dev_hits,
+             xg_stream_t stream) {
+    if (!h || !dev_hits || (reinterpret_cast<uintptr_t>(dev_hits) % 8) != 0) return XG_EINVAL;
+    if (samples_per_stream == 0) return XG_OK;
+    DeviceGuard dg(h->device);
+    if (!dg.ok) return XG_ECUDA;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = settle_next(h, s);
+    if (rc) return rc;
+    // Per-lane hit counters are 32-bit: bound samples per launch to 2^36.
+    constexpr uint64_t kChunk = 1ull << 36;
+    uint64_t left = samples_per_stream;
+    while (left) {
+        const uint64_t n = std::min(left, kChunk);
+        rc = launch_fill<kMC>(h, 0, h->num_streams, 2 * n, nullptr,
+                              reinterpret_cast<unsigned long long*>(dev_hits), s);
+        if (rc) return rc;
+        left -= n;
+    }
+    return XG_OK;
+}
+
+int xg_skip(xg_ensemble_t h, uint64_t words, xg_stream_t stream) {
+    if (!h) return XG_EINVAL;
+    if (words == 0) return XG_OK;
+    DeviceGuard dg(h->device);
+    if (!dg.ok) return XG_ECUDA;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = settle_next(h, s);
+    if (rc) return rc;
+    return launch_fill<kSkip>(h, 0, h->num_streams, words, nullptr, nullptr, s);
+}
+
+int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,
+                     xg_stream_t stream) {
+    if (!h) return XG_EINVAL;
+    uint64_t total;
+    if (mul_overflows(per_stream, h->num_streams, &total)) return XG_EINVAL;
+    if (per_stream == 0) return XG_OK;
+    if (!host_out) return XG_EINVAL;
+    DeviceGuard dg(h->device);
+    if (!dg.ok) return XG_ECUDA;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = settle_next(h, s);
+    if (rc) return rc;
+    // Two staging slots of up to 64 Mi words; chunk i is generated on `s`
+    // while chunk i-1 is copied on a second stream.
+    constexpr uint64_t kSlotWords = 1ull << 26;
+    uint64_t streams_per_chunk = std::max<uint64_t>(1, kSlotWords / per_stream);
+    streams_per_chunk = std::min<uint64_t>(streams_per_chunk, h->num_streams);
+    const uint64_t slot_words = streams_per_chunk * per_stream;
+    if (h->stage_words < 2 * slot_words) {
+        cudaFree(h->d_stage);
+        h->d_stage = nullptr;
+        h->stage_words = 0;
+        rc = cuda_rc(cudaMalloc(&h->d_stage, 2 * slot_words * sizeof(uint32_t)));
+        if (rc) return rc;
+        h->stage_words = 2 * slot_words;
+    }
+    cudaStream_t cs;
+    rc = cuda_rc(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    if (rc) return rc;
+    cudaEvent_t gen_done[2], copy_done[2];
+    for (int i = 0; i < 2; ++i) {
+        cudaEventCreateWithFlags(&gen_done[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&copy_done[i], cudaEventDisableTiming);
+        cudaEventRecord(copy_done[i], cs);
+    }
+    uint32_t g = 0;
+    int slot = 0;
+    while (g < h->num_streams && !rc) {
+        const uint32_t cnt = static_cast<uint32_t>(
+            std::min<uint64_t>(streams_per_chunk, h->num_streams - g));
+        uint32_t* d = h->d_stage + slot * slot_words;
+        cudaStreamWaitEvent(s, copy_done[slot], 0);
+        rc = launch_fill<kU32>(h, g, cnt, per_stream, d, nullptr, s);
+        if (rc) break;
+        cudaEventRecord(gen_done[slot], s);
+        cudaStreamWaitEvent(cs, gen_done[slot], 0);
+        rc = cuda_rc(cudaMemcpyAsync(host_out + static_cast<size_t>(g) * per_stream, d,
+                                     static_cast<size_t>(cnt) * per_stream * sizeof(uint32_t),
+                                     cudaMemcpyDeviceToHost, cs));
+        cudaEventRecord(copy_done[slot], cs);
+        g += cnt;
+        slot ^= 1;
+    }
+    const int rc2 = cuda_rc(cudaStreamSynchronize(cs));
+    const int rc3 = cuda_rc(cudaStreamSynchronize(s));
+    for (int i = 0; i < 2; ++i) {
+        cudaEventDestroy(gen_done[i]);
+        cudaEventDestroy(copy_done[i]);
+    }
+    cudaStreamDestroy(cs);
+    return rc ? rc : (rc2 ? rc2 : rc3);
+}
+
+int xg_next_u32(xg_ensemble_t h, uint32_t* out) {
+    if (!h || !out) return XG_EINVAL;
+    if (h->num_streams != 1) return XG_EINVAL;
+    if (h->npos < h->nbuf.size()) {
+        *out = h->nbuf[h->npos++];
+        return XG_OK;
+    }
+    DeviceGuard dg(h->device);
+    if (!dg.ok) return XG_ECUDA;
+    int rc = XG_OK;
+    if (!h->d_snap) rc = cuda_rc(cudaMalloc(&h->d_snap, (kR + 4) * sizeof(uint32_t)));
+    if (!rc && !h->d_scratch) rc = cuda_rc(cudaMalloc(&h->d_scratch, kNextBuf * sizeof(uint32_t)));
+    if (rc) return rc;
+    cudaStream_t s = nullptr;
+    rc = cuda_rc(cudaMemcpyAsync(h->d_snap, h->d_win, kR * 4, cudaMemcpyDeviceToDevice, s));
+    if (!rc) rc = cuda_rc(cudaMemcpyAsync(h->d_snap + kR, h->d_weyl, 4, cudaMemcpyDeviceToDevice, s));
+    if (!rc) rc = launch_fill<kU32>(h, 0, 1, kNextBuf, h->d_scratch, nullptr, s);
+    h->nbuf.assign(kNextBuf, 0);
+    if (!rc) rc = cuda_rc(cudaMemcpy(h->nbuf.data(), h->d_scratch, kNextBuf * 4, cudaMemcpyDeviceToHost));
+    if (rc) {
+        h->nbuf.clear();
+        h->npos = 0;
+        return rc;
+    }
+    h->npos = 0;
+    *out = h->nbuf[h->npos++];
+    return XG_OK;
+}
+
+int xg_next_u64(xg_ensemble_t h, uint64_t* out) {
+    if (!out) return XG_EINVAL;
+    uint32_t lo, hi;
+    int rc = xg_next_u32(h, &lo);
+    if (rc) return rc;
+    rc = xg_next_u32(h, &hi);
+    if (rc) return rc;
+    *out = static_cast<uint64_t>(lo) | (static_cast<uint64_t>(hi) << 32);
+    return XG_OK;
+}
+
+int xg_state_export(xg_ensemble_t h, uint32_t index, uint64_t* buffer, uint64_t* weyl) {
+    if (!h || !buffer || !weyl) return XG_EINVAL;
+    if (index >= h->num_streams) return XG_ERANGE;
+    DeviceGuard dg(h->device);
+    if (!dg.ok) return XG_ECUDA;
+    int rc = cuda_rc(cudaDeviceSynchronize());
+    if (!rc) rc = settle_next(h, nullptr);
+    if (rc) return rc;
+    uint32_t win[kR], wy;
+    rc = cuda_rc(cudaMemcpy(win, h->d_win + static_cast<size_t>(index) * kR, sizeof win,
+                            cudaMemcpyDeviceToHost));
+    if (!rc) rc = cuda_rc(cudaMemcpy(&wy, h->d_weyl + index, 4, cudaMemcpyDeviceToHost));
+    if (rc) return rc;
+    for (unsigned i = 0; i < kR; ++i) buffer[i] = win[i];
+    *weyl = wy;
+    return XG_OK;
+}
+
+int xg_state_import(xg_ensemble_t h, uint32_t index, const uint64_t* buffer, uint64_t weyl) {
+    if (!h || !buffer) return XG_EINVAL;
+    if (index >= h->num_streams) return XG_ERANGE;
+    DeviceGuard dg(h->device);
+    if (!dg.ok) return XG_ECUDA;
+    int rc = cuda_rc(cudaDeviceSynchronize());
+    if (!rc) rc = settle_next(h, nullptr);
+    if (rc) return rc;
+    uint32_t win[kR];
+    for (unsigned i = 0; i < kR; ++i) win[i] = static_cast<uint32_t>(buffer[i] & kMask32);
+    const uint32_t wy = static_cast<uint32_t>(weyl & kMask32);
+    rc = cuda_rc(cudaMemcpy(h->d_win + static_cast<size_t>(index) * kR, win, sizeof win,
+                            cudaMemcpyHostToDevice));
+    if (!rc) rc = cuda_rc(cudaMemcpy(h->d_weyl + index, &wy, 4, cudaMemcpyHostToDevice));
+    return rc;
+}
+
+int xg_partition(uint64_t total_streams, uint32_t world, uint32_t rank, uint64_t* first,
+                 uint32_t* count) {
+    if (!first || !count || world == 0) return XG_EINVAL;
+    if (rank >= world) return XG_ERANGE;
+    const unsigned __int128 t = total_streams;
+    const uint64_t lo = static_cast<uint64_t>(t * rank / world);
+    const uint64_t hi = static_cast<uint64_t>(t * (rank + 1) / world);
+    if (hi - lo > 0xffffffffull) return XG_ERANGE;
+    *first = lo;
+    *count = static_cast<uint32_t>(hi - lo);
+    return XG_OK;
+}
+
+uint64_t xg_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+const char* xg_build_info(void) {
+    return "libxg_gpu: xorgensGP warp-per-stream register-window kernels, sm_100a";
+}
+
+}  // extern "C"

@@ -1,0 +1,307 @@
+// xg_kernels.cuh -- sm_100a device code for the xorgensGP generation path.
+//
+// Design: ONE WARP PER STREAM, the r = 128 word window in
+// registers.  Lane l holds logical window words W[l], W[32+l], W[64+l],
+// W[96+l] (oldest first), i.e. four registers R[0..3].  One warp step makes
+// the next 32 words of the stream at once -- 32 <= lane_bound = min(s, r-s)
+// = 63, so every operand is older than the step (the gather/commit argument of
+// proj/src/parallel.cpp:8-42):
+//
+//   x_{i+l} = T(W[l], a, b) ^ T(W[(r-s)+l], c, d)          (xorgens.hpp:39-47)
+//
+// W[l] is the lane's own R[0]; W[(r-s)+l] lives in lane (l+delta)&31 in
+// register J or J+1 ((r-s) = 32*J + delta), so it costs one select + one
+// shuffle.  The new word replaces R[0] and the window rotates by renaming
+// registers (4-step unroll), so there are no moves.  The Weyl term of lane l in
+// step k is weyl + (32k + l + 1)*omega (closed form, parallel.cpp:33-39), and
+// the output is ((w ^ (w >> gamma)) + x) mod 2^32 (xorgens.hpp:58-62).
+//
+// Each warp step emits one contiguous, 128-byte aligned line of the
+// block-major output (out[g*per_stream + k], parallel.cpp:97-135), stored with
+// one coalesced STG.32 per step -- the cheapest store in issue slots for this
+// layout (a smem transpose to STG.128 would add STS+LDS per word).
+#pragma once
+
+#include <cstdint>
+
+namespace xgk {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kWarpsPerBlock = 8;  // 256 threads: 8 streams per CTA
+constexpr int kThreads = 32 * kWarpsPerBlock;
+constexpr unsigned kR = 128;       // GPU path: r = 128 (four registers per lane)
+
+// xorgensgp32 (proj/src/params.cpp:83): (r,s,a,b,c,d) = (128,65,15,14,12,17),
+// w = 32, omega = 2654435769, gamma = 16.  Compile-time so every shift is an
+// immediate (the paper bakes parameters in).
+struct GP32 {
+    static constexpr int J = 1;              // (r - s) / 32 = 63 / 32
+    static constexpr unsigned delta = 31;    // (r - s) % 32
+    static constexpr unsigned a = 15, b = 14, c = 12, d = 17, gamma = 16;
+    static constexpr uint32_t omega = 2654435769u;
+};
+
+// Any other valid w = 32, r = 128 set with lane_bound >= 32: r - s is odd
+// (gcd(128, s) = 1), so J is 1 or 2 and delta is in 1..31.
+template <int J_>
+struct RtParams {
+    static constexpr int J = J_;
+    unsigned delta, a, b, c, d, gamma;
+    uint32_t omega;
+};
+
+enum Mode : int { kU32 = 0, kF32 = 1, kF64 = 2, kMC = 3, kSkip = 4 };
+
+// xorshift_transform (proj/include/xg/xorgens.hpp:13-18) on 32-bit words.
+__device__ __forceinline__ uint32_t xs(uint32_t x, unsigned l, unsigned r) {
+    const uint32_t t = x ^ (x << l);
+    return t ^ (t >> r);
+}
+
+// One warp step on the register window.  S is the position in the 4-step
+// rotation: logical block j of the window lives in R[(S + j) & 3].
+template <int S, class P>
+__device__ __forceinline__ uint32_t warp_step(uint32_t (&R)[4], const P& p, unsigned src,
+                                              bool gives_J) {
+    constexpr int i0 = S & 3;
+    constexpr int iJ = (S + P::J) & 3;
+    constexpr int iJ1 = (S + P::J + 1) & 3;
+    const uint32_t give = gives_J ? R[iJ] : R[iJ1];
+    const uint32_t tap_s = __shfl_sync(kFull, give, src);
+    const uint32_t v = xs(R[i0], p.a, p.b) ^ xs(tap_s, p.c, p.d);
+    R[i0] = v;  // newest block; the old block 0 is no longer needed
+    return v;
+}
+
+// Output stage (xorgens.hpp:58-62): ((w ^ (w >> gamma)) + x) mod 2^32.
+template <class P>
+__device__ __forceinline__ uint32_t weyl_out(uint32_t w, uint32_t v, const P& p) {
+    return (w ^ (w >> p.gamma)) + v;
+}
+
+// Uniform float: (u >> 8) * 2^-24, exact.
+__device__ __forceinline__ float u32_to_f32(uint32_t u) {
+    return __uint2float_rn(u >> 8) * 0x1p-24f;
+}
+
+// Uniform double: (u64 >> 11) * 2^-53 with u64 = lo | hi << 32.
+// = hi * 2^-32 + (lo >> 11) * 2^-53; both products and the sum are exact.
+__device__ __forceinline__ double pair_to_f64(uint32_t lo, uint32_t hi) {
+    return __fma_rn(__uint2double_rn(hi), 0x1p-32, __uint2double_rn(lo >> 11) * 0x1p-53);
+}
+
+// MC predicate: x = lo >> 8, y = hi >> 8, hit iff x^2 + y^2 < 2^48 (exact).
+__device__ __forceinline__ uint32_t mc_hit(uint32_t x, uint32_t y) {
+    const uint64_t xx = x >> 8, yy = y >> 8;
+    return (xx * xx + yy * yy) < (1ull << 48) ? 1u : 0u;
+}
+
+// Pairs consecutive words for the two-word consumers.  Steps A (words
+// 32k..32k+31) and B (32k+32..32k+63) hold 32 pairs (2m, 2m+1): even lanes
+// take pair l/2 from A, odd lanes pair 16 + l/2 from B, via one xor-shuffle.
+__device__ __forceinline__ void pair_words(uint32_t a, uint32_t b, bool odd, uint32_t& lo,
+                                           uint32_t& hi) {
+    const uint32_t give = odd ? a : b;
+    const uint32_t got = __shfl_xor_sync(kFull, give, 1);
+    lo = odd ? got : a;
+    hi = odd ? b : got;
+}
+
+// SplitMix64 draw k (1-based) from `seed` in closed form: the chain of
+// proj/include/xg/mix.hpp:9-14 has state seed + k * 0x9e3779b97f4a7c15 at draw k.
+__device__ __forceinline__ uint64_t splitmix_draw(uint64_t seed, uint64_t k) {
+    uint64_t z = seed + k * 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+// K1: XorgensState(params, seed) for stream g (proj/src/xorgens.cpp:19-32):
+// r SplitMix draws (lane-parallel, closed form), weyl = draw r+1, zero guard
+// (warp vote), then 4r = 512 discarded outputs = 16 warp steps.  The discarded
+// outputs do not feed back, so the warm-up runs the linear part only and
+// advances the Weyl accumulator in closed form.
+template <class P>
+__global__ void __launch_bounds__(kThreads)
+seed_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32_t nstreams,
+            uint64_t seed0) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint32_t g = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (g >= nstreams) return;
+    const uint64_t seed = seed0 + g;  // base_seed + i, uint64 wrap (parallel.cpp:93-94)
+    uint32_t R[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) R[j] = static_cast<uint32_t>(splitmix_draw(seed, 32u * j + lane + 1));
+    const uint32_t w0 = static_cast<uint32_t>(splitmix_draw(seed, kR + 1));
+    const bool any = __any_sync(kFull, (R[0] | R[1] | R[2] | R[3]) != 0u);
+    if (!any && lane == 0) R[0] = 0x7f4a7c15u;  // 0x9e3779b97f4a7c15 & mask (xorgens.cpp:28-29)
+    const unsigned src = (lane + p.delta) & 31u;
+    const bool gives_J = lane >= p.delta;
+#pragma unroll 1
+    for (int it = 0; it < 4; ++it) {  // 16 steps = 4r words
+        warp_step<0>(R, p, src, gives_J);
+        warp_step<1>(R, p, src, gives_J);
+        warp_step<2>(R, p, src, gives_J);
+        warp_step<3>(R, p, src, gives_J);
+    }
+    uint32_t* w = win + static_cast<size_t>(g) * kR;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w[32 * j + lane] = R[j];
+    if (lane == 0) weyl[g] = w0 + 4u * kR * p.omega;
+}
+
+// Emits one step's word (single-word modes) at o[j].
+template <int MODE>
+__device__ __forceinline__ void emit1(void* o, int j, uint32_t word) {
+    if constexpr (MODE == kU32) {
+        __stcs(static_cast<uint32_t*>(o) + j, word);
+    } else if constexpr (MODE == kF32) {
+        __stcs(static_cast<float*>(o) + j, u32_to_f32(word));
+    }
+}
+
+// Emits (or counts) one pair at o[j] (two-word modes).
+template <int MODE>
+__device__ __forceinline__ void emit2(void* o, int j, uint32_t lo, uint32_t hi, uint32_t& hits) {
+    if constexpr (MODE == kF64) {
+        __stcs(static_cast<double*>(o) + j, pair_to_f64(lo, hi));
+    } else if constexpr (MODE == kMC) {
+        hits += mc_hit(lo, hi);
+    }
+}
+
+template <int MODE>
+__device__ __forceinline__ void* advance(void* o, int n) {
+    if constexpr (MODE == kF64) return static_cast<double*>(o) + n;
+    else if constexpr (MODE == kU32 || MODE == kF32) return static_cast<uint32_t*>(o) + n;
+    else return o;
+}
+
+// Four warp steps (one full register rotation) = 128 words of the stream,
+// emitted at cursor o.  Returns nothing; R, wl and hits are updated.
+template <int MODE, class P>
+__device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, unsigned src, bool gives_J,
+                                      bool odd, uint32_t& wl, uint32_t w_step, void* o,
+                                      uint32_t& hits) {
+    const uint32_t o0 = weyl_out(wl, warp_step<0>(R, p, src, gives_J), p);
+    const uint32_t o1 = weyl_out(wl + w_step, warp_step<1>(R, p, src, gives_J), p);
+    const uint32_t o2 = weyl_out(wl + 2u * w_step, warp_step<2>(R, p, src, gives_J), p);
+    const uint32_t o3 = weyl_out(wl + 3u * w_step, warp_step<3>(R, p, src, gives_J), p);
+    wl += 4u * w_step;
+    if constexpr (MODE == kF64 || MODE == kMC) {
+        uint32_t lo, hi;
+        pair_words(o0, o1, odd, lo, hi);
+        emit2<MODE>(o, 0, lo, hi, hits);
+        pair_words(o2, o3, odd, lo, hi);
+        emit2<MODE>(o, 32, lo, hi, hits);
+    } else {
+        emit1<MODE>(o, 0, o0);
+        emit1<MODE>(o, 32, o1);
+        emit1<MODE>(o, 64, o2);
+        emit1<MODE>(o, 96, o3);
+    }
+}
+
+// K2/K3/K4: fill / fused conversion / fused Monte Carlo / skip for streams
+// [g_begin, g_begin + g_count) of the ensemble, `words` words per stream,
+// continuing from (and saving back) each stream's state.
+//   kU32/kF32: out is stream-major with `words` values per stream, out[0] is
+//              stream g_begin's first value.
+//   kF64:      `words` must be even; words/2 doubles per stream.
+//   kMC:       `words` even; words/2 samples per stream; hit total added to *hits.
+template <class P, int MODE>
+__global__ void __launch_bounds__(kThreads)
+fill_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32_t g_begin,
+            uint32_t g_count, uint64_t words, void* __restrict__ out,
+            unsigned long long* __restrict__ hits_out) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint32_t gl = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (gl >= g_count) return;
+    const uint32_t g = g_begin + gl;
+    constexpr bool kPairs = (MODE == kF64 || MODE == kMC);
+
+    uint32_t* w = win + static_cast<size_t>(g) * kR;
+    uint32_t R[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) R[j] = w[32 * j + lane];
+    const uint32_t weyl0 = weyl[g];
+    uint32_t wl = weyl0 + (lane + 1u) * p.omega;
+    const uint32_t w_step = 32u * p.omega;
+    const unsigned src = (lane + p.delta) & 31u;
+    const bool gives_J = lane >= p.delta;
+    const bool odd = lane & 1u;
+
+    // Output cursor: single-word modes index words, pair modes index pairs.
+    const uint64_t per_stream_vals = kPairs ? (words >> 1) : words;
+    void* o = advance<MODE>(out, 0);
+    if constexpr (MODE != kMC && MODE != kSkip) {
+        const uint64_t first = static_cast<uint64_t>(gl) * per_stream_vals +
+                               (kPairs ? ((lane >> 1) + ((lane & 1u) << 4)) : lane);
+        if constexpr (MODE == kF64) o = static_cast<double*>(out) + first;
+        else o = static_cast<uint32_t*>(out) + first;
+    }
+    constexpr int kValsPerBody = kPairs ? 64 : 128;
+    uint32_t hits = 0;
+
+    uint64_t iters = words >> 7;  // 4 steps = 128 words per body
+    while (iters != 0) {
+        const uint32_t n = static_cast<uint32_t>(iters < (1ull << 30) ? iters : (1ull << 30));
+        iters -= n;
+        uint32_t i = 0;
+#pragma unroll 1
+        for (; i + 2 <= n; i += 2) {
+            body4<MODE>(R, p, src, gives_J, odd, wl, w_step, o, hits);
+            body4<MODE>(R, p, src, gives_J, odd, wl, w_step, advance<MODE>(o, kValsPerBody), hits);
+            o = advance<MODE>(o, 2 * kValsPerBody);
+        }
+        if (i < n) {
+            body4<MODE>(R, p, src, gives_J, odd, wl, w_step, o, hits);
+            o = advance<MODE>(o, kValsPerBody);
+        }
+    }
+
+    const unsigned tail = static_cast<unsigned>(words & 127u);
+    if (tail != 0) {
+        // One more (full) 4-step body; only the first `tail` words are
+        // emitted.  The state saved below ends exactly at word `words`.
+        const uint32_t O[4] = {R[0], R[1], R[2], R[3]};
+        const uint32_t o0 = weyl_out(wl, warp_step<0>(R, p, src, gives_J), p);
+        const uint32_t o1 = weyl_out(wl + w_step, warp_step<1>(R, p, src, gives_J), p);
+        const uint32_t o2 = weyl_out(wl + 2u * w_step, warp_step<2>(R, p, src, gives_J), p);
+        const uint32_t o3 = weyl_out(wl + 3u * w_step, warp_step<3>(R, p, src, gives_J), p);
+        if constexpr (kPairs) {
+            const unsigned tail_pairs = tail >> 1;
+            const unsigned m = (lane >> 1) + ((lane & 1u) << 4);
+            uint32_t lo, hi;
+            pair_words(o0, o1, odd, lo, hi);
+            if (m < tail_pairs) emit2<MODE>(o, 0, lo, hi, hits);
+            pair_words(o2, o3, odd, lo, hi);
+            if (m + 32 < tail_pairs) emit2<MODE>(o, 32, lo, hi, hits);
+        } else {
+            if (lane < tail) emit1<MODE>(o, 0, o0);
+            if (lane + 32 < tail) emit1<MODE>(o, 32, o1);
+            if (lane + 64 < tail) emit1<MODE>(o, 64, o2);
+            if (lane + 96 < tail) emit1<MODE>(o, 96, o3);
+        }
+        // New logical window = words [words-128, words): positions tail..tail+127
+        // of the 256 words held in O (old window) followed by R (new block).
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const unsigned q = 32u * j + lane;
+            if (q >= tail && q < tail + kR) w[q - tail] = (j < 4) ? O[j & 3] : R[j & 3];
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[32 * j + lane] = R[j];
+    }
+    if (lane == 0) weyl[g] = weyl0 + static_cast<uint32_t>(words) * p.omega;
+
+    if constexpr (MODE == kMC) {
+        unsigned long long t = hits;
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) t += __shfl_xor_sync(kFull, t, s);
+        if (lane == 0 && t) atomicAdd(hits_out, t);
+    }
+}
+
+}  // namespace xgk

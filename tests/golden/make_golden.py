@@ -1,0 +1,130 @@
+#!/usr/bin/env python3
+"""Generates tests/golden/ref_vectors.json from the REFERENCE ITSELF.
+
+Every word below comes out of oracle/_ref/libxgref.so, i.e. the reference's
+own proj/src/{params,xorgens,parallel}.cpp compiled unmodified (see
+oracle/Makefile).  The float / uint64 / Monte Carlo entries apply the
+conventions of DESIGN.md section 3 (numpy, exact) to reference words, since
+the reference has no conversions of its own.
+
+Run in the container that has /root/reference:  python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+from oracle import Oracle, Params, Reference  # noqa: E402
+
+M64 = (1 << 64) - 1
+
+
+def hexs(a):
+    return [f"{int(v):08x}" for v in a]
+
+
+def stream_checksums(ref: Reference, p, seed: int, n: int):
+    w = ref.stream(seed, n, p).astype(np.uint64)
+    x = int(np.bitwise_xor.reduce(w)) & 0xFFFFFFFF
+    s = int(np.sum(w * np.arange(1, n + 1, dtype=np.uint64), dtype=np.uint64))
+    return x, s, int(w[-1])
+
+
+def main() -> None:
+    ref = Reference()
+    o = Oracle()
+    gp32 = o.gp32()
+    out = {"generator": "xorgensgp32 (128,65,15,14,12,17) w=32",
+           "source": "oracle/_ref/libxgref.so = reference proj/src/{params,xorgens,parallel}.cpp"}
+
+    # 1. per-seed stream prefixes (incl. the reference KAT seeds 0 and 42)
+    seeds = [0, 1, 2, 3, 42, 1000, 1001, 2**63, M64]
+    out["streams"] = {str(s): hexs(ref.stream(s, 300, gp32)) for s in seeds}
+
+    # 2. seeded state of seed 1 (logical buffer oldest first + weyl)
+    buf, wy = ref.seeded_state(1, gp32)
+    out["seeded_state_seed1"] = {"buffer": hexs(buf), "weyl": f"{wy:08x}"}
+
+    # 3. other parameter sets the GPU path accepts (w=32, r=128, lane_bound>=32)
+    alt = Params(128, 95, 17, 12, 13, 15, 32, 2654435769, 16)   # lane_bound 33 (test_params.cpp:65)
+    alt2 = Params(128, 33, 11, 7, 9, 19, 32, 0x6A09E667 | 1, 11)
+    out["alt_params"] = []
+    for p in (alt, alt2):
+        out["alt_params"].append({
+            "params": [p.r, p.s, p.a, p.b, p.c, p.d, p.w, p.omega, p.gamma],
+            "check": ref.check(p),
+            "streams": {str(s): hexs(ref.stream(s, 600, p)) for s in (5, 6, 7)}})
+
+    # 4. BlockEnsemble::generate, block-major, awkward sizes (test_parallel.cpp:145-153)
+    gens = []
+    for base, blocks, lanes, per in ((7, 3, 63, 1), (7, 3, 63, 17), (7, 3, 63, 1000), (M64, 2, 63, 64),
+                                     (42, 8, 32, 600)):
+        h = ref.ensemble(gp32, base, blocks, lanes)
+        words, _, _ = ref.generate_words(h, blocks, per)
+        words2, _, _ = ref.generate_words(h, blocks, per)  # continuation
+        ref.destroy(h)
+        gens.append({"base_seed": base, "blocks": blocks, "lanes": lanes, "per_block": per,
+                     "first": [hexs(r) for r in words], "second": [hexs(r) for r in words2]})
+    out["generate"] = gens
+
+    # 5. from_raw streams
+    rng = np.random.default_rng(2024)
+    raw = rng.integers(0, 2**32, size=128, dtype=np.uint64)
+    out["from_raw"] = {"buffer": hexs(raw), "weyl": "deadbeef",
+                       "stream": hexs(ref.from_raw_stream(raw, 0xDEADBEEF, 400, gp32))}
+
+    # 6. conversions on reference words
+    w = ref.stream(42, 256, gp32).astype(np.uint64)
+    f32 = ((w.astype(np.uint32) >> 8).astype(np.float32) * np.float32(2.0 ** -24))
+    u64 = w[0::2] | (w[1::2] << np.uint64(32))
+    f64 = (u64 >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    x = (w[0::2] >> np.uint64(8))
+    y = (w[1::2] >> np.uint64(8))
+    hits = int(np.count_nonzero(x * x + y * y < np.uint64(1 << 48)))
+    out["conversions_seed42"] = {"f32_bits": [f"{v:08x}" for v in f32.view(np.uint32)],
+                                 "u64": [f"{int(v):016x}" for v in u64],
+                                 "f64_bits": [f"{v:016x}" for v in f64.view(np.uint64)],
+                                 "mc_hits_128_samples": hits}
+
+    # 7. BASELINE config 1: seed 1, 10^8 words
+    x1, s1, last1 = stream_checksums(ref, gp32, 1, 10**8)
+    out["config1"] = {"seed": 1, "n": 10**8, "xor": f"{x1:08x}", "sum": f"{s1 % 2**64:016x}",
+                      "last": f"{last1:08x}"}
+
+    # 8. BASELINE config 2: base_seed 1, P = 2^14 streams x 2^16 words, block-major,
+    #    xor and sum_pos word*(pos+1) mod 2^64 with pos = g*2^16 + k; per-stream xor.
+    P, n = 1 << 14, 1 << 16
+
+    def one(g):
+        wg = ref.stream(1 + g, n, gp32).astype(np.uint64)
+        pos = np.arange(g * n + 1, g * n + n + 1, dtype=np.uint64)
+        return (int(np.bitwise_xor.reduce(wg)), int(np.sum(wg * pos, dtype=np.uint64)))
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count()) as ex:
+        res = list(ex.map(one, range(P)))
+    gx = 0
+    gs = 0
+    for xv, sv in res:
+        gx ^= xv
+        gs = (gs + sv) % 2**64
+    per_stream_xor = np.array([r[0] for r in res], dtype=np.uint32)
+    out["config2"] = {"base_seed": 1, "streams": P, "per_stream": n, "xor": f"{gx:08x}",
+                      "wsum": f"{gs:016x}",
+                      "per_stream_xor_sha": __import__("hashlib").sha256(per_stream_xor.tobytes()).hexdigest(),
+                      "per_stream_xor_first16": hexs(per_stream_xor[:16])}
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ref_vectors.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print("wrote", path, "config1", out["config1"], "config2", out["config2"]["xor"],
+          out["config2"]["wsum"])
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,281 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the oracle,
+the reference goldens and size-independent properties.  Bit-exact everywhere
+(integer work; the float conversions are exact by construction)."""
+import numpy as np
+import pytest
+
+from helpers import u32
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1108_0486_b200 as xg  # noqa: E402
+from oracle import Params  # noqa: E402
+
+GP32 = xg.xorgensgp32_params()
+KAT_SEED0 = ["a2c5f91b", "bd5797de", "cac8bc67", "7ba44aee", "11254d96", "198b2ab0", "656ea882",
+             "9a94ce3e", "45568ed8", "1a4d6e4b", "bdcd2db4", "4bb14332", "74e6e085", "4cafd1e2",
+             "04dbdceb", "07ba0f22"]  # proj/tests/test_xorgens.cpp:165-170
+
+
+def np_u32(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def test_kat_seed0_and_golden_seed42():
+    e = xg.BlockEnsemble(GP32, 0, 1, 63)
+    assert np.array_equal(np_u32(e.fill_u32(16))[0], u32(KAT_SEED0))
+    e = xg.BlockEnsemble(GP32, 42, 1, 63)
+    assert [f"{v:08x}" for v in np_u32(e.fill_u32(4))[0]] == ["a61e8308", "8469633b", "80f8af0d",
+                                                               "57f95c64"]
+
+
+def test_golden_streams(golden):
+    for seed, words in golden["streams"].items():
+        e = xg.BlockEnsemble(GP32, int(seed), 1, 63)
+        assert np.array_equal(np_u32(e.fill_u32(len(words)))[0], u32(words)), seed
+
+
+def test_golden_seeded_state(golden):
+    e = xg.BlockEnsemble(GP32, 1, 1, 63)
+    buf, wy = e.block_state(0)
+    g = golden["seeded_state_seed1"]
+    assert np.array_equal(np.array(buf, dtype=np.uint32), u32(g["buffer"]))
+    assert wy == int(g["weyl"], 16)
+
+
+def test_golden_generate_and_continuation(golden):
+    for g in golden["generate"]:
+        e = xg.BlockEnsemble(GP32, g["base_seed"], g["blocks"], g["lanes"])
+        first = np_u32(e.fill_u32(g["per_block"]))
+        second = e.generate(g["per_block"])  # host path continues the same streams
+        assert np.array_equal(first, np.stack([u32(r) for r in g["first"]]))
+        assert np.array_equal(second, np.stack([u32(r) for r in g["second"]]))
+
+
+@pytest.mark.parametrize("idx", [0, 1])
+def test_golden_alt_params_runtime_kernels(golden, idx):
+    entry = golden["alt_params"][idx]
+    p = xg.GeneratorParams(*entry["params"])
+    assert xg.gpu_supported(p)
+    for seed, words in entry["streams"].items():
+        e = xg.BlockEnsemble(p, int(seed), 1, 32)
+        a = np_u32(e.fill_u32(250))[0]
+        b = np_u32(e.fill_u32(len(words) - 250))[0]
+        assert np.array_equal(np.concatenate([a, b]), u32(words))
+
+
+@pytest.mark.parametrize("streams", [1, 7, 8, 9, 257])
+@pytest.mark.parametrize("per", [1, 17, 31, 32, 33, 127, 128, 129, 1000, 4101])
+def test_fill_u32_vs_oracle(oracle, streams, per):
+    base = 0x1234_5678_9ABC + streams * 1000 + per
+    e = xg.BlockEnsemble(GP32, base, streams, 63)
+    o = oracle.ensemble(base, streams)
+    for _ in range(2):  # second call checks continuation from a ragged end
+        assert np.array_equal(np_u32(e.fill_u32(per)), o.fill_u32(per))
+
+
+def test_fill_random_call_sequence(oracle):
+    rng = np.random.default_rng(11)
+    e = xg.BlockEnsemble(GP32, 99, 33, 63)
+    o = oracle.ensemble(99, 33)
+    for _ in range(12):
+        kind = rng.integers(0, 5)
+        n = int(rng.integers(0, 700))
+        if kind == 0:
+            assert np.array_equal(np_u32(e.fill_u32(n)), o.fill_u32(n))
+        elif kind == 1:
+            got = np_u32(e.fill_f32(n))
+            assert np.array_equal(got.view(np.uint32), o.fill_f32(n).view(np.uint32))
+        elif kind == 2:
+            got = np_u32(e.fill_f64(n))
+            assert np.array_equal(got.view(np.uint64), o.fill_f64(n).view(np.uint64))
+        elif kind == 3:
+            hits = e.mc_pi(n)
+            assert int(hits.item()) == int(o.mc_hits(n).sum())
+        else:
+            e.skip(n)
+            o.fill_u32(n)
+    assert np.array_equal(np_u32(e.fill_u32(300)), o.fill_u32(300))
+
+
+def test_partitioned_slices_equal_single_fill(oracle):
+    total, per = 100, 777
+    full = np_u32(xg.BlockEnsemble(GP32, 5, total, 63).fill_u32(per))
+    for world in (2, 3, 8):
+        parts = []
+        for rank in range(world):
+            first, count = xg.partition(total, world, rank)
+            parts.append(np_u32(xg.BlockEnsemble(GP32, 5, count, 63, first_stream=first).fill_u32(per)))
+        assert np.array_equal(np.concatenate(parts), full)
+
+
+def test_seed_wrap():
+    e = xg.BlockEnsemble(GP32, 2**64 - 1, 2, 63)
+    w = np_u32(e.fill_u32(40))
+    assert np.array_equal(w[1], np_u32(xg.BlockEnsemble(GP32, 0, 1, 63).fill_u32(40))[0])
+
+
+@pytest.mark.parametrize("per", [1, 2, 31, 32, 33, 63, 64, 65, 1001])
+def test_conversions_vs_oracle(oracle, per):
+    e = xg.BlockEnsemble(GP32, 77, 5, 63)
+    o = oracle.ensemble(77, 5)
+    f = np_u32(e.fill_f32(per))
+    assert np.array_equal(f.view(np.uint32), o.fill_f32(per).view(np.uint32))
+    d = np_u32(e.fill_f64(per))
+    assert np.array_equal(d.view(np.uint64), o.fill_f64(per).view(np.uint64))
+    u = np_u32(e.fill_u64(per))
+    w = o.fill_u32(2 * per).astype(np.uint64)
+    assert np.array_equal(u, w[:, 0::2] | (w[:, 1::2] << np.uint64(32)))
+    assert (f >= 0).all() and (f < 1).all() and (d >= 0).all() and (d < 1).all()
+
+
+def test_golden_conversions(golden):
+    g = golden["conversions_seed42"]
+    assert np.array_equal(np_u32(xg.BlockEnsemble(GP32, 42, 1, 63).fill_f32(256))[0].view(np.uint32),
+                          u32(g["f32_bits"]))
+    d = np_u32(xg.BlockEnsemble(GP32, 42, 1, 63).fill_f64(128))[0]
+    assert [f"{v:016x}" for v in d.view(np.uint64)] == g["f64_bits"]
+    u = np_u32(xg.BlockEnsemble(GP32, 42, 1, 63).fill_u64(128))[0]
+    assert [f"{int(v):016x}" for v in u] == g["u64"]
+    h = xg.BlockEnsemble(GP32, 42, 1, 63).mc_pi(128)
+    assert int(h.item()) == g["mc_hits_128_samples"]
+
+
+@pytest.mark.parametrize("samples", [1, 31, 32, 33, 64, 1000, 65536 + 3])
+def test_mc_pi_exact_vs_oracle(oracle, samples):
+    e = xg.BlockEnsemble(GP32, 3, 19, 63)
+    o = oracle.ensemble(3, 19)
+    hits = e.mc_pi(samples)
+    hits = e.mc_pi(samples, hits=hits)  # accumulates, continues streams
+    assert int(hits.item()) == int(o.mc_hits(samples).sum() + o.mc_hits(samples).sum())
+
+
+def test_from_raw_and_state_roundtrip(oracle, golden):
+    g = golden["from_raw"]
+    buf = u32(g["buffer"]).astype(np.uint64)
+    st = xg.XorgensState.from_raw(GP32, buf.tolist(), int(g["weyl"], 16))
+    words = [st.next_word() for _ in range(len(g["stream"]))]
+    assert np.array_equal(np.array(words, dtype=np.uint32), u32(g["stream"]))
+    # export after an odd number of words equals the oracle's logical buffer
+    e = xg.BlockEnsemble(GP32, 8, 3, 63)
+    e.fill_u32(333)
+    o = oracle.ensemble(8, 3)
+    o.fill_u32(333)
+    for i in range(3):
+        b, w = e.block_state(i)
+        assert np.array_equal(np.array(b, dtype=np.uint64), o.logical_buffer(i))
+        assert w == o.weyl(i)
+    # import stream 0's state into stream 2: they then agree
+    b0, w0 = e.block_state(0)
+    e.set_block_state(2, b0, w0)
+    out = np_u32(e.fill_u32(500))
+    assert np.array_equal(out[0], out[2])
+    assert not np.array_equal(out[0], out[1])
+
+
+def test_next_word_interleaves_with_fills(oracle):
+    st = xg.XorgensState(GP32, 1234)
+    ref = oracle.stream(1234, 40000)
+    got = [st.next_word() for _ in range(1000)]
+    got += np_u32(st.ensemble.fill_u32(3000))[0].tolist()
+    got += [st.next_word() for _ in range(20000)]       # crosses a refill boundary
+    v = st.next_u64()
+    got += [v & 0xFFFFFFFF, v >> 32]
+    got += np_u32(st.ensemble.fill_u32(1000))[0].tolist()
+    assert np.array_equal(np.array(got, dtype=np.uint32), ref[:len(got)])
+    b, w = st.logical_buffer(), st.weyl_value()
+    o = oracle.ensemble(1234, 1)
+    o.fill_u32(len(got))
+    assert np.array_equal(np.array(b, dtype=np.uint64), o.logical_buffer(0)) and w == o.weyl(0)
+
+
+def test_batch_step_and_source(oracle):
+    st = xg.XorgensState(GP32, 5)
+    got = []
+    for lanes in (1, 32, 63, 7):
+        got += xg.batch_step(st, lanes)
+    assert np.array_equal(np.array(got, dtype=np.uint32), oracle.stream(5, len(got)))
+    with pytest.raises(xg.OutOfRangeError):
+        xg.batch_step(st, 64)
+    with pytest.raises(xg.OutOfRangeError):
+        xg.batch_step(st, 0)
+    src = xg.XorgensSource(GP32, 42)
+    assert [src.next() for _ in range(4)] == [0xa61e8308, 0x8469633b, 0x80f8af0d, 0x57f95c64]
+    assert src.word_bits() == 32
+
+
+def test_empty_and_errors():
+    e = xg.BlockEnsemble(GP32, 0, 2, 1)
+    assert e.generate(0).shape == (2, 0)
+    with pytest.raises(xg.OutOfRangeError):
+        xg.BlockEnsemble(GP32, 0, 0, 1)
+    with pytest.raises(xg.OutOfRangeError):
+        xg.BlockEnsemble(GP32, 0, 1, 64)
+    with pytest.raises(xg.UnsupportedParamsError):
+        xg.BlockEnsemble(xg.tiny_r4w16_params(), 0, 1, 1)
+    with pytest.raises(ValueError):
+        e.fill_u32(10, out=torch.empty(3, dtype=torch.uint32, device="cuda"))
+    with pytest.raises(xg.OutOfRangeError):
+        e.block_state(2)
+
+
+def test_block_independence(oracle):
+    # proj/tests/test_parallel.cpp:155-167
+    a = xg.BlockEnsemble(GP32, 55, 3, 63)
+    b = xg.BlockEnsemble(GP32, 55, 3, 63)
+    buf, w = a.block_state(1)
+    o = oracle.from_raw(np.array(buf, dtype=np.uint64)[None, :], [w])
+    o.fill_u32(100)
+    a.set_block_state(1, o.logical_buffer(0).tolist(), o.weyl(0))
+    ra, rb = np_u32(a.fill_u32(200)), np_u32(b.fill_u32(200))
+    assert np.array_equal(ra[0], rb[0]) and np.array_equal(ra[2], rb[2])
+    assert not np.array_equal(ra[1], rb[1])
+
+
+@pytest.mark.slow
+def test_config2_full_size_checksum(golden, oracle):
+    """BASELINE config 2: 2^30 words, P = 2^14 streams x 2^16, base_seed 1 --
+    xor and block-major weighted sum against the reference-derived golden,
+    plus sampled streams word-for-word against the oracle."""
+    g = golden["config2"]
+    P, n = g["streams"], g["per_stream"]
+    e = xg.BlockEnsemble(GP32, g["base_seed"], P, 63)
+    out = e.fill_u32(n)
+    host = np_u32(out).reshape(-1)
+    del out
+    per_stream_xor = np.bitwise_xor.reduce(host.reshape(P, n), axis=1).astype(np.uint32)
+    gx = int(np.bitwise_xor.reduce(per_stream_xor))
+    gs = 0
+    chunk = 1 << 24
+    for start in range(0, host.size, chunk):
+        w = host[start:start + chunk].astype(np.uint64)
+        pos = np.arange(start + 1, start + w.size + 1, dtype=np.uint64)
+        gs = (gs + int(np.sum(w * pos, dtype=np.uint64))) % 2**64
+    assert f"{gx:08x}" == g["xor"]
+    assert f"{gs:016x}" == g["wsum"]
+    import hashlib
+    assert hashlib.sha256(per_stream_xor.tobytes()).hexdigest() == g["per_stream_xor_sha"]
+    for s in (0, 1, 4095, P - 1):
+        assert np.array_equal(host[s * n:(s + 1) * n], oracle.stream(g["base_seed"] + s, n))
+
+
+@pytest.mark.slow
+def test_full_size_float_properties(oracle):
+    """2^30 f32 and f64 values: range, mean, and sampled streams bit-exact."""
+    P, n = 1 << 14, 1 << 16
+    e = xg.BlockEnsemble(GP32, 1, P, 63)
+    f = e.fill_f32(n)
+    assert float(f.min()) >= 0.0 and float(f.max()) < 1.0
+    assert abs(float(f.double().mean()) - 0.5) < 1e-4
+    o = oracle.ensemble(1, 2)
+    assert np.array_equal(np_u32(f[:2]).view(np.uint32), o.fill_f32(n).view(np.uint32))
+    del f
+    d = e.fill_f64(n // 2)
+    assert float(d.min()) >= 0.0 and float(d.max()) < 1.0
+    assert abs(float(d.mean()) - 0.5) < 1e-4
+    assert np.array_equal(np_u32(d[:2]).view(np.uint64), o.fill_f64(n // 2).view(np.uint64))
