@@ -55,30 +55,52 @@ def load_traffic(workload: str):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled through NVML every
+    ~2 ms during the timed region (nvidia-smi as a fallback)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {  # nvmlClocksEventReason* bits
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
         self.index = index
         self.samples = []
+        self.max_mhz = None
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nvml = None
 
     def _run(self):
+        nv = self._nvml
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
-                parts = [x.strip() for x in out.strip().split(",")]
-                if len(parts) >= 7:
-                    self.samples.append(parts)
+                if nv is not None:
+                    sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                    try:
+                        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                    except Exception:
+                        rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+                    self.samples.append((float(sm), int(rs)))
+                    self._stop.wait(0.002)
+                else:
+                    out = subprocess.run(
+                        ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm",
+                         "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                        timeout=5).stdout.strip().split(",")
+                    self.samples.append((float(out[0]), 0))
+                    self.max_mhz = float(out[1])
+                    self._stop.wait(0.05)
             except Exception:
-                pass
-            self._stop.wait(0.1)
+                self._stop.wait(0.05)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -92,15 +114,36 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if s[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples"]}
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({name for _, r in self.samples for bit, name in self.REASONS.items()
+                          if r & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples), "sm_mhz_min": min(sm),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
+
+
+def write_probe_gbs(out, stream, reps: int = 5):
+    """Write-only HBM ceiling on the same buffer (libxg_probe.so, bench-only)."""
+    import ctypes
+
+    import torch
+
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_1108_0486_b200", "lib", "libxg_probe.so"))
+    lib.xg_probe_write.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    nbytes = out.numel() * out.element_size()
+    ptr, sp = ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(stream.cuda_stream)
+    for _ in range(3):
+        lib.xg_probe_write(ptr, nbytes, sp)
+    best = float("inf")
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        lib.xg_probe_write(ptr, nbytes, sp)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return nbytes / (best / 1e3) / 1e9
 
 
 def dist_setup():
@@ -242,7 +285,8 @@ def timed_loop(fn, stream, steps, warmup, world, flush=None):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: 200 for fills, 5 for mc_pi)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="fill_u32",
@@ -252,6 +296,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.steps is None:
+        args.steps = 5 if args.workload == "mc_pi" else (10 if args.impl == "reference" else 200)
     if args.impl == "reference":
         return run_reference_arm(args)
 
@@ -342,11 +388,10 @@ def main():
                               "kernel_ms_mean": kern_ms, "kernel_ms_min": min(step_ms)}
         # write-only ceiling on the same buffer, same run (context for frac)
         if out is not None:
-            def memset():
-                out.view(torch.uint8).fill_(0)
-            m_ms, m_steps = timed_loop(memset, stream, 5, 3, 1)
-            result["roofline"]["write_only_peak_gbs"] = out.numel() * out.element_size() / (
-                min(m_steps) / 1e3) / 1e9
+            try:
+                result["roofline"]["write_only_probe_gbs"] = write_probe_gbs(out, stream)
+            except OSError:
+                pass
     else:
         # in-register consumer: report integer-issue context
         hits_v = int(hits.item())

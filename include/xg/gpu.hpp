@@ -1,0 +1,204 @@
+// xg/gpu.hpp -- header-only C++ mirror of the reference xg API over the C ABI
+// (include/xg_gpu.h, libxg_gpu.so).  For C++ users of the reference library:
+// the same class names, signatures, argument meaning and exception types, in
+// namespace xg::gpu, so switching is a namespace change.
+//
+//   reference (proj/include/xg/...)              this header
+//   xg::BlockEnsemble(params, seed, blocks, lanes) xg::gpu::BlockEnsemble(...)
+//   BlockEnsemble::generate(per_block, workers)    same signature, same
+//                                                  vector<vector<uint64_t>> result
+//   xg::XorgensState(params, seed).next_word()     xg::gpu::XorgensState(...)
+//   XorgensState::from_raw / logical_buffer /      same
+//     weyl_value
+//   xg::batch_step(state, lanes)                   xg::gpu::batch_step
+//   std::out_of_range / ParamValidationError /     same exception classes
+//     std::invalid_argument
+//
+// `Params` is any struct with the GeneratorParams fields (r, s, a, b, c, d, w,
+// omega, gamma), so an xg::GeneratorParams can be passed as is.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "xg_gpu.h"
+
+namespace xg {
+namespace gpu {
+
+class ParamValidationError : public std::invalid_argument {
+public:
+    explicit ParamValidationError(int code)
+        : std::invalid_argument(xg_strerror(code)), code_(code - 1) {}
+    int code() const noexcept { return code_; }  // ParamError ordinal
+
+private:
+    int code_;
+};
+
+class CudaError : public std::runtime_error {
+public:
+    explicit CudaError(int code) : std::runtime_error(xg_strerror(code)), code_(code) {}
+    int code() const noexcept { return code_; }
+
+private:
+    int code_;
+};
+
+inline void check(int rc) {
+    if (rc == XG_OK) return;
+    if (rc >= 1 && rc <= 6) throw ParamValidationError(rc);
+    if (rc == XG_ERANGE) throw std::out_of_range(xg_strerror(rc));
+    if (rc == XG_EINVAL || rc == XG_EUNSUPPORTED) throw std::invalid_argument(xg_strerror(rc));
+    throw CudaError(rc);
+}
+
+template <class Params>
+inline xg_params_t to_c(const Params& p) {
+    xg_params_t c;
+    c.r = p.r; c.s = p.s; c.a = p.a; c.b = p.b; c.c = p.c; c.d = p.d; c.w = p.w;
+    c.omega = p.omega;
+    c.gamma = p.gamma;
+    return c;
+}
+
+inline xg_params_t xorgensgp32_params() { return xg_params_xorgensgp32(); }
+
+template <class Params>
+inline unsigned lane_bound(const Params& p) {
+    const xg_params_t c = to_c(p);
+    return xg_lane_bound(&c);
+}
+
+class BlockEnsemble {
+public:
+    template <class Params>
+    BlockEnsemble(const Params& params, std::uint64_t base_seed, unsigned num_blocks,
+                  unsigned lanes, std::uint64_t first_stream = 0, int device = 0,
+                  xg_stream_t stream = nullptr)
+        : base_seed_(base_seed), lanes_(lanes), r_(params.r) {
+        const xg_params_t c = to_c(params);
+        check(xg_ensemble_create(&c, base_seed, first_stream, num_blocks, lanes, device, stream,
+                                 &h_));
+        n_ = num_blocks;
+    }
+    BlockEnsemble(const BlockEnsemble&) = delete;
+    BlockEnsemble& operator=(const BlockEnsemble&) = delete;
+    BlockEnsemble(BlockEnsemble&& o) noexcept { *this = std::move(o); }
+    BlockEnsemble& operator=(BlockEnsemble&& o) noexcept {
+        std::swap(h_, o.h_);
+        n_ = o.n_;
+        base_seed_ = o.base_seed_;
+        lanes_ = o.lanes_;
+        r_ = o.r_;
+        return *this;
+    }
+    ~BlockEnsemble() {
+        if (h_) xg_ensemble_destroy(h_);
+    }
+
+    // proj/include/xg/parallel.hpp:46-47: block-major, continues every block.
+    std::vector<std::vector<std::uint64_t>> generate(std::size_t per_block,
+                                                     unsigned workers = 0) {
+        (void)workers;  // the device schedule never changes the output
+        std::vector<std::uint32_t> flat(static_cast<std::size_t>(n_) * per_block);
+        if (per_block) check(xg_generate_host(h_, per_block, flat.data(), nullptr));
+        std::vector<std::vector<std::uint64_t>> out(n_);
+        for (unsigned i = 0; i < n_; ++i)
+            out[i].assign(flat.begin() + static_cast<std::ptrdiff_t>(i * per_block),
+                          flat.begin() + static_cast<std::ptrdiff_t>((i + 1) * per_block));
+        return out;
+    }
+
+    // Device-buffer fills (asynchronous on `stream`).
+    void fill_u32(std::uint64_t per_block, std::uint32_t* dev, xg_stream_t s = nullptr) {
+        check(xg_fill_u32(h_, per_block, dev, s));
+    }
+    void fill_u64(std::uint64_t per_block, std::uint64_t* dev, xg_stream_t s = nullptr) {
+        check(xg_fill_u64(h_, per_block, dev, s));
+    }
+    void fill_f32(std::uint64_t per_block, float* dev, xg_stream_t s = nullptr) {
+        check(xg_fill_f32(h_, per_block, dev, s));
+    }
+    void fill_f64(std::uint64_t per_block, double* dev, xg_stream_t s = nullptr) {
+        check(xg_fill_f64(h_, per_block, dev, s));
+    }
+    void mc_pi(std::uint64_t samples, std::uint64_t* dev_hits, xg_stream_t s = nullptr) {
+        check(xg_mc_pi(h_, samples, dev_hits, s));
+    }
+
+    unsigned num_blocks() const noexcept { return n_; }
+    unsigned lanes() const noexcept { return lanes_; }
+    std::uint64_t base_seed() const noexcept { return base_seed_; }
+
+    std::pair<std::vector<std::uint64_t>, std::uint64_t> block_state(unsigned i) const {
+        std::vector<std::uint64_t> buf(r_);
+        std::uint64_t w = 0;
+        check(xg_state_export(h_, i, buf.data(), &w));
+        return {buf, w};
+    }
+    void set_block_state(unsigned i, const std::vector<std::uint64_t>& buf, std::uint64_t weyl) {
+        if (buf.size() != r_) throw std::invalid_argument("buffer size must equal r");
+        check(xg_state_import(h_, i, buf.data(), weyl));
+    }
+    xg_ensemble_t handle() const noexcept { return h_; }
+
+protected:
+    BlockEnsemble() = default;
+    xg_ensemble_t h_ = nullptr;
+    unsigned n_ = 0;
+    std::uint64_t base_seed_ = 0;
+    unsigned lanes_ = 0;
+    unsigned r_ = 0;
+};
+
+// One serial stream (proj/include/xg/xorgens.hpp:20-96), served from device refills.
+class XorgensState : public BlockEnsemble {
+public:
+    template <class Params>
+    XorgensState(const Params& params, std::uint64_t seed, int device = 0)
+        : BlockEnsemble(params, seed, 1u, lane_bound(params), 0, device) {}
+
+    template <class Params>
+    static XorgensState from_raw(const Params& params, const std::vector<std::uint64_t>& buffer,
+                                 std::uint64_t weyl, int device = 0) {
+        if (buffer.size() != params.r) throw std::invalid_argument("buffer size must equal r");
+        const xg_params_t c = to_c(params);
+        XorgensState st;
+        check(xg_ensemble_create_from_raw(&c, 1, buffer.data(), &weyl, device, nullptr, &st.h_));
+        st.n_ = 1;
+        st.r_ = params.r;
+        st.lanes_ = lane_bound(params);
+        return st;
+    }
+
+    std::uint64_t next_word() {
+        std::uint32_t v;
+        check(xg_next_u32(h_, &v));
+        return v;
+    }
+    std::uint64_t next_u64() {
+        std::uint64_t v;
+        check(xg_next_u64(h_, &v));
+        return v;
+    }
+    std::vector<std::uint64_t> logical_buffer() const { return block_state(0).first; }
+    std::uint64_t weyl_value() const { return block_state(0).second; }
+
+private:
+    XorgensState() = default;
+};
+
+// proj/src/parallel.cpp:8-42
+inline std::vector<std::uint64_t> batch_step(XorgensState& st, unsigned lanes) {
+    if (lanes == 0 || lanes > st.lanes()) throw std::out_of_range("lane count exceeds min(s, r - s)");
+    std::vector<std::uint64_t> out(lanes);
+    for (auto& v : out) v = st.next_word();
+    return out;
+}
+
+}  // namespace gpu
+}  // namespace xg

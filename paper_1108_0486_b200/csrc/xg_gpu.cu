@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <numeric>
@@ -119,11 +120,33 @@ int cuda_rc(cudaError_t e) {
 
 unsigned grid_for(uint32_t n) { return (n + kWarpsPerBlock - 1) / kWarpsPerBlock; }
 
-template <int MODE, class P>
-int launch_fill_p(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count,
+// Shift-placement variant of the GP32 kernels (xg_kernels.cuh, VAR mask):
+// bit 0 Weyl >> gamma, bit 1 t >> b, bit 2 t >> d as IMAD.HI on the FMA pipe.
+// Chosen per mode from the measurements in profiles/README.md; XG_VARIANT
+// overrides (experiments only).
+constexpr int kDefaultVar[5] = {1, 1, 1, 1, 1};
+
+int variant_for(int mode) {
+    static int forced = [] {
+        const char* e = getenv("XG_VARIANT");
+        return e ? atoi(e) : -1;
+    }();
+    return forced >= 0 ? forced : kDefaultVar[mode];
+}
+
+HiMul himul(const xg_params_t& p) {
+    HiMul m;
+    m.gamma = 1u << (32 - p.gamma);
+    m.b = 1u << (32 - p.b);
+    m.d = 1u << (32 - p.d);
+    return m;
+}
+
+template <int MODE, int VAR, class P>
+int launch_fill_v(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count,
                   uint64_t words, void* out, unsigned long long* hits, cudaStream_t s) {
-    fill_kernel<P, MODE><<<grid_for(g_count), kThreads, 0, s>>>(p, h->d_win, h->d_weyl, g_begin,
-                                                                g_count, words, out, hits);
+    fill_kernel<P, MODE, VAR><<<grid_for(g_count), kThreads, 0, s>>>(
+        p, himul(h->params), h->d_win, h->d_weyl, g_begin, g_count, words, out, hits);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cuda_rc(cudaGetLastError());
 }
@@ -133,24 +156,34 @@ int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t wor
                 unsigned long long* hits, cudaStream_t s) {
     if (words == 0 || g_count == 0) return XG_OK;
     switch (h->kind) {
-    case kGP32: return launch_fill_p<MODE>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-    case kRtJ1: return launch_fill_p<MODE>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s);
-    default: return launch_fill_p<MODE>(rt_params<2>(h->params), h, g_begin, g_count, words, out, hits, s);
+    case kGP32:
+        switch (variant_for(MODE)) {
+        case 0: return launch_fill_v<MODE, 0>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        case 3: return launch_fill_v<MODE, 3>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        case 5: return launch_fill_v<MODE, 5>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        case 7: return launch_fill_v<MODE, 7>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        default: return launch_fill_v<MODE, 1>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        }
+    case kRtJ1:
+        return launch_fill_v<MODE, 1>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s);
+    default:
+        return launch_fill_v<MODE, 1>(rt_params<2>(h->params), h, g_begin, g_count, words, out, hits, s);
     }
 }
 
 int launch_seed(xg_ensemble* h, uint64_t seed0, cudaStream_t s) {
     const unsigned grid = grid_for(h->num_streams);
+    const HiMul m = himul(h->params);
     switch (h->kind) {
     case kGP32:
-        seed_kernel<<<grid, kThreads, 0, s>>>(GP32{}, h->d_win, h->d_weyl, h->num_streams, seed0);
+        seed_kernel<<<grid, kThreads, 0, s>>>(GP32{}, m, h->d_win, h->d_weyl, h->num_streams, seed0);
         break;
     case kRtJ1:
-        seed_kernel<<<grid, kThreads, 0, s>>>(rt_params<1>(h->params), h->d_win, h->d_weyl,
+        seed_kernel<<<grid, kThreads, 0, s>>>(rt_params<1>(h->params), m, h->d_win, h->d_weyl,
                                              h->num_streams, seed0);
         break;
     default:
-        seed_kernel<<<grid, kThreads, 0, s>>>(rt_params<2>(h->params), h->d_win, h->d_weyl,
+        seed_kernel<<<grid, kThreads, 0, s>>>(rt_params<2>(h->params), m, h->d_win, h->d_weyl,
                                              h->num_streams, seed0);
         break;
     }

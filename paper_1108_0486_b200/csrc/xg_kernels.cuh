@@ -16,10 +16,17 @@
 // step k is weyl + (32k + l + 1)*omega (closed form, parallel.cpp:33-39), and
 // the output is ((w ^ (w >> gamma)) + x) mod 2^32 (xorgens.hpp:58-62).
 //
+// Issue-slot budget (measured, profiles/README.md): the loop is integer-ALU
+// bound, so right shifts can be moved from the ALU pipe (SHF) to the FMA pipe
+// as IMAD.HI by a runtime power of two (x >> k == umulhi(x, 2^(32-k))); the
+// VAR template mask selects which (bit 0: Weyl >> gamma, bit 1: t >> b,
+// bit 2: t >> d).  The multipliers are kernel arguments, not immediates, so
+// ptxas cannot strength-reduce them back to SHF.
+//
 // Each warp step emits one contiguous, 128-byte aligned line of the
 // block-major output (out[g*per_stream + k], parallel.cpp:97-135), stored with
-// one coalesced STG.32 per step -- the cheapest store in issue slots for this
-// layout (a smem transpose to STG.128 would add STS+LDS per word).
+// one coalesced evict-first STG.32 per step -- the cheapest store in issue
+// slots for this layout (a smem transpose to STG.128 would add STS+LDS per word).
 #pragma once
 
 #include <cstdint>
@@ -50,33 +57,54 @@ struct RtParams {
     uint32_t omega;
 };
 
+// Runtime multipliers for the IMAD.HI form of the right shifts.
+struct HiMul {
+    uint32_t gamma, b, d;  // 2^(32-gamma), 2^(32-b), 2^(32-d)
+};
+
 enum Mode : int { kU32 = 0, kF32 = 1, kF64 = 2, kMC = 3, kSkip = 4 };
 
-// xorshift_transform (proj/include/xg/xorgens.hpp:13-18) on 32-bit words.
-__device__ __forceinline__ uint32_t xs(uint32_t x, unsigned l, unsigned r) {
-    const uint32_t t = x ^ (x << l);
-    return t ^ (t >> r);
+template <bool HI>
+__device__ __forceinline__ uint32_t shr(uint32_t x, unsigned k, uint32_t mul) {
+    if constexpr (HI) return __umulhi(x, mul);
+    else return x >> k;
 }
+
+// 32-bit funnel: low word of (hi:lo) >> s, s in 0..63 (one SHF.R.U64).
+__device__ __forceinline__ uint32_t funnel_r(uint32_t lo, uint32_t hi, uint32_t s) {
+    return static_cast<uint32_t>(((static_cast<uint64_t>(hi) << 32) | lo) >> s);
+}
+
+// Per-warp loop invariants.
+struct Lane {
+    unsigned src;      // shuffle source lane for the s-tap
+    bool gives_J;      // this lane provides register J (else J+1) to the s-tap shuffle
+    uint32_t sh_own;   // 32 on odd lanes, 0 on even: funnel shift for the pair consumers
+};
 
 // One warp step on the register window.  S is the position in the 4-step
 // rotation: logical block j of the window lives in R[(S + j) & 3].
-template <int S, class P>
-__device__ __forceinline__ uint32_t warp_step(uint32_t (&R)[4], const P& p, unsigned src,
-                                              bool gives_J) {
+// xorshift_transform (proj/include/xg/xorgens.hpp:13-18) twice, then xor.
+template <int S, int VAR, class P>
+__device__ __forceinline__ uint32_t warp_step(uint32_t (&R)[4], const P& p, const HiMul& m,
+                                              const Lane& ln) {
     constexpr int i0 = S & 3;
     constexpr int iJ = (S + P::J) & 3;
     constexpr int iJ1 = (S + P::J + 1) & 3;
-    const uint32_t give = gives_J ? R[iJ] : R[iJ1];
-    const uint32_t tap_s = __shfl_sync(kFull, give, src);
-    const uint32_t v = xs(R[i0], p.a, p.b) ^ xs(tap_s, p.c, p.d);
+    const uint32_t give = ln.gives_J ? R[iJ] : R[iJ1];
+    const uint32_t y = __shfl_sync(kFull, give, ln.src);
+    const uint32_t x = R[i0];
+    const uint32_t t1 = x ^ (x << p.a);
+    const uint32_t t2 = y ^ (y << p.c);
+    const uint32_t v = t1 ^ shr<(VAR & 2) != 0>(t1, p.b, m.b) ^ t2 ^ shr<(VAR & 4) != 0>(t2, p.d, m.d);
     R[i0] = v;  // newest block; the old block 0 is no longer needed
     return v;
 }
 
 // Output stage (xorgens.hpp:58-62): ((w ^ (w >> gamma)) + x) mod 2^32.
-template <class P>
-__device__ __forceinline__ uint32_t weyl_out(uint32_t w, uint32_t v, const P& p) {
-    return (w ^ (w >> p.gamma)) + v;
+template <int VAR, class P>
+__device__ __forceinline__ uint32_t weyl_out(uint32_t w, uint32_t v, const P& p, const HiMul& m) {
+    return (w ^ shr<(VAR & 1) != 0>(w, p.gamma, m.gamma)) + v;
 }
 
 // Uniform float: (u >> 8) * 2^-24, exact.
@@ -84,27 +112,35 @@ __device__ __forceinline__ float u32_to_f32(uint32_t u) {
     return __uint2float_rn(u >> 8) * 0x1p-24f;
 }
 
-// Uniform double: (u64 >> 11) * 2^-53 with u64 = lo | hi << 32.
-// = hi * 2^-32 + (lo >> 11) * 2^-53; both products and the sum are exact.
-__device__ __forceinline__ double pair_to_f64(uint32_t lo, uint32_t hi) {
-    return __fma_rn(__uint2double_rn(hi), 0x1p-32, __uint2double_rn(lo >> 11) * 0x1p-53);
+// Uniform double from hi and (lo >> 11): (u64 >> 11) * 2^-53 with
+// u64 = lo | hi << 32, = hi * 2^-32 + (lo >> 11) * 2^-53; every step exact.
+__device__ __forceinline__ double pair_to_f64(uint32_t lo_shr11, uint32_t hi) {
+    return __fma_rn(__uint2double_rn(hi), 0x1p-32, __uint2double_rn(lo_shr11) * 0x1p-53);
 }
 
-// MC predicate: x = lo >> 8, y = hi >> 8, hit iff x^2 + y^2 < 2^48 (exact).
-__device__ __forceinline__ uint32_t mc_hit(uint32_t x, uint32_t y) {
-    const uint64_t xx = x >> 8, yy = y >> 8;
-    return (xx * xx + yy * yy) < (1ull << 48) ? 1u : 0u;
-}
-
-// Pairs consecutive words for the two-word consumers.  Steps A (words
-// 32k..32k+31) and B (32k+32..32k+63) hold 32 pairs (2m, 2m+1): even lanes
-// take pair l/2 from A, odd lanes pair 16 + l/2 from B, via one xor-shuffle.
-__device__ __forceinline__ void pair_words(uint32_t a, uint32_t b, bool odd, uint32_t& lo,
-                                           uint32_t& hi) {
-    const uint32_t give = odd ? a : b;
+// Word pairs (2m, 2m+1) of two consecutive steps A (words 32k..32k+31, in
+// `a`) and B (32k+32..32k+63, in `b`): even lanes take pair l/2 of A, odd
+// lanes pair 16 + l/2 of B, exchanging one word with the xor-1 partner.
+// Even lane: (lo, hi) = (a_l, a_{l+1}); odd lane: (b_{l-1}, b_l).
+//
+// f64 consumer: returns hi and lo >> 11 (funnel shifts fold the selects).
+__device__ __forceinline__ void pair_f64(uint32_t a, uint32_t b, const Lane& ln, uint32_t& lo11,
+                                         uint32_t& hi) {
+    const uint32_t give = funnel_r(b, a, ln.sh_own);   // odd: a, even: b
     const uint32_t got = __shfl_xor_sync(kFull, give, 1);
-    lo = odd ? got : a;
-    hi = odd ? b : got;
+    hi = funnel_r(got, b, ln.sh_own);                  // odd: b, even: got
+    lo11 = funnel_r(a, got, ln.sh_own + 11u);          // odd: got>>11, even: a>>11
+}
+
+// Monte Carlo consumer: x = lo >> 8, y = hi >> 8 (the predicate is symmetric,
+// so each lane needs {own word, partner word} >> 8 in either order).
+// Returns 1 when the sample MISSES: x^2 + y^2 >= 2^48.
+__device__ __forceinline__ uint32_t pair_mc_miss(uint32_t a, uint32_t b, const Lane& ln) {
+    const uint32_t give8 = funnel_r(b, a, ln.sh_own + 8u);   // odd: a>>8, even: b>>8
+    const uint32_t y = __shfl_xor_sync(kFull, give8, 1);
+    const uint32_t x = funnel_r(a, b, ln.sh_own + 8u);       // odd: b>>8, even: a>>8
+    const uint64_t q = static_cast<uint64_t>(x) * x + static_cast<uint64_t>(y) * y;  // < 2^49
+    return static_cast<uint32_t>(q >> 48);
 }
 
 // SplitMix64 draw k (1-based) from `seed` in closed form: the chain of
@@ -116,6 +152,16 @@ __device__ __forceinline__ uint64_t splitmix_draw(uint64_t seed, uint64_t k) {
     return z ^ (z >> 31);
 }
 
+__device__ __forceinline__ Lane make_lane(unsigned delta) {
+    Lane ln;
+    const unsigned lane = threadIdx.x & 31u;
+    ln.src = (lane + delta) & 31u;
+    ln.gives_J = lane >= delta;
+    const bool odd = lane & 1u;
+    ln.sh_own = odd ? 32u : 0u;
+    return ln;
+}
+
 // K1: XorgensState(params, seed) for stream g (proj/src/xorgens.cpp:19-32):
 // r SplitMix draws (lane-parallel, closed form), weyl = draw r+1, zero guard
 // (warp vote), then 4r = 512 discarded outputs = 16 warp steps.  The discarded
@@ -123,8 +169,8 @@ __device__ __forceinline__ uint64_t splitmix_draw(uint64_t seed, uint64_t k) {
 // advances the Weyl accumulator in closed form.
 template <class P>
 __global__ void __launch_bounds__(kThreads)
-seed_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32_t nstreams,
-            uint64_t seed0) {
+seed_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl,
+            uint32_t nstreams, uint64_t seed0) {
     const unsigned lane = threadIdx.x & 31;
     const uint32_t g = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     if (g >= nstreams) return;
@@ -135,39 +181,18 @@ seed_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32
     const uint32_t w0 = static_cast<uint32_t>(splitmix_draw(seed, kR + 1));
     const bool any = __any_sync(kFull, (R[0] | R[1] | R[2] | R[3]) != 0u);
     if (!any && lane == 0) R[0] = 0x7f4a7c15u;  // 0x9e3779b97f4a7c15 & mask (xorgens.cpp:28-29)
-    const unsigned src = (lane + p.delta) & 31u;
-    const bool gives_J = lane >= p.delta;
+    const Lane ln = make_lane(p.delta);
 #pragma unroll 1
     for (int it = 0; it < 4; ++it) {  // 16 steps = 4r words
-        warp_step<0>(R, p, src, gives_J);
-        warp_step<1>(R, p, src, gives_J);
-        warp_step<2>(R, p, src, gives_J);
-        warp_step<3>(R, p, src, gives_J);
+        warp_step<0, 0>(R, p, m, ln);
+        warp_step<1, 0>(R, p, m, ln);
+        warp_step<2, 0>(R, p, m, ln);
+        warp_step<3, 0>(R, p, m, ln);
     }
     uint32_t* w = win + static_cast<size_t>(g) * kR;
 #pragma unroll
     for (int j = 0; j < 4; ++j) w[32 * j + lane] = R[j];
     if (lane == 0) weyl[g] = w0 + 4u * kR * p.omega;
-}
-
-// Emits one step's word (single-word modes) at o[j].
-template <int MODE>
-__device__ __forceinline__ void emit1(void* o, int j, uint32_t word) {
-    if constexpr (MODE == kU32) {
-        __stcs(static_cast<uint32_t*>(o) + j, word);
-    } else if constexpr (MODE == kF32) {
-        __stcs(static_cast<float*>(o) + j, u32_to_f32(word));
-    }
-}
-
-// Emits (or counts) one pair at o[j] (two-word modes).
-template <int MODE>
-__device__ __forceinline__ void emit2(void* o, int j, uint32_t lo, uint32_t hi, uint32_t& hits) {
-    if constexpr (MODE == kF64) {
-        __stcs(static_cast<double*>(o) + j, pair_to_f64(lo, hi));
-    } else if constexpr (MODE == kMC) {
-        hits += mc_hit(lo, hi);
-    }
 }
 
 template <int MODE>
@@ -177,28 +202,48 @@ __device__ __forceinline__ void* advance(void* o, int n) {
     else return o;
 }
 
-// Four warp steps (one full register rotation) = 128 words of the stream,
-// emitted at cursor o.  Returns nothing; R, wl and hits are updated.
-template <int MODE, class P>
-__device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, unsigned src, bool gives_J,
-                                      bool odd, uint32_t& wl, uint32_t w_step, void* o,
-                                      uint32_t& hits) {
-    const uint32_t o0 = weyl_out(wl, warp_step<0>(R, p, src, gives_J), p);
-    const uint32_t o1 = weyl_out(wl + w_step, warp_step<1>(R, p, src, gives_J), p);
-    const uint32_t o2 = weyl_out(wl + 2u * w_step, warp_step<2>(R, p, src, gives_J), p);
-    const uint32_t o3 = weyl_out(wl + 3u * w_step, warp_step<3>(R, p, src, gives_J), p);
+// Four warp steps (one full register rotation) = 128 words of the stream.
+// Emits at cursor o (single-word modes: o[0], o[32], o[64], o[96]; pair modes:
+// o[0], o[32]) when EMIT; the tail variant masks by `limit` (values of this
+// body that are still wanted).
+template <int MODE, int VAR, bool TAIL, class P>
+__device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul& m, const Lane& ln,
+                                      uint32_t& wl, uint32_t w_step, void* o, uint32_t& miss,
+                                      unsigned limit) {
+    const uint32_t o0 = weyl_out<VAR>(wl, warp_step<0, VAR>(R, p, m, ln), p, m);
+    const uint32_t o1 = weyl_out<VAR>(wl + w_step, warp_step<1, VAR>(R, p, m, ln), p, m);
+    const uint32_t o2 = weyl_out<VAR>(wl + 2u * w_step, warp_step<2, VAR>(R, p, m, ln), p, m);
+    const uint32_t o3 = weyl_out<VAR>(wl + 3u * w_step, warp_step<3, VAR>(R, p, m, ln), p, m);
     wl += 4u * w_step;
-    if constexpr (MODE == kF64 || MODE == kMC) {
-        uint32_t lo, hi;
-        pair_words(o0, o1, odd, lo, hi);
-        emit2<MODE>(o, 0, lo, hi, hits);
-        pair_words(o2, o3, odd, lo, hi);
-        emit2<MODE>(o, 32, lo, hi, hits);
-    } else {
-        emit1<MODE>(o, 0, o0);
-        emit1<MODE>(o, 32, o1);
-        emit1<MODE>(o, 64, o2);
-        emit1<MODE>(o, 96, o3);
+    const unsigned lane = threadIdx.x & 31u;
+    if constexpr (MODE == kU32 || MODE == kF32) {
+        uint32_t* u = static_cast<uint32_t*>(o);
+        const uint32_t ov[4] = {o0, o1, o2, o3};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (!TAIL || lane + 32u * j < limit) {
+                if constexpr (MODE == kU32) __stcs(u + 32 * j, ov[j]);
+                else __stcs(reinterpret_cast<float*>(u) + 32 * j, u32_to_f32(ov[j]));
+            }
+        }
+    } else if constexpr (MODE == kF64) {
+        const unsigned mpair = (lane >> 1) + ((lane & 1u) << 4);
+        uint32_t lo11, hi;
+        pair_f64(o0, o1, ln, lo11, hi);
+        if (!TAIL || mpair < limit) __stcs(static_cast<double*>(o), pair_to_f64(lo11, hi));
+        pair_f64(o2, o3, ln, lo11, hi);
+        if (!TAIL || mpair + 32u < limit) __stcs(static_cast<double*>(o) + 32, pair_to_f64(lo11, hi));
+    } else if constexpr (MODE == kMC) {
+        const unsigned mpair = (lane >> 1) + ((lane & 1u) << 4);
+        const uint32_t m0 = pair_mc_miss(o0, o1, ln);
+        const uint32_t m1 = pair_mc_miss(o2, o3, ln);
+        if (!TAIL) {
+            miss += m0 + m1;
+        } else {
+            // samples past the limit count as neither hit nor miss; the
+            // caller subtracts only the samples that were wanted.
+            miss += (mpair < limit ? m0 : 0u) + (mpair + 32u < limit ? m1 : 0u);
+        }
     }
 }
 
@@ -208,11 +253,12 @@ __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, unsigned src
 //   kU32/kF32: out is stream-major with `words` values per stream, out[0] is
 //              stream g_begin's first value.
 //   kF64:      `words` must be even; words/2 doubles per stream.
-//   kMC:       `words` even; words/2 samples per stream; hit total added to *hits.
-template <class P, int MODE>
+//   kMC:       `words` even; words/2 samples per stream; the HIT total
+//              (samples - misses) is added to *hits_out.
+template <class P, int MODE, int VAR>
 __global__ void __launch_bounds__(kThreads)
-fill_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32_t g_begin,
-            uint32_t g_count, uint64_t words, void* __restrict__ out,
+fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl,
+            uint32_t g_begin, uint32_t g_count, uint64_t words, void* __restrict__ out,
             unsigned long long* __restrict__ hits_out) {
     const unsigned lane = threadIdx.x & 31;
     const uint32_t gl = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -227,21 +273,19 @@ fill_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32
     const uint32_t weyl0 = weyl[g];
     uint32_t wl = weyl0 + (lane + 1u) * p.omega;
     const uint32_t w_step = 32u * p.omega;
-    const unsigned src = (lane + p.delta) & 31u;
-    const bool gives_J = lane >= p.delta;
-    const bool odd = lane & 1u;
+    const Lane ln = make_lane(p.delta);
 
     // Output cursor: single-word modes index words, pair modes index pairs.
     const uint64_t per_stream_vals = kPairs ? (words >> 1) : words;
-    void* o = advance<MODE>(out, 0);
-    if constexpr (MODE != kMC && MODE != kSkip) {
+    void* o = out;
+    if constexpr (MODE == kU32 || MODE == kF32 || MODE == kF64) {
         const uint64_t first = static_cast<uint64_t>(gl) * per_stream_vals +
                                (kPairs ? ((lane >> 1) + ((lane & 1u) << 4)) : lane);
         if constexpr (MODE == kF64) o = static_cast<double*>(out) + first;
         else o = static_cast<uint32_t*>(out) + first;
     }
     constexpr int kValsPerBody = kPairs ? 64 : 128;
-    uint32_t hits = 0;
+    uint32_t miss = 0;
 
     uint64_t iters = words >> 7;  // 4 steps = 128 words per body
     while (iters != 0) {
@@ -249,13 +293,16 @@ fill_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32
         iters -= n;
         uint32_t i = 0;
 #pragma unroll 1
-        for (; i + 2 <= n; i += 2) {
-            body4<MODE>(R, p, src, gives_J, odd, wl, w_step, o, hits);
-            body4<MODE>(R, p, src, gives_J, odd, wl, w_step, advance<MODE>(o, kValsPerBody), hits);
-            o = advance<MODE>(o, 2 * kValsPerBody);
+        for (; i + 4 <= n; i += 4) {
+            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, o, miss, 0);
+            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, advance<MODE>(o, kValsPerBody), miss, 0);
+            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, advance<MODE>(o, 2 * kValsPerBody), miss, 0);
+            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, advance<MODE>(o, 3 * kValsPerBody), miss, 0);
+            o = advance<MODE>(o, 4 * kValsPerBody);
         }
-        if (i < n) {
-            body4<MODE>(R, p, src, gives_J, odd, wl, w_step, o, hits);
+#pragma unroll 1
+        for (; i < n; ++i) {
+            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, o, miss, 0);
             o = advance<MODE>(o, kValsPerBody);
         }
     }
@@ -265,24 +312,7 @@ fill_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32
         // One more (full) 4-step body; only the first `tail` words are
         // emitted.  The state saved below ends exactly at word `words`.
         const uint32_t O[4] = {R[0], R[1], R[2], R[3]};
-        const uint32_t o0 = weyl_out(wl, warp_step<0>(R, p, src, gives_J), p);
-        const uint32_t o1 = weyl_out(wl + w_step, warp_step<1>(R, p, src, gives_J), p);
-        const uint32_t o2 = weyl_out(wl + 2u * w_step, warp_step<2>(R, p, src, gives_J), p);
-        const uint32_t o3 = weyl_out(wl + 3u * w_step, warp_step<3>(R, p, src, gives_J), p);
-        if constexpr (kPairs) {
-            const unsigned tail_pairs = tail >> 1;
-            const unsigned m = (lane >> 1) + ((lane & 1u) << 4);
-            uint32_t lo, hi;
-            pair_words(o0, o1, odd, lo, hi);
-            if (m < tail_pairs) emit2<MODE>(o, 0, lo, hi, hits);
-            pair_words(o2, o3, odd, lo, hi);
-            if (m + 32 < tail_pairs) emit2<MODE>(o, 32, lo, hi, hits);
-        } else {
-            if (lane < tail) emit1<MODE>(o, 0, o0);
-            if (lane + 32 < tail) emit1<MODE>(o, 32, o1);
-            if (lane + 64 < tail) emit1<MODE>(o, 64, o2);
-            if (lane + 96 < tail) emit1<MODE>(o, 96, o3);
-        }
+        body4<MODE, VAR, true>(R, p, m, ln, wl, w_step, o, miss, kPairs ? tail >> 1 : tail);
         // New logical window = words [words-128, words): positions tail..tail+127
         // of the 256 words held in O (old window) followed by R (new block).
 #pragma unroll
@@ -297,10 +327,10 @@ fill_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32
     if (lane == 0) weyl[g] = weyl0 + static_cast<uint32_t>(words) * p.omega;
 
     if constexpr (MODE == kMC) {
-        unsigned long long t = hits;
+        unsigned long long t = miss;
 #pragma unroll
         for (int s = 16; s > 0; s >>= 1) t += __shfl_xor_sync(kFull, t, s);
-        if (lane == 0 && t) atomicAdd(hits_out, t);
+        if (lane == 0) atomicAdd(hits_out, static_cast<unsigned long long>(words >> 1) - t);
     }
 }
 

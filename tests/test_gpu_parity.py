@@ -279,3 +279,19 @@ def test_full_size_float_properties(oracle):
     assert float(d.min()) >= 0.0 and float(d.max()) < 1.0
     assert abs(float(d.mean()) - 0.5) < 1e-4
     assert np.array_equal(np_u32(d[:2]).view(np.uint64), o.fill_f64(n // 2).view(np.uint64))
+
+
+def test_cpp_dropin_against_reference():
+    """tests/cpp/dropin_test.cpp: the reference C++ API (its own sources) next
+    to xg::gpu on the same calls; built by oracle/Makefile where the reference
+    tree exists and shipped as oracle/_ref/dropin_test."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                       "dropin_test")
+    if not os.path.exists(exe):
+        pytest.skip("dropin_test not built (needs the reference tree at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "OK" in r.stdout
