@@ -290,7 +290,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="fill_u32",
-                    choices=["fill_u32", "fill_f32", "fill_f64", "fill_2p34", "mc_pi"])
+                    choices=["fill_u32", "fill_f32", "fill_f64", "fill_2p34", "mc_pi", "skip"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -312,7 +312,7 @@ def main():
     hbm_peak, peak_src = load_peaks()
 
     # workload geometry (per rank)
-    if wl in ("fill_u32", "fill_f32", "fill_f64"):
+    if wl in ("fill_u32", "fill_f32", "fill_f64", "skip"):
         P, per = 1 << 14, 1 << 16                       # 2^30 values per GPU (weak scaling)
         first, count = rank * P, P
         scaling = "weak"
@@ -328,7 +328,8 @@ def main():
     ens = xg.BlockEnsemble(p, 1, count, 63, first_stream=first, device=local)
 
     out = None
-    bytes_per_val = {"fill_u32": 4, "fill_f32": 4, "fill_f64": 8, "fill_2p34": 4, "mc_pi": 0}[wl]
+    bytes_per_val = {"fill_u32": 4, "fill_f32": 4, "fill_f64": 8, "fill_2p34": 4, "mc_pi": 0,
+                     "skip": 0}[wl]
     words_per_val = 2 if wl in ("fill_f64", "mc_pi") else 1
     if wl in ("fill_u32", "fill_2p34"):
         out = torch.empty((count, per), dtype=torch.uint32, device="cuda")
@@ -339,6 +340,9 @@ def main():
     elif wl == "fill_f64":
         out = torch.empty((count, per), dtype=torch.float64, device="cuda")
         fn = lambda: ens.fill_f64(per, out=out)  # noqa: E731
+    elif wl == "skip":  # generator core only (no stores): the integer-issue ceiling
+        hits = None
+        fn = lambda: ens.skip(per)  # noqa: E731
     else:
         hits = torch.zeros(1, dtype=torch.int64, device="cuda")
         fn = lambda: ens.mc_pi(per, hits=hits)  # noqa: E731
@@ -369,7 +373,8 @@ def main():
             "fill_f32": "uniform float32 [0,1) fill of 2^30 values per GPU, fused conversion",
             "fill_f64": "uniform float64 [0,1) fill of 2^30 values (2^31 words) per GPU, fused conversion",
             "fill_2p34": "disjoint-stream fill of 2^34 uint32 across N GPUs",
-            "mc_pi": "fused in-register Monte Carlo pi, 2^40 samples across N GPUs"}[wl],
+            "mc_pi": "fused in-register Monte Carlo pi, 2^40 samples across N GPUs",
+            "skip": "generator core only (advance 2^30 words, no stores)"}[wl],
             "params": "xorgensgp32 (128,65,15,14,12,17) w=32", "base_seed": 1,
             "streams_per_gpu": count, "values_per_stream": per,
             "layout": "block-major out[g*per_stream+k]",
@@ -392,6 +397,10 @@ def main():
                 result["roofline"]["write_only_probe_gbs"] = write_probe_gbs(out, stream)
             except OSError:
                 pass
+    elif wl == "skip":
+        result["roofline"] = {"bound": "int-issue", "achieved": value / world, "peak": None,
+                              "unit": "RN/s per GPU", "frac": None, "traffic": None,
+                              "kernel_ms_mean": kern_ms}
     else:
         # in-register consumer: report integer-issue context
         hits_v = int(hits.item())

@@ -122,9 +122,13 @@ int xg_fill_u64(xg_ensemble_t h, uint64_t per_stream, uint64_t* dev_out, xg_stre
 int xg_fill_f32(xg_ensemble_t h, uint64_t per_stream, float* dev_out, xg_stream_t stream);
 /* Uniform [0,1): f64 = (u64 >> 11) * 2^-53 with u64 as in xg_fill_u64. Exact. */
 int xg_fill_f64(xg_ensemble_t h, uint64_t per_stream, double* dev_out, xg_stream_t stream);
-/* Fused Monte Carlo pi: sample j of a stream uses words (2j, 2j+1) as
- * x = w >> 8, y = w' >> 8 and hits iff x^2 + y^2 < 2^48.  The hit count over
- * all streams is ADDED to *dev_hits (a device uint64).  No HBM traffic. */
+/* Fused in-register Monte Carlo pi.  samples_per_stream must be a multiple
+ * of 32 (XG_EINVAL otherwise): each stream supplies 2*samples_per_stream words
+ * in blocks of 64, block j giving the 32 samples (w[64j+i], w[64j+32+i]) --
+ * the two words one lane holds after two consecutive warp steps, so no word
+ * moves between lanes.  x = w >> 8, y = w' >> 8, hit iff x^2 + y^2 < 2^48
+ * (exact integer test).  The hit count over all streams is ADDED to
+ * *dev_hits (a device uint64).  No HBM traffic. */
 int xg_mc_pi(xg_ensemble_t h, uint64_t samples_per_stream, uint64_t* dev_hits,
              xg_stream_t stream);
 /* Advance every stream by `words` without storing (discard). */

@@ -109,8 +109,11 @@ class Oracle:
         return (u >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
 
     def mc_hits(self, words: np.ndarray) -> int:
-        w = words.astype(np.uint64).reshape(-1, 2) >> np.uint64(8)
-        return int(np.count_nonzero(w[:, 0] * w[:, 0] + w[:, 1] * w[:, 1] < np.uint64(1 << 48)))
+        """Hits over a stream prefix of 64k words: block j gives samples
+        (w[64j+i], w[64j+32+i])."""
+        w = (words.astype(np.uint64).reshape(-1, 2, 32) >> np.uint64(8))
+        x, y = w[:, 0, :], w[:, 1, :]
+        return int(np.count_nonzero(x * x + y * y < np.uint64(1 << 48)))
 
 
 class OracleEnsemble:
@@ -158,7 +161,8 @@ class OracleEnsemble:
 
     def mc_hits(self, samples: int) -> np.ndarray:
         out = np.empty(self.n, dtype=np.uint64)
-        self.o.lib.xgo_ensemble_mc_pi(self.buf, self.n, samples, _ptr(out), self.o.threads)
+        if self.o.lib.xgo_ensemble_mc_pi(self.buf, self.n, samples, _ptr(out), self.o.threads):
+            raise ValueError("samples per stream must be a multiple of 32")
         return out
 
     def checksums(self, n: int):

@@ -287,11 +287,13 @@ static void run_one(job_t* j, uint32_t g) {
         break;
     }
     case J_MC: {
+        /* blocks of 64 words, sample i of a block is
+         * (w[i], w[32+i]); samples_per_stream is a multiple of 32. */
         uint64_t hits = 0;
-        for (uint64_t k = 0; k < j->n; ++k) {
-            uint32_t x = (uint32_t)xgo_next_word(st);
-            uint32_t y = (uint32_t)xgo_next_word(st);
-            hits += (uint64_t)xgo_mc_hit(x, y);
+        uint32_t blk[64];
+        for (uint64_t k = 0; k < j->n / 32; ++k) {
+            for (int i = 0; i < 64; ++i) blk[i] = (uint32_t)xgo_next_word(st);
+            for (int i = 0; i < 32; ++i) hits += (uint64_t)xgo_mc_hit(blk[i], blk[32 + i]);
         }
         ((uint64_t*)j->out)[g] = hits;
         break;
@@ -392,6 +394,7 @@ int xgo_ensemble_fill_f64(xgo_state* states, uint32_t num_streams, uint64_t per_
 }
 int xgo_ensemble_mc_pi(xgo_state* states, uint32_t num_streams, uint64_t samples_per_stream,
                        uint64_t* hits_per_stream, int threads) {
+    if (samples_per_stream % 32 != 0) return -1;
     return fill(J_MC, states, num_streams, samples_per_stream, hits_per_stream, NULL, threads);
 }
 int xgo_ensemble_checksums(xgo_state* states, uint32_t num_streams, uint64_t n,

@@ -124,7 +124,7 @@ unsigned grid_for(uint32_t n) { return (n + kWarpsPerBlock - 1) / kWarpsPerBlock
 // bit 0 Weyl >> gamma, bit 1 t >> b, bit 2 t >> d as IMAD.HI on the FMA pipe.
 // Chosen per mode from the measurements in profiles/README.md; XG_VARIANT
 // overrides (experiments only).
-constexpr int kDefaultVar[5] = {1, 1, 1, 1, 1};
+constexpr int kDefaultVar[5] = {0, 0, 0, 0, 0};
 
 int variant_for(int mode) {
     static int forced = [] {
@@ -139,6 +139,7 @@ HiMul himul(const xg_params_t& p) {
     m.gamma = 1u << (32 - p.gamma);
     m.b = 1u << (32 - p.b);
     m.d = 1u << (32 - p.d);
+    m.eight = 1u << 24;
     return m;
 }
 
@@ -162,6 +163,8 @@ int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t wor
         case 3: return launch_fill_v<MODE, 3>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         case 5: return launch_fill_v<MODE, 5>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         case 7: return launch_fill_v<MODE, 7>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        case 8: return launch_fill_v<MODE, 8>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        case 9: return launch_fill_v<MODE, 9>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         default: return launch_fill_v<MODE, 1>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         }
     case kRtJ1:
@@ -428,6 +431,8 @@ int xg_fill_f64(xg_ensemble_t h, uint64_t per_stream, double* dev_out, xg_stream
 int xg_mc_pi(xg_ensemble_t h, uint64_t samples_per_stream, uint64_t* dev_hits,
              xg_stream_t stream) {
     if (!h || !dev_hits || (reinterpret_cast<uintptr_t>(dev_hits) % 8) != 0) return XG_EINVAL;
+    // Samples come in blocks of 32 per stream (64 words, one lane-pair of warp steps).
+    if (samples_per_stream % 32 != 0) return XG_EINVAL;
     if (samples_per_stream == 0) return XG_OK;
     DeviceGuard dg(h->device);
     if (!dg.ok) return XG_ECUDA;

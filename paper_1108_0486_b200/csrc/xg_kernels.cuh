@@ -60,6 +60,7 @@ struct RtParams {
 // Runtime multipliers for the IMAD.HI form of the right shifts.
 struct HiMul {
     uint32_t gamma, b, d;  // 2^(32-gamma), 2^(32-b), 2^(32-d)
+    uint32_t eight;        // 2^24 (MC coordinate shift)
 };
 
 enum Mode : int { kU32 = 0, kF32 = 1, kF64 = 2, kMC = 3, kSkip = 4 };
@@ -121,24 +122,26 @@ __device__ __forceinline__ double pair_to_f64(uint32_t lo_shr11, uint32_t hi) {
 // Word pairs (2m, 2m+1) of two consecutive steps A (words 32k..32k+31, in
 // `a`) and B (32k+32..32k+63, in `b`): even lanes take pair l/2 of A, odd
 // lanes pair 16 + l/2 of B, exchanging one word with the xor-1 partner.
-// Even lane: (lo, hi) = (a_l, a_{l+1}); odd lane: (b_{l-1}, b_l).
-//
-// f64 consumer: returns hi and lo >> 11 (funnel shifts fold the selects).
+// Even lane: (lo, hi) = (a_l, a_{l+1}); odd lane: (b_{l-1}, b_l).  The
+// selects are exact funnel shifts by 0 or 32 (one SHF.R.U64 each).
 __device__ __forceinline__ void pair_f64(uint32_t a, uint32_t b, const Lane& ln, uint32_t& lo11,
                                          uint32_t& hi) {
     const uint32_t give = funnel_r(b, a, ln.sh_own);   // odd: a, even: b
     const uint32_t got = __shfl_xor_sync(kFull, give, 1);
     hi = funnel_r(got, b, ln.sh_own);                  // odd: b, even: got
-    lo11 = funnel_r(a, got, ln.sh_own + 11u);          // odd: got>>11, even: a>>11
+    lo11 = funnel_r(a, got, ln.sh_own) >> 11;          // odd: got, even: a
 }
 
-// Monte Carlo consumer: x = lo >> 8, y = hi >> 8 (the predicate is symmetric,
-// so each lane needs {own word, partner word} >> 8 in either order).
-// Returns 1 when the sample MISSES: x^2 + y^2 >= 2^48.
-__device__ __forceinline__ uint32_t pair_mc_miss(uint32_t a, uint32_t b, const Lane& ln) {
-    const uint32_t give8 = funnel_r(b, a, ln.sh_own + 8u);   // odd: a>>8, even: b>>8
-    const uint32_t y = __shfl_xor_sync(kFull, give8, 1);
-    const uint32_t x = funnel_r(a, b, ln.sh_own + 8u);       // odd: b>>8, even: a>>8
+// Monte Carlo consumer, in-register: a lane pairs the two words it holds
+// after two consecutive warp steps, so block j of 64 stream words gives the
+// 32 samples (w[64j+i], w[64j+32+i]), i = 0..31, with
+// no data movement between lanes.  x = a >> 8, y = b >> 8; returns 1 when the
+// sample MISSES (x^2 + y^2 >= 2^48, exact in 64-bit).  HI: the >> 8 shifts run
+// as IMAD.HI on the FMA pipe instead of SHF on the ALU pipe.
+template <bool HI>
+__device__ __forceinline__ uint32_t mc_miss(uint32_t a, uint32_t b, uint32_t mul8) {
+    const uint32_t x = shr<HI>(a, 8, mul8);
+    const uint32_t y = shr<HI>(b, 8, mul8);
     const uint64_t q = static_cast<uint64_t>(x) * x + static_cast<uint64_t>(y) * y;  // < 2^49
     return static_cast<uint32_t>(q >> 48);
 }
@@ -234,15 +237,14 @@ __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul&
         pair_f64(o2, o3, ln, lo11, hi);
         if (!TAIL || mpair + 32u < limit) __stcs(static_cast<double*>(o) + 32, pair_to_f64(lo11, hi));
     } else if constexpr (MODE == kMC) {
-        const unsigned mpair = (lane >> 1) + ((lane & 1u) << 4);
-        const uint32_t m0 = pair_mc_miss(o0, o1, ln);
-        const uint32_t m1 = pair_mc_miss(o2, o3, ln);
+        // VAR bit 3: MC coordinate shifts on the FMA pipe.
+        const uint32_t m0 = mc_miss<(VAR & 8) != 0>(o0, o1, m.eight);
+        const uint32_t m1 = mc_miss<(VAR & 8) != 0>(o2, o3, m.eight);
         if (!TAIL) {
             miss += m0 + m1;
         } else {
-            // samples past the limit count as neither hit nor miss; the
-            // caller subtracts only the samples that were wanted.
-            miss += (mpair < limit ? m0 : 0u) + (mpair + 32u < limit ? m1 : 0u);
+            // limit = wanted 64-word blocks of this body (0 or 1).
+            miss += (limit > 0u ? m0 : 0u);
         }
     }
 }
@@ -253,8 +255,8 @@ __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul&
 //   kU32/kF32: out is stream-major with `words` values per stream, out[0] is
 //              stream g_begin's first value.
 //   kF64:      `words` must be even; words/2 doubles per stream.
-//   kMC:       `words` even; words/2 samples per stream; the HIT total
-//              (samples - misses) is added to *hits_out.
+//   kMC:       `words` a multiple of 64; words/2 samples per stream; the HIT
+//              total (samples - misses) is added to *hits_out.
 template <class P, int MODE, int VAR>
 __global__ void __launch_bounds__(kThreads)
 fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl,
@@ -312,7 +314,8 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
         // One more (full) 4-step body; only the first `tail` words are
         // emitted.  The state saved below ends exactly at word `words`.
         const uint32_t O[4] = {R[0], R[1], R[2], R[3]};
-        body4<MODE, VAR, true>(R, p, m, ln, wl, w_step, o, miss, kPairs ? tail >> 1 : tail);
+        body4<MODE, VAR, true>(R, p, m, ln, wl, w_step, o, miss,
+                               MODE == kMC ? tail >> 6 : (kPairs ? tail >> 1 : tail));
         // New logical window = words [words-128, words): positions tail..tail+127
         // of the 256 words held in O (old window) followed by R (new block).
 #pragma unroll

@@ -1,25 +1,32 @@
 #!/bin/bash
-# Correctness of every shift-placement variant + throughput per workload.
+# Correctness of the shift-placement variants + throughput per workload + ncu of MC.
 set -u
 TAG=${1:-var}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 timeout 900 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
-for V in 0 3 5 7; do
-  XG_VARIANT=$V timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "vs_oracle or golden or random" > $OUT/pytest_v$V.log 2>&1; echo "rc=$?" >> $OUT/pytest_v$V.log
+for V in 1 7 8 9; do
+  XG_VARIANT=$V timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "vs_oracle or golden or random or mc" > $OUT/pytest_v$V.log 2>&1; echo "rc=$?" >> $OUT/pytest_v$V.log
 done
-for W in fill_u32 fill_f32 fill_f64 mc_pi; do
-  for V in 0 1 3 5 7; do
-    S=100; [ $W = mc_pi ] && S=3
-    XG_VARIANT=$V timeout 300 python bench.py --workload $W --steps $S --warmup 3 --no-e2e --no-cpu > $OUT/b_${W}_v$V.json 2>> $OUT/bench.err
-    python - "$OUT/b_${W}_v$V.json" "$W" "$V" >> $OUT/summary.txt <<'PY'
+run() {  # workload variant steps
+  XG_VARIANT=$2 timeout 300 python bench.py --workload $1 --steps $3 --warmup 3 --no-e2e --no-cpu > $OUT/b_$1_v$2.json 2>> $OUT/bench.err
+  python - "$OUT/b_$1_v$2.json" "$1" "$2" >> $OUT/summary.txt <<'PY'
 import json,sys
 try:
     d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
-    print(sys.argv[2], "v"+sys.argv[3], "%.4e"%d["value"], "frac=%s"%(d.get("roofline",{}).get("frac")), "clk=%s"%d["clocks"].get("sm_mhz"), d["clocks"].get("reasons"))
+    print(sys.argv[2], "v"+sys.argv[3], "%.4e"%d["value"], "frac=%s"%(d.get("roofline",{}).get("frac")), "kms=%s"%(d.get("roofline",{}).get("kernel_ms_mean")), "clk=%s"%d["clocks"].get("sm_mhz"), d["clocks"].get("reasons"), "probe=%s"%d.get("roofline",{}).get("write_only_probe_gbs"))
 except Exception as e:
     print(sys.argv[2], sys.argv[3], "ERR", e)
 PY
-  done
+}
+for V in 0 1; do run fill_u32 $V 100; run fill_f32 $V 100; run fill_f64 $V 50; run skip $V 100; done
+for V in 0 1 8 9; do run mc_pi $V 3; done
+for V in 0 8; do
+  XG_VARIANT=$V timeout 600 ncu --set full --clock-control none --import-source on -k regex:fill_kernel -s 3 -c 1 \
+    -o $OUT/prof_mc_v$V python bench.py --workload mc_pi --steps 1 --warmup 3 --no-cpu > /dev/null 2>> $OUT/ncu.err
 done
+XG_VARIANT=0 timeout 600 ncu --set full --clock-control none --import-source on -k regex:fill_kernel -s 3 -c 1 \
+    -o $OUT/prof_skip_v0 python bench.py --workload skip --steps 1 --warmup 3 --no-cpu > /dev/null 2>> $OUT/ncu.err
+XG_VARIANT=0 timeout 600 ncu --set full --clock-control none --import-source on -k regex:fill_kernel -s 3 -c 1 \
+    -o $OUT/prof_f32_v0 python bench.py --workload fill_f32 --steps 1 --warmup 3 --no-cpu --no-e2e > /dev/null 2>> $OUT/ncu.err
 echo done > $OUT/DONE

@@ -1,0 +1,58 @@
+#!/usr/bin/env python3
+"""Summarise an ncu --set full report (raw page) into the metrics we cite.
+
+usage: python scripts/ncu_summary.py report.ncu-rep [label]  -> JSON on stdout
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "dram__bytes_write.sum.per_second", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__cycles_elapsed.avg.per_second", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+]
+
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1e-9, "us": 1e-6,
+        "ms": 1e-3, "s": 1, "byte/s": 1, "Kbyte/s": 1e3, "Mbyte/s": 1e6, "Gbyte/s": 1e9,
+        "Tbyte/s": 1e12, "hz": 1, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9}
+
+
+def main():
+    rep = sys.argv[1]
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    out = []
+    for vals in rows[2:]:
+        d = dict(zip(hdr, vals))
+        rec = {"kernel": d.get("Kernel Name", "")[:120]}
+        for k in KEYS:
+            if k in d:
+                u = units[hdr.index(k)]
+                try:
+                    v = float(d[k].replace(",", ""))
+                except ValueError:
+                    continue
+                rec[k] = v * UNIT.get(u, 1) if u in UNIT else v
+                if u and u not in UNIT and u != "%":
+                    rec[k + ".unit"] = u
+        if "dram__bytes_read.sum" in rec and "dram__bytes_write.sum" in rec:
+            rec["dram_bytes_per_launch"] = rec["dram__bytes_read.sum"] + rec["dram__bytes_write.sum"]
+        out.append(rec)
+    print(json.dumps(out if len(out) > 1 else out[0], indent=1))
+
+
+if __name__ == "__main__":
+    main()

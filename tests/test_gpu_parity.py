@@ -95,6 +95,7 @@ def test_fill_random_call_sequence(oracle):
             got = np_u32(e.fill_f64(n))
             assert np.array_equal(got.view(np.uint64), o.fill_f64(n).view(np.uint64))
         elif kind == 3:
+            n -= n % 32
             hits = e.mc_pi(n)
             assert int(hits.item()) == int(o.mc_hits(n).sum())
         else:
@@ -146,13 +147,28 @@ def test_golden_conversions(golden):
     assert int(h.item()) == g["mc_hits_128_samples"]
 
 
-@pytest.mark.parametrize("samples", [1, 31, 32, 33, 64, 1000, 65536 + 3])
+@pytest.mark.parametrize("samples", [32, 64, 96, 1024, 32 * 1001, 65536 + 32])
 def test_mc_pi_exact_vs_oracle(oracle, samples):
     e = xg.BlockEnsemble(GP32, 3, 19, 63)
     o = oracle.ensemble(3, 19)
     hits = e.mc_pi(samples)
     hits = e.mc_pi(samples, hits=hits)  # accumulates, continues streams
     assert int(hits.item()) == int(o.mc_hits(samples).sum() + o.mc_hits(samples).sum())
+
+
+def test_mc_pi_block_rule_and_continuation(oracle):
+    """Samples come in 64-word blocks (w[64j+i], w[64j+32+i]); a call must be
+    a multiple of 32 samples; MC and fills interleave on the same streams."""
+    e = xg.BlockEnsemble(GP32, 21, 3, 63)
+    with pytest.raises(ValueError):
+        e.mc_pi(33)
+    e.fill_u32(17)                      # leave the streams at a ragged position
+    words = oracle.ensemble(21, 3)
+    words.fill_u32(17)
+    w = words.fill_u32(64 * 5)          # the words MC will consume
+    want = sum(oracle.mc_hits(w[g]) for g in range(3))
+    assert int(e.mc_pi(160).item()) == want
+    assert np.array_equal(np_u32(e.fill_u32(50)), words.fill_u32(50))
 
 
 def test_from_raw_and_state_roundtrip(oracle, golden):
