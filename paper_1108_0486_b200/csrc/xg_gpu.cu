@@ -165,6 +165,8 @@ int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t wor
         case 7: return launch_fill_v<MODE, 7>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         case 8: return launch_fill_v<MODE, 8>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         case 9: return launch_fill_v<MODE, 9>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        case 16: return launch_fill_v<MODE, 16>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        case 17: return launch_fill_v<MODE, 17>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         default: return launch_fill_v<MODE, 1>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         }
     case kRtJ1:

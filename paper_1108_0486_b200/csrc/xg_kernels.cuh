@@ -81,6 +81,11 @@ struct Lane {
     unsigned src;      // shuffle source lane for the s-tap
     bool gives_J;      // this lane provides register J (else J+1) to the s-tap shuffle
     uint32_t sh_own;   // 32 on odd lanes, 0 on even: funnel shift for the pair consumers
+    // VAR bit 4 (shared-memory s-tap): the warp's 128-word ring mirrors the
+    // register window, block j of rotation position S at ring slot (S+j)&3;
+    // the s-tap W[(r-s)+l] is ring[(32S + (r-s) + l) & 127].
+    uint32_t* ring;
+    unsigned ld[4];
 };
 
 // One warp step on the register window.  S is the position in the 4-step
@@ -92,13 +97,24 @@ __device__ __forceinline__ uint32_t warp_step(uint32_t (&R)[4], const P& p, cons
     constexpr int i0 = S & 3;
     constexpr int iJ = (S + P::J) & 3;
     constexpr int iJ1 = (S + P::J + 1) & 3;
-    const uint32_t give = ln.gives_J ? R[iJ] : R[iJ1];
-    const uint32_t y = __shfl_sync(kFull, give, ln.src);
+    uint32_t y;
+    if constexpr ((VAR & 16) != 0) {
+        y = ln.ring[ln.ld[S & 3]];  // written >= 2 steps ago, published by __syncwarp
+    } else {
+        const uint32_t give = ln.gives_J ? R[iJ] : R[iJ1];
+        y = __shfl_sync(kFull, give, ln.src);
+    }
     const uint32_t x = R[i0];
     const uint32_t t1 = x ^ (x << p.a);
     const uint32_t t2 = y ^ (y << p.c);
     const uint32_t v = t1 ^ shr<(VAR & 2) != 0>(t1, p.b, m.b) ^ t2 ^ shr<(VAR & 4) != 0>(t2, p.d, m.d);
     R[i0] = v;  // newest block; the old block 0 is no longer needed
+    if constexpr ((VAR & 16) != 0) {
+        ln.ring[32 * (S & 3) + (threadIdx.x & 31u)] = v;
+        // Reads at step S see writes of steps <= S-2, so publishing after
+        // every odd step suffices.
+        if constexpr ((S & 1) == 1) __syncwarp();
+    }
     return v;
 }
 
@@ -155,13 +171,16 @@ __device__ __forceinline__ uint64_t splitmix_draw(uint64_t seed, uint64_t k) {
     return z ^ (z >> 31);
 }
 
-__device__ __forceinline__ Lane make_lane(unsigned delta) {
+__device__ __forceinline__ Lane make_lane(unsigned delta, unsigned q) {  // q = r - s
     Lane ln;
     const unsigned lane = threadIdx.x & 31u;
     ln.src = (lane + delta) & 31u;
     ln.gives_J = lane >= delta;
     const bool odd = lane & 1u;
     ln.sh_own = odd ? 32u : 0u;
+    ln.ring = nullptr;
+#pragma unroll
+    for (int S = 0; S < 4; ++S) ln.ld[S] = (32u * S + q + lane) & 127u;
     return ln;
 }
 
@@ -184,7 +203,7 @@ seed_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
     const uint32_t w0 = static_cast<uint32_t>(splitmix_draw(seed, kR + 1));
     const bool any = __any_sync(kFull, (R[0] | R[1] | R[2] | R[3]) != 0u);
     if (!any && lane == 0) R[0] = 0x7f4a7c15u;  // 0x9e3779b97f4a7c15 & mask (xorgens.cpp:28-29)
-    const Lane ln = make_lane(p.delta);
+    const Lane ln = make_lane(p.delta, 32u * P::J + p.delta);
 #pragma unroll 1
     for (int it = 0; it < 4; ++it) {  // 16 steps = 4r words
         warp_step<0, 0>(R, p, m, ln);
@@ -275,7 +294,14 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
     const uint32_t weyl0 = weyl[g];
     uint32_t wl = weyl0 + (lane + 1u) * p.omega;
     const uint32_t w_step = 32u * p.omega;
-    const Lane ln = make_lane(p.delta);
+    Lane ln = make_lane(p.delta, 32u * P::J + p.delta);
+    if constexpr ((VAR & 16) != 0) {
+        __shared__ uint32_t ring[kWarpsPerBlock][kR];
+        ln.ring = ring[threadIdx.x >> 5];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ln.ring[32 * j + lane] = R[j];
+        __syncwarp();
+    }
 
     // Output cursor: single-word modes index words, pair modes index pairs.
     const uint64_t per_stream_vals = kPairs ? (words >> 1) : words;
