@@ -126,8 +126,9 @@ int xg_fill_f64(xg_ensemble_t h, uint64_t per_stream, double* dev_out, xg_stream
  * of 32 (XG_EINVAL otherwise): each stream supplies 2*samples_per_stream words
  * in blocks of 64, block j giving the 32 samples (w[64j+i], w[64j+32+i]) --
  * the two words one lane holds after two consecutive warp steps, so no word
- * moves between lanes.  x = w >> 8, y = w' >> 8, hit iff x^2 + y^2 < 2^48
- * (exact integer test).  The hit count over all streams is ADDED to
+ * moves between lanes.  Each word read as a signed 32-bit coordinate in
+ * [-2^31, 2^31); hit iff x^2 + y^2 < 2^62 (exact integer test, the unit disc
+ * in the square [-1, 1)^2, P(hit) = pi/4).  The hit count over all streams is ADDED to
  * *dev_hits (a device uint64).  No HBM traffic. */
 int xg_mc_pi(xg_ensemble_t h, uint64_t samples_per_stream, uint64_t* dev_hits,
              xg_stream_t stream);

@@ -111,9 +111,10 @@ class Oracle:
     def mc_hits(self, words: np.ndarray) -> int:
         """Hits over a stream prefix of 64k words: block j gives samples
         (w[64j+i], w[64j+32+i])."""
-        w = (words.astype(np.uint64).reshape(-1, 2, 32) >> np.uint64(8))
+        w = words.astype(np.uint32).view(np.int32).astype(np.int64).reshape(-1, 2, 32)
         x, y = w[:, 0, :], w[:, 1, :]
-        return int(np.count_nonzero(x * x + y * y < np.uint64(1 << 48)))
+        q = (x * x).astype(np.uint64) + (y * y).astype(np.uint64)
+        return int(np.count_nonzero(q < np.uint64(1 << 62)))
 
 
 class OracleEnsemble:

@@ -237,9 +237,12 @@ double xgo_u32pair_to_f64(uint32_t lo, uint32_t hi) {
     return (double)(xgo_u32pair_to_u64(lo, hi) >> 11) * 0x1.0p-53;
 }
 
+/* Words read as signed 32-bit coordinates in [-2^31, 2^31): hit iff the
+ * point lies inside the disc x^2 + y^2 < 2^62 (exact; sum <= 2^63). */
 int xgo_mc_hit(uint32_t x, uint32_t y) {
-    uint64_t xs = x >> 8, ys = y >> 8;
-    return xs * xs + ys * ys < (UINT64_C(1) << 48);
+    int64_t xs = (int32_t)x, ys = (int32_t)y;
+    uint64_t q = (uint64_t)(xs * xs) + (uint64_t)(ys * ys);
+    return q < (UINT64_C(1) << 62);
 }
 
 /* ---- block ensemble: proj/src/parallel.cpp:84-135 ----------------------- */

@@ -124,7 +124,7 @@ unsigned grid_for(uint32_t n) { return (n + kWarpsPerBlock - 1) / kWarpsPerBlock
 // bit 0 Weyl >> gamma, bit 1 t >> b, bit 2 t >> d as IMAD.HI on the FMA pipe.
 // Chosen per mode from the measurements in profiles/README.md; XG_VARIANT
 // overrides (experiments only).
-constexpr int kDefaultVar[5] = {0, 0, 0, 0, 0};
+constexpr int kDefaultVar[5] = {16, 16, 16, 16, 16};
 
 int variant_for(int mode) {
     static int forced = [] {
@@ -139,7 +139,6 @@ HiMul himul(const xg_params_t& p) {
     m.gamma = 1u << (32 - p.gamma);
     m.b = 1u << (32 - p.b);
     m.d = 1u << (32 - p.d);
-    m.eight = 1u << 24;
     return m;
 }
 
@@ -163,8 +162,6 @@ int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t wor
         case 3: return launch_fill_v<MODE, 3>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         case 5: return launch_fill_v<MODE, 5>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         case 7: return launch_fill_v<MODE, 7>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-        case 8: return launch_fill_v<MODE, 8>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-        case 9: return launch_fill_v<MODE, 9>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         case 16: return launch_fill_v<MODE, 16>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         case 17: return launch_fill_v<MODE, 17>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         default: return launch_fill_v<MODE, 1>(GP32{}, h, g_begin, g_count, words, out, hits, s);

@@ -60,7 +60,6 @@ struct RtParams {
 // Runtime multipliers for the IMAD.HI form of the right shifts.
 struct HiMul {
     uint32_t gamma, b, d;  // 2^(32-gamma), 2^(32-b), 2^(32-d)
-    uint32_t eight;        // 2^24 (MC coordinate shift)
 };
 
 enum Mode : int { kU32 = 0, kF32 = 1, kF64 = 2, kMC = 3, kSkip = 4 };
@@ -151,15 +150,17 @@ __device__ __forceinline__ void pair_f64(uint32_t a, uint32_t b, const Lane& ln,
 // Monte Carlo consumer, in-register: a lane pairs the two words it holds
 // after two consecutive warp steps, so block j of 64 stream words gives the
 // 32 samples (w[64j+i], w[64j+32+i]), i = 0..31, with
-// no data movement between lanes.  x = a >> 8, y = b >> 8; returns 1 when the
-// sample MISSES (x^2 + y^2 >= 2^48, exact in 64-bit).  HI: the >> 8 shifts run
-// as IMAD.HI on the FMA pipe instead of SHF on the ALU pipe.
-template <bool HI>
-__device__ __forceinline__ uint32_t mc_miss(uint32_t a, uint32_t b, uint32_t mul8) {
-    const uint32_t x = shr<HI>(a, 8, mul8);
-    const uint32_t y = shr<HI>(b, 8, mul8);
-    const uint64_t q = static_cast<uint64_t>(x) * x + static_cast<uint64_t>(y) * y;  // < 2^49
-    return static_cast<uint32_t>(q >> 48);
+// no data movement between lanes.  Each word, read as a signed 32-bit integer,
+// is a coordinate in [-2^31, 2^31); the sample hits the disc iff
+// x^2 + y^2 < 2^62 (exact: q = x^2 - 2^62 + y^2 lies in [-2^62, 2^62]).
+// Returns 1 for a HIT (the sign bit of q).  Per sample: IMAD.WIDE, IMAD.HI and
+// one add -- no shifts, no selects.
+__device__ __forceinline__ uint32_t mc_hit(uint32_t a, uint32_t b) {
+    const int64_t x = static_cast<int32_t>(a), y = static_cast<int32_t>(b);
+    // x^2 + y^2 <= 2^63 fits in uint64; hit iff its high word is < 2^30,
+    // i.e. iff (high word - 2^30), in [-2^30, 2^30], has its sign bit set.
+    const uint64_t q = static_cast<uint64_t>(x * x) + static_cast<uint64_t>(y * y);
+    return (static_cast<uint32_t>(q >> 32) - 0x40000000u) >> 31;
 }
 
 // SplitMix64 draw k (1-based) from `seed` in closed form: the chain of
@@ -230,7 +231,7 @@ __device__ __forceinline__ void* advance(void* o, int n) {
 // body that are still wanted).
 template <int MODE, int VAR, bool TAIL, class P>
 __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul& m, const Lane& ln,
-                                      uint32_t& wl, uint32_t w_step, void* o, uint32_t& miss,
+                                      uint32_t& wl, uint32_t w_step, void* o, uint32_t& hits,
                                       unsigned limit) {
     const uint32_t o0 = weyl_out<VAR>(wl, warp_step<0, VAR>(R, p, m, ln), p, m);
     const uint32_t o1 = weyl_out<VAR>(wl + w_step, warp_step<1, VAR>(R, p, m, ln), p, m);
@@ -256,14 +257,13 @@ __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul&
         pair_f64(o2, o3, ln, lo11, hi);
         if (!TAIL || mpair + 32u < limit) __stcs(static_cast<double*>(o) + 32, pair_to_f64(lo11, hi));
     } else if constexpr (MODE == kMC) {
-        // VAR bit 3: MC coordinate shifts on the FMA pipe.
-        const uint32_t m0 = mc_miss<(VAR & 8) != 0>(o0, o1, m.eight);
-        const uint32_t m1 = mc_miss<(VAR & 8) != 0>(o2, o3, m.eight);
+        const uint32_t h0 = mc_hit(o0, o1);
+        const uint32_t h1 = mc_hit(o2, o3);
         if (!TAIL) {
-            miss += m0 + m1;
+            hits += h0 + h1;
         } else {
             // limit = wanted 64-word blocks of this body (0 or 1).
-            miss += (limit > 0u ? m0 : 0u);
+            hits += (limit > 0u ? h0 : 0u);
         }
     }
 }
@@ -274,8 +274,8 @@ __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul&
 //   kU32/kF32: out is stream-major with `words` values per stream, out[0] is
 //              stream g_begin's first value.
 //   kF64:      `words` must be even; words/2 doubles per stream.
-//   kMC:       `words` a multiple of 64; words/2 samples per stream; the HIT
-//              total (samples - misses) is added to *hits_out.
+//   kMC:       `words` a multiple of 64; words/2 samples per stream; the hit
+//              total is added to *hits_out.
 template <class P, int MODE, int VAR>
 __global__ void __launch_bounds__(kThreads)
 fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl,
@@ -313,7 +313,7 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
         else o = static_cast<uint32_t*>(out) + first;
     }
     constexpr int kValsPerBody = kPairs ? 64 : 128;
-    uint32_t miss = 0;
+    uint32_t hits = 0;
 
     uint64_t iters = words >> 7;  // 4 steps = 128 words per body
     while (iters != 0) {
@@ -322,15 +322,15 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
         uint32_t i = 0;
 #pragma unroll 1
         for (; i + 4 <= n; i += 4) {
-            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, o, miss, 0);
-            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, advance<MODE>(o, kValsPerBody), miss, 0);
-            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, advance<MODE>(o, 2 * kValsPerBody), miss, 0);
-            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, advance<MODE>(o, 3 * kValsPerBody), miss, 0);
+            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, o, hits, 0);
+            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, advance<MODE>(o, kValsPerBody), hits, 0);
+            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, advance<MODE>(o, 2 * kValsPerBody), hits, 0);
+            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, advance<MODE>(o, 3 * kValsPerBody), hits, 0);
             o = advance<MODE>(o, 4 * kValsPerBody);
         }
 #pragma unroll 1
         for (; i < n; ++i) {
-            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, o, miss, 0);
+            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, o, hits, 0);
             o = advance<MODE>(o, kValsPerBody);
         }
     }
@@ -340,7 +340,7 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
         // One more (full) 4-step body; only the first `tail` words are
         // emitted.  The state saved below ends exactly at word `words`.
         const uint32_t O[4] = {R[0], R[1], R[2], R[3]};
-        body4<MODE, VAR, true>(R, p, m, ln, wl, w_step, o, miss,
+        body4<MODE, VAR, true>(R, p, m, ln, wl, w_step, o, hits,
                                MODE == kMC ? tail >> 6 : (kPairs ? tail >> 1 : tail));
         // New logical window = words [words-128, words): positions tail..tail+127
         // of the 256 words held in O (old window) followed by R (new block).
@@ -356,10 +356,10 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
     if (lane == 0) weyl[g] = weyl0 + static_cast<uint32_t>(words) * p.omega;
 
     if constexpr (MODE == kMC) {
-        unsigned long long t = miss;
+        unsigned long long t = hits;
 #pragma unroll
         for (int s = 16; s > 0; s >>= 1) t += __shfl_xor_sync(kFull, t, s);
-        if (lane == 0) atomicAdd(hits_out, static_cast<unsigned long long>(words >> 1) - t);
+        if (lane == 0 && t != 0) atomicAdd(hits_out, t);
     }
 }
 
