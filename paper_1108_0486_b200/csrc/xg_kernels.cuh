@@ -85,6 +85,7 @@ struct Lane {
     // the s-tap W[(r-s)+l] is ring[(32S + (r-s) + l) & 127].
     uint32_t* ring;
     unsigned ld[4];
+    uint32_t* stage;   // f64 with VAR bit 4: 2 x 64-word output staging for word pairs
 };
 
 // One warp step on the register window.  S is the position in the 4-step
@@ -123,9 +124,20 @@ __device__ __forceinline__ uint32_t weyl_out(uint32_t w, uint32_t v, const P& p,
     return (w ^ shr<(VAR & 1) != 0>(w, p.gamma, m.gamma)) + v;
 }
 
-// Uniform float: (u >> 8) * 2^-24, exact.
+// Uniform float: (u >> 8) * 2^-24, exact.  The
+// conversion of a 24-bit integer is exact in every rounding mode; the _rd
+// form compiles to I2F.U32.RM (XU pipe) instead of I2FP (ALU pipe), which is
+// the busiest pipe of this kernel.
 __device__ __forceinline__ float u32_to_f32(uint32_t u) {
-    return __uint2float_rn(u >> 8) * 0x1p-24f;
+    return __uint2float_rd(u >> 8) * 0x1p-24f;
+}
+
+// Uniform double from raw (lo, hi) on the FP64 pipe, no integer shift:
+// t = RD(lo * 2^-11 + 2^52) = 2^52 + (lo >> 11) exactly (ulp 1 in [2^52, 2^53));
+// t * 2^-53 - 0.5 = (lo >> 11) * 2^-53 exactly; + hi * 2^-32 exact.
+__device__ __forceinline__ double raw_pair_to_f64(uint32_t lo, uint32_t hi) {
+    const double t = __fma_rd(__uint2double_rn(lo), 0x1p-11, 0x1p52);
+    return __fma_rn(__uint2double_rn(hi), 0x1p-32, __fma_rn(t, 0x1p-53, -0.5));
 }
 
 // Uniform double from hi and (lo >> 11): (u64 >> 11) * 2^-53 with
@@ -180,6 +192,7 @@ __device__ __forceinline__ Lane make_lane(unsigned delta, unsigned q) {  // q = 
     const bool odd = lane & 1u;
     ln.sh_own = odd ? 32u : 0u;
     ln.ring = nullptr;
+    ln.stage = nullptr;
 #pragma unroll
     for (int S = 0; S < 4; ++S) ln.ld[S] = (32u * S + q + lane) & 127u;
     return ln;
@@ -249,6 +262,21 @@ __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul&
                 else __stcs(reinterpret_cast<float*>(u) + 32 * j, u32_to_f32(ov[j]));
             }
         }
+    } else if constexpr (MODE == kF64 && (VAR & 16) != 0) {
+        // Pairs through shared memory: the 64 outputs of two steps are staged
+        // in order, then lane l reads words (2l, 2l+1) with one LDS.64 --
+        // value 32*pair + l in natural order, no shuffles or selects.
+        uint32_t* st = ln.stage;
+        st[lane] = o0;
+        st[32 + lane] = o1;
+        st[64 + lane] = o2;
+        st[96 + lane] = o3;
+        __syncwarp();
+        const uint2 pa = reinterpret_cast<const uint2*>(st)[lane];
+        const uint2 pb = reinterpret_cast<const uint2*>(st + 64)[lane];
+        __syncwarp();  // the next body rewrites the stage
+        if (!TAIL || lane < limit) __stcs(static_cast<double*>(o), raw_pair_to_f64(pa.x, pa.y));
+        if (!TAIL || lane + 32u < limit) __stcs(static_cast<double*>(o) + 32, raw_pair_to_f64(pb.x, pb.y));
     } else if constexpr (MODE == kF64) {
         const unsigned mpair = (lane >> 1) + ((lane & 1u) << 4);
         uint32_t lo11, hi;
@@ -301,14 +329,19 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
 #pragma unroll
         for (int j = 0; j < 4; ++j) ln.ring[32 * j + lane] = R[j];
         __syncwarp();
+        if constexpr (MODE == kF64) {
+            __shared__ __align__(16) uint32_t stage[kWarpsPerBlock][128];
+            ln.stage = stage[threadIdx.x >> 5];
+        }
     }
 
     // Output cursor: single-word modes index words, pair modes index pairs.
     const uint64_t per_stream_vals = kPairs ? (words >> 1) : words;
     void* o = out;
     if constexpr (MODE == kU32 || MODE == kF32 || MODE == kF64) {
+        constexpr bool kShuffledPairs = kPairs && (VAR & 16) == 0;
         const uint64_t first = static_cast<uint64_t>(gl) * per_stream_vals +
-                               (kPairs ? ((lane >> 1) + ((lane & 1u) << 4)) : lane);
+                               (kShuffledPairs ? ((lane >> 1) + ((lane & 1u) << 4)) : lane);
         if constexpr (MODE == kF64) o = static_cast<double*>(out) + first;
         else o = static_cast<uint32_t*>(out) + first;
     }
