@@ -132,12 +132,12 @@ __device__ __forceinline__ float u32_to_f32(uint32_t u) {
     return __uint2float_rd(u >> 8) * 0x1p-24f;
 }
 
-// Uniform double from raw (lo, hi) on the FP64 pipe, no integer shift:
-// t = RD(lo * 2^-11 + 2^52) = 2^52 + (lo >> 11) exactly (ulp 1 in [2^52, 2^53));
-// t * 2^-53 - 0.5 = (lo >> 11) * 2^-53 exactly; + hi * 2^-32 exact.
+// Uniform double from raw (lo, hi): clearing the low 11 bits leaves a value
+// (u64 >> 11) << 11 with at most 53 significant bits, so the u64 -> f64
+// conversion is exact and so is the scaling by 2^-64.
 __device__ __forceinline__ double raw_pair_to_f64(uint32_t lo, uint32_t hi) {
-    const double t = __fma_rd(__uint2double_rn(lo), 0x1p-11, 0x1p52);
-    return __fma_rn(__uint2double_rn(hi), 0x1p-32, __fma_rn(t, 0x1p-53, -0.5));
+    const uint64_t u = (static_cast<uint64_t>(hi) << 32) | (lo & ~0x7ffu);
+    return __ull2double_rz(u) * 0x1p-64;
 }
 
 // Uniform double from hi and (lo >> 11): (u64 >> 11) * 2^-53 with
@@ -242,7 +242,7 @@ __device__ __forceinline__ void* advance(void* o, int n) {
 // Emits at cursor o (single-word modes: o[0], o[32], o[64], o[96]; pair modes:
 // o[0], o[32]) when EMIT; the tail variant masks by `limit` (values of this
 // body that are still wanted).
-template <int MODE, int VAR, bool TAIL, class P>
+template <int MODE, int VAR, bool TAIL, int BUF = 0, class P>
 __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul& m, const Lane& ln,
                                       uint32_t& wl, uint32_t w_step, void* o, uint32_t& hits,
                                       unsigned limit) {
@@ -266,7 +266,9 @@ __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul&
         // Pairs through shared memory: the 64 outputs of two steps are staged
         // in order, then lane l reads words (2l, 2l+1) with one LDS.64 --
         // value 32*pair + l in natural order, no shuffles or selects.
-        uint32_t* st = ln.stage;
+        // Two stage buffers alternate between consecutive bodies (BUF), so the
+        // publishing __syncwarp of body k+1 also retires body k's reads.
+        uint32_t* st = ln.stage + 128 * BUF;
         st[lane] = o0;
         st[32 + lane] = o1;
         st[64 + lane] = o2;
@@ -274,7 +276,6 @@ __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul&
         __syncwarp();
         const uint2 pa = reinterpret_cast<const uint2*>(st)[lane];
         const uint2 pb = reinterpret_cast<const uint2*>(st + 64)[lane];
-        __syncwarp();  // the next body rewrites the stage
         if (!TAIL || lane < limit) __stcs(static_cast<double*>(o), raw_pair_to_f64(pa.x, pa.y));
         if (!TAIL || lane + 32u < limit) __stcs(static_cast<double*>(o) + 32, raw_pair_to_f64(pb.x, pb.y));
     } else if constexpr (MODE == kF64) {
@@ -330,7 +331,7 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
         for (int j = 0; j < 4; ++j) ln.ring[32 * j + lane] = R[j];
         __syncwarp();
         if constexpr (MODE == kF64) {
-            __shared__ __align__(16) uint32_t stage[kWarpsPerBlock][128];
+            __shared__ __align__(16) uint32_t stage[kWarpsPerBlock][256];
             ln.stage = stage[threadIdx.x >> 5];
         }
     }
@@ -355,15 +356,17 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
         uint32_t i = 0;
 #pragma unroll 1
         for (; i + 4 <= n; i += 4) {
-            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, o, hits, 0);
-            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, advance<MODE>(o, kValsPerBody), hits, 0);
-            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, advance<MODE>(o, 2 * kValsPerBody), hits, 0);
-            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, advance<MODE>(o, 3 * kValsPerBody), hits, 0);
+            body4<MODE, VAR, false, 0>(R, p, m, ln, wl, w_step, o, hits, 0);
+            body4<MODE, VAR, false, 1>(R, p, m, ln, wl, w_step, advance<MODE>(o, kValsPerBody), hits, 0);
+            body4<MODE, VAR, false, 0>(R, p, m, ln, wl, w_step, advance<MODE>(o, 2 * kValsPerBody), hits, 0);
+            body4<MODE, VAR, false, 1>(R, p, m, ln, wl, w_step, advance<MODE>(o, 3 * kValsPerBody), hits, 0);
             o = advance<MODE>(o, 4 * kValsPerBody);
         }
+        if constexpr (MODE == kF64) __syncwarp();  // retire stage reads before reuse
 #pragma unroll 1
         for (; i < n; ++i) {
-            body4<MODE, VAR, false>(R, p, m, ln, wl, w_step, o, hits, 0);
+            body4<MODE, VAR, false, 0>(R, p, m, ln, wl, w_step, o, hits, 0);
+            if constexpr (MODE == kF64) __syncwarp();
             o = advance<MODE>(o, kValsPerBody);
         }
     }
@@ -372,6 +375,7 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
     if (tail != 0) {
         // One more (full) 4-step body; only the first `tail` words are
         // emitted.  The state saved below ends exactly at word `words`.
+        if constexpr (MODE == kF64) __syncwarp();
         const uint32_t O[4] = {R[0], R[1], R[2], R[3]};
         body4<MODE, VAR, true>(R, p, m, ln, wl, w_step, o, hits,
                                MODE == kMC ? tail >> 6 : (kPairs ? tail >> 1 : tail));
