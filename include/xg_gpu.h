@@ -118,6 +118,11 @@ int xg_fill_u32(xg_ensemble_t h, uint64_t per_stream, uint32_t* dev_out, xg_stre
 /* Two consecutive words per value, lo = first: value = w[2k] | w[2k+1] << 32
  * (the raw-le stream read as little-endian uint64).  Not in the reference. */
 int xg_fill_u64(xg_ensemble_t h, uint64_t per_stream, uint64_t* dev_out, xg_stream_t stream);
+/* The Weyl-ablated linear stream: RawXorgens::next() = step_linear()
+ * (proj/include/xg/baselines.hpp:60-71, registry id "xorgens-raw",
+ * proj/src/registry.cpp:29-30) -- same seeding, output x_i, and the Weyl
+ * accumulator is left unchanged.  Same layout as xg_fill_u32. */
+int xg_fill_raw_u32(xg_ensemble_t h, uint64_t per_stream, uint32_t* dev_out, xg_stream_t stream);
 /* Uniform [0,1): f32 = (word >> 8) * 2^-24, one word per value.  Exact. */
 int xg_fill_f32(xg_ensemble_t h, uint64_t per_stream, float* dev_out, xg_stream_t stream);
 /* Uniform [0,1): f64 = (u64 >> 11) * 2^-53 with u64 as in xg_fill_u64. Exact. */

@@ -60,7 +60,7 @@ class Oracle:
         L.xgo_stream_u32.argtypes = [ctypes.POINTER(Params), _u64, _u64, _vp]
         L.xgo_ensemble_seed.argtypes = [_vp, ctypes.POINTER(Params), _u64, _u64, _u32, _int]
         for n in ("xgo_ensemble_fill_u32", "xgo_ensemble_fill_f32", "xgo_ensemble_fill_f64",
-                  "xgo_ensemble_mc_pi"):
+                  "xgo_ensemble_mc_pi", "xgo_ensemble_fill_raw_u32"):
             getattr(L, n).argtypes = [_vp, _u32, _u64, _vp, _int]
         L.xgo_ensemble_checksums.argtypes = [_vp, _u32, _u64, _vp, _vp, _int]
         L.xgo_batch_step.argtypes = [_vp, ctypes.c_uint, _vp]
@@ -150,6 +150,11 @@ class OracleEnsemble:
         self.o.lib.xgo_ensemble_fill_u32(self.buf, self.n, per_stream, _ptr(out), self.o.threads)
         return out
 
+    def fill_raw_u32(self, per_stream: int) -> np.ndarray:
+        out = np.empty((self.n, per_stream), dtype=np.uint32)
+        self.o.lib.xgo_ensemble_fill_raw_u32(self.buf, self.n, per_stream, _ptr(out), self.o.threads)
+        return out
+
     def fill_f32(self, per_stream: int) -> np.ndarray:
         out = np.empty((self.n, per_stream), dtype=np.float32)
         self.o.lib.xgo_ensemble_fill_f32(self.buf, self.n, per_stream, _ptr(out), self.o.threads)
@@ -206,6 +211,7 @@ class Reference:
         L.xgref_ensemble_generate.argtypes = [_vp, _u64, ctypes.c_uint, _vp,
                                               ctypes.POINTER(ctypes.c_double),
                                               ctypes.POINTER(_u64)]
+        L.xgref_raw_stream.argtypes = [arr, _u64, ctypes.c_uint, _u64, _u64, _vp]
         L.xgref_serial_rate.restype = ctypes.c_double
         L.xgref_serial_rate.argtypes = [_u64, _u64, ctypes.c_uint, ctypes.POINTER(_u64)]
 
@@ -219,6 +225,14 @@ class Reference:
     def stream(self, seed: int, n: int, p) -> np.ndarray:
         out = np.empty(n, dtype=np.uint64)
         rc = self.lib.xgref_stream(self._arr(p), p.omega, p.gamma, seed & (2**64 - 1), n, _ptr(out))
+        if rc:
+            raise ValueError("reference rejected the parameters")
+        return out
+
+    def raw_stream(self, seed: int, n: int, p) -> np.ndarray:
+        """RawXorgens(p, seed).next() x n (the reference baseline class)."""
+        out = np.empty(n, dtype=np.uint64)
+        rc = self.lib.xgref_raw_stream(self._arr(p), p.omega, p.gamma, seed & (2**64 - 1), n, _ptr(out))
         if rc:
             raise ValueError("reference rejected the parameters")
         return out

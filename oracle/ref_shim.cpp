@@ -15,6 +15,7 @@
 #include <stdexcept>
 #include <vector>
 
+#include "xg/baselines.hpp"
 #include "xg/params.hpp"
 #include "xg/parallel.hpp"
 #include "xg/xorgens.hpp"
@@ -58,6 +59,19 @@ int xgref_stream(const unsigned* rsabcdw, std::uint64_t omega, unsigned gamma,
         xg::XorgensState st(to_params(rsabcdw, omega, gamma), seed);
         for (std::uint64_t k = 0; k < n; ++k)
             out[k] = st.next_word();
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// RawXorgens(params, seed).next() x n (proj/include/xg/baselines.hpp:60-71).
+int xgref_raw_stream(const unsigned* rsabcdw, std::uint64_t omega, unsigned gamma,
+                     std::uint64_t seed, std::uint64_t n, std::uint64_t* out) {
+    try {
+        xg::RawXorgens g(to_params(rsabcdw, omega, gamma), seed);
+        for (std::uint64_t k = 0; k < n; ++k)
+            out[k] = g.next();
         return 0;
     } catch (const std::exception&) {
         return -1;

@@ -59,6 +59,7 @@ SIGNATURES = {
     "xg_fill_u32": (_int, [_vp, _u64, _vp, _vp]),
     "xg_fill_u64": (_int, [_vp, _u64, _vp, _vp]),
     "xg_fill_f32": (_int, [_vp, _u64, _vp, _vp]),
+    "xg_fill_raw_u32": (_int, [_vp, _u64, _vp, _vp]),
     "xg_fill_f64": (_int, [_vp, _u64, _vp, _vp]),
     "xg_mc_pi": (_int, [_vp, _u64, _vp, _vp]),
     "xg_skip": (_int, [_vp, _u64, _vp]),

@@ -124,7 +124,7 @@ unsigned grid_for(uint32_t n) { return (n + kWarpsPerBlock - 1) / kWarpsPerBlock
 // bit 0 Weyl >> gamma, bit 1 t >> b, bit 2 t >> d as IMAD.HI on the FMA pipe.
 // Chosen per mode from the measurements in profiles/README.md; XG_VARIANT
 // overrides (experiments only).
-constexpr int kDefaultVar[5] = {16, 16, 16, 16, 16};
+constexpr int kDefaultVar[6] = {16, 16, 16, 16, 16, 16};
 
 int variant_for(int mode) {
     static int forced = [] {
@@ -250,6 +250,7 @@ int fill_common(xg_ensemble_t h, uint64_t per_stream, void* dev_out, size_t alig
     switch (mode) {
     case kU32: return launch_fill<kU32>(h, 0, h->num_streams, per_stream, dev_out, nullptr, s);
     case kF32: return launch_fill<kF32>(h, 0, h->num_streams, per_stream, dev_out, nullptr, s);
+    case kRaw: return launch_fill<kRaw>(h, 0, h->num_streams, per_stream, dev_out, nullptr, s);
     case kF64: {
         uint64_t words;
         if (mul_overflows(per_stream, 2, &words)) return XG_EINVAL;
@@ -417,6 +418,10 @@ int xg_fill_u64(xg_ensemble_t h, uint64_t per_stream, uint64_t* dev_out, xg_stre
     if (reinterpret_cast<uintptr_t>(dev_out) % 8 != 0) return XG_EINVAL;
     // Little-endian: (lo, hi) word pairs are exactly the uint64 values.
     return fill_common(h, words, dev_out, 8, kU32, stream);
+}
+
+int xg_fill_raw_u32(xg_ensemble_t h, uint64_t per_stream, uint32_t* dev_out, xg_stream_t stream) {
+    return fill_common(h, per_stream, dev_out, 4, kRaw, stream);
 }
 
 int xg_fill_f32(xg_ensemble_t h, uint64_t per_stream, float* dev_out, xg_stream_t stream) {

@@ -62,7 +62,10 @@ struct HiMul {
     uint32_t gamma, b, d;  // 2^(32-gamma), 2^(32-b), 2^(32-d)
 };
 
-enum Mode : int { kU32 = 0, kF32 = 1, kF64 = 2, kMC = 3, kSkip = 4 };
+// kRaw: the linear recurrence alone (RawXorgens::next = step_linear,
+// proj/include/xg/baselines.hpp:60-71, registry id "xorgens-raw"): emits x_i
+// and leaves the Weyl accumulator untouched.
+enum Mode : int { kU32 = 0, kF32 = 1, kF64 = 2, kMC = 3, kSkip = 4, kRaw = 5 };
 
 template <bool HI>
 __device__ __forceinline__ uint32_t shr(uint32_t x, unsigned k, uint32_t mul) {
@@ -234,7 +237,7 @@ seed_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
 template <int MODE>
 __device__ __forceinline__ void* advance(void* o, int n) {
     if constexpr (MODE == kF64) return static_cast<double*>(o) + n;
-    else if constexpr (MODE == kU32 || MODE == kF32) return static_cast<uint32_t*>(o) + n;
+    else if constexpr (MODE == kU32 || MODE == kF32 || MODE == kRaw) return static_cast<uint32_t*>(o) + n;
     else return o;
 }
 
@@ -246,19 +249,24 @@ template <int MODE, int VAR, bool TAIL, int BUF = 0, class P>
 __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul& m, const Lane& ln,
                                       uint32_t& wl, uint32_t w_step, void* o, uint32_t& hits,
                                       unsigned limit) {
-    const uint32_t o0 = weyl_out<VAR>(wl, warp_step<0, VAR>(R, p, m, ln), p, m);
-    const uint32_t o1 = weyl_out<VAR>(wl + w_step, warp_step<1, VAR>(R, p, m, ln), p, m);
-    const uint32_t o2 = weyl_out<VAR>(wl + 2u * w_step, warp_step<2, VAR>(R, p, m, ln), p, m);
-    const uint32_t o3 = weyl_out<VAR>(wl + 3u * w_step, warp_step<3, VAR>(R, p, m, ln), p, m);
+    constexpr bool kW = MODE != kRaw;  // Weyl output stage applied
+    const uint32_t v0 = warp_step<0, VAR>(R, p, m, ln);
+    const uint32_t o0 = kW ? weyl_out<VAR>(wl, v0, p, m) : v0;
+    const uint32_t v1 = warp_step<1, VAR>(R, p, m, ln);
+    const uint32_t o1 = kW ? weyl_out<VAR>(wl + w_step, v1, p, m) : v1;
+    const uint32_t v2 = warp_step<2, VAR>(R, p, m, ln);
+    const uint32_t o2 = kW ? weyl_out<VAR>(wl + 2u * w_step, v2, p, m) : v2;
+    const uint32_t v3 = warp_step<3, VAR>(R, p, m, ln);
+    const uint32_t o3 = kW ? weyl_out<VAR>(wl + 3u * w_step, v3, p, m) : v3;
     wl += 4u * w_step;
     const unsigned lane = threadIdx.x & 31u;
-    if constexpr (MODE == kU32 || MODE == kF32) {
+    if constexpr (MODE == kU32 || MODE == kF32 || MODE == kRaw) {
         uint32_t* u = static_cast<uint32_t*>(o);
         const uint32_t ov[4] = {o0, o1, o2, o3};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (!TAIL || lane + 32u * j < limit) {
-                if constexpr (MODE == kU32) __stcs(u + 32 * j, ov[j]);
+                if constexpr (MODE == kU32 || MODE == kRaw) __stcs(u + 32 * j, ov[j]);
                 else __stcs(reinterpret_cast<float*>(u) + 32 * j, u32_to_f32(ov[j]));
             }
         }
@@ -339,7 +347,7 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
     // Output cursor: single-word modes index words, pair modes index pairs.
     const uint64_t per_stream_vals = kPairs ? (words >> 1) : words;
     void* o = out;
-    if constexpr (MODE == kU32 || MODE == kF32 || MODE == kF64) {
+    if constexpr (MODE == kU32 || MODE == kF32 || MODE == kF64 || MODE == kRaw) {
         constexpr bool kShuffledPairs = kPairs && (VAR & 16) == 0;
         const uint64_t first = static_cast<uint64_t>(gl) * per_stream_vals +
                                (kShuffledPairs ? ((lane >> 1) + ((lane & 1u) << 4)) : lane);
@@ -390,7 +398,7 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
 #pragma unroll
         for (int j = 0; j < 4; ++j) w[32 * j + lane] = R[j];
     }
-    if (lane == 0) weyl[g] = weyl0 + static_cast<uint32_t>(words) * p.omega;
+    if (MODE != kRaw && lane == 0) weyl[g] = weyl0 + static_cast<uint32_t>(words) * p.omega;
 
     if constexpr (MODE == kMC) {
         unsigned long long t = hits;

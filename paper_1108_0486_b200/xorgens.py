@@ -346,6 +346,10 @@ class BlockEnsemble:
         """Device fill, out[g, k] = word k of block g (continuing)."""
         return self._fill(lib.xg_fill_u32, per_block, out, _torch().uint32, per_block, stream)
 
+    def fill_raw_u32(self, per_block: int, out=None, stream=None):
+        """Weyl-ablated linear stream (RawXorgens::next, registry "xorgens-raw")."""
+        return self._fill(lib.xg_fill_raw_u32, per_block, out, _torch().uint32, per_block, stream)
+
     def fill_u64(self, per_block: int, out=None, stream=None):
         """Two consecutive words per value, lo first."""
         return self._fill(lib.xg_fill_u64, per_block, out, _torch().uint64, per_block, stream)

@@ -47,6 +47,9 @@ def main() -> None:
     seeds = [0, 1, 2, 3, 42, 1000, 1001, 2**63, M64]
     out["streams"] = {str(s): hexs(ref.stream(s, 300, gp32)) for s in seeds}
 
+    # 1b. the Weyl-ablated baseline (RawXorgens, registry id "xorgens-raw")
+    out["raw_streams"] = {str(s): hexs(ref.raw_stream(s, 300, gp32)) for s in (0, 42, M64)}
+
     # 2. seeded state of seed 1 (logical buffer oldest first + weyl)
     buf, wy = ref.seeded_state(1, gp32)
     out["seeded_state_seed1"] = {"buffer": hexs(buf), "weyl": f"{wy:08x}"}

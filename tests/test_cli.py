@@ -1,0 +1,121 @@
+"""The GPU backend of the reference CLI (paper_1108_0486_b200/lib/xgen), checked
+the way the reference checks its own xgen (proj/tests/test_cli.cpp): golden
+stream file, block-major concatenation of consecutive seeds, lane invariance,
+exit codes, the params table.  Exit-code cases that fail before any device
+work run on CPU; stream cases need the GPU."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from helpers import u32
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+XGEN = os.path.join(ROOT, "paper_1108_0486_b200", "lib", "xgen")
+GOLDEN_SEED42 = "a61e8308\n8469633b\n80f8af0d\n57f95c64\n"  # proj/tests/golden/gen_gp32_seed42_count4.hex
+
+
+def run(*args, timeout=300):
+    r = subprocess.run([XGEN, *args], capture_output=True, timeout=timeout)
+    return r.returncode, r.stdout
+
+
+def has_gpu():
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def test_binary_built():
+    assert os.access(XGEN, os.X_OK)
+
+
+@pytest.mark.parametrize("args,code", [
+    (("gen", "-g", "nosuchgen", "--count", "4"), 64),          # test_cli.cpp:95
+    (("params", "nosuchgen"), 64),                              # :96
+    (("gen", "-g", "xorgensgp32", "--count", "64", "--lanes", "64"), 65),  # :97
+    (("gen", "-g", "xorgensgp32", "--count", "7", "--blocks", "2"), 67),   # :98
+    (("gen", "-g", "xorgens-raw", "--count", "4", "--blocks", "2"), 67),   # :99 (non-Weyl id)
+    (("gen", "-g", "xorgensgp32", "--count", "4", "--format", "bogus"), 67),  # :100
+    (("gen", "-g", "xorgensgp32"), 67),                         # --count is required
+    (("frobnicate",), 67),
+])
+def test_exit_codes(args, code):
+    assert run(*args)[0] == code
+
+
+def test_params_table():
+    # proj/tests/test_cli.cpp:104-115
+    rc, out = run("params", "xorgensgp32")
+    assert rc == 0
+    for line in ("r,s:          128,65", "a,b,c,d:      15,14,12,17", "word bits:    32",
+                 "gamma:        16", "omega:        2654435769", "lane bound:   63",
+                 "state words:  129", "~2^4128"):
+        assert line.encode() in out, line
+    rc, out = run("params", "xorgens-raw")
+    assert rc == 0 and b"2^4096-1" in out and b"gamma" not in out
+
+
+gpu = pytest.mark.gpu
+
+
+@gpu
+def test_gen_golden_stream():
+    # proj/tests/test_cli.cpp:59-63
+    rc, out = run("gen", "--generator", "xorgensgp32", "--seed", "42", "--count", "4",
+                  "--format", "hex")
+    assert rc == 0 and out.decode() == GOLDEN_SEED42
+
+
+@gpu
+def test_gen_block_major_and_lanes():
+    # proj/tests/test_cli.cpp:79-92
+    _, combined = run("gen", "-g", "xorgensgp32", "--seed", "42", "--count", "8", "--blocks", "2",
+                      "--format", "u32-lines")
+    _, first = run("gen", "-g", "xorgensgp32", "--seed", "42", "--count", "4", "--format", "u32-lines")
+    _, second = run("gen", "-g", "xorgensgp32", "--seed", "43", "--count", "4", "--format", "u32-lines")
+    assert combined == first + second
+    _, serial = run("gen", "-g", "xorgensgp32", "--seed", "5", "--count", "256", "--format", "hex")
+    rc, laned = run("gen", "-g", "xorgensgp32", "--seed", "5", "--count", "256", "--lanes", "63",
+                    "--format", "hex")
+    assert rc == 0 and laned == serial
+    rc, empty = run("gen", "-g", "xorgensgp32", "--seed", "1", "--count", "0")
+    assert rc == 0 and empty == b""
+
+
+@gpu
+def test_gen_raw_le_matches_oracle(oracle, golden, tmp_path):
+    # raw-le bytes == little-endian uint32 buffer; 3 blocks, ragged size
+    path = tmp_path / "out.bin"
+    rc, _ = run("gen", "--seed", "2", "--count", str(3 * 1001), "--blocks", "3", "--format",
+                "raw-le", "-o", str(path))
+    assert rc == 0
+    got = np.fromfile(path, dtype="<u4").reshape(3, 1001)
+    assert np.array_equal(got, oracle.ensemble(2, 3).fill_u32(1001))
+    rc, raw = run("gen", "-g", "xorgens-raw", "--seed", "42", "--count", "300", "--format", "hex")
+    assert rc == 0 and raw.decode().split() == golden["raw_streams"]["42"]
+
+
+@gpu
+def test_gen_long_single_block_chunks(oracle, tmp_path):
+    # longer than the 2^26-word staging buffer: produced in continuation chunks
+    n = (1 << 26) + 777
+    path = tmp_path / "long.bin"
+    rc, _ = run("gen", "--seed", "9", "--count", str(n), "--format", "raw-le", "-o", str(path),
+                timeout=600)
+    assert rc == 0
+    got = np.fromfile(path, dtype="<u4")
+    assert got.size == n
+    assert np.array_equal(got, oracle.stream(9, n))
+
+
+@gpu
+def test_bench_reports():
+    rc, out = run("bench", "--count", "16777216", "--blocks", "4096", "--trials", "3")
+    assert rc == 0 and b"RN/s" in out
+    rc, out = run("bench", "--count", "16777216", "--blocks", "4096", "--trials", "3", "--json")
+    assert rc == 0 and b'"mean"' in out

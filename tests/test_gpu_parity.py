@@ -311,3 +311,20 @@ def test_cpp_dropin_against_reference():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "OK" in r.stdout
+
+
+def test_raw_stream_vs_golden_and_oracle(oracle, golden):
+    """xg_fill_raw_u32 = RawXorgens::next (Weyl ablated); the Weyl accumulator
+    is untouched, so raw and full fills interleave exactly like the reference
+    classes sharing one XorgensState."""
+    for seed, words in golden["raw_streams"].items():
+        e = xg.BlockEnsemble(GP32, int(seed), 1, 63)
+        assert np.array_equal(np_u32(e.fill_raw_u32(len(words)))[0], u32(words))
+    e = xg.BlockEnsemble(GP32, 11, 9, 63)
+    o = oracle.ensemble(11, 9)
+    for n in (100, 129, 4096):
+        assert np.array_equal(np_u32(e.fill_raw_u32(n)), o.fill_raw_u32(n))
+        assert np.array_equal(np_u32(e.fill_u32(n)), o.fill_u32(n))
+    for i in range(9):
+        b, w = e.block_state(i)
+        assert w == o.weyl(i) and np.array_equal(np.array(b, dtype=np.uint64), o.logical_buffer(i))

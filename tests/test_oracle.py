@@ -228,3 +228,11 @@ def test_oracle_matches_live_reference(oracle, reference):
     for rs, _ in PARAM_CASES:
         p = oracle.params(*rs, omega=159 if rs[6] == 12 else None)
         assert oracle.check(p) == reference.check(p)
+
+
+def test_golden_raw_streams(oracle, golden):
+    # RawXorgens (proj/include/xg/baselines.hpp:60-71): seeding as XorgensState,
+    # then step_linear only.
+    for seed, words in golden["raw_streams"].items():
+        e = oracle.ensemble(int(seed), 1)
+        assert np.array_equal(e.fill_raw_u32(len(words))[0], u32(words)), seed
