@@ -297,7 +297,7 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     if args.steps is None:
-        args.steps = 5 if args.workload == "mc_pi" else (10 if args.impl == "reference" else 200)
+        args.steps = 5 if args.workload == "mc_pi" else (10 if args.impl == "reference" else 500)
     if args.impl == "reference":
         return run_reference_arm(args)
 
