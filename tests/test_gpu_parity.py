@@ -328,3 +328,88 @@ def test_raw_stream_vs_golden_and_oracle(oracle, golden):
     for i in range(9):
         b, w = e.block_state(i)
         assert w == o.weyl(i) and np.array_equal(np.array(b, dtype=np.uint64), o.logical_buffer(i))
+
+
+# ---- runtime-parameter kernels (any w=32, r=128 set with lane_bound >= 32) ----
+
+RT_SETS = [
+    (128, 95, 17, 12, 13, 15, 32, 2654435769, 16),   # J=1, delta=1 (proj/tests/test_params.cpp:65)
+    (128, 33, 11, 7, 9, 19, 32, 0x6A09E667 | 1, 11),  # J=2, delta=31
+    (128, 63, 9, 23, 5, 27, 32, 0x9E3779B9, 5),       # J=2, delta=1
+    (128, 65, 15, 14, 12, 17, 32, 2654435761, 16),    # gp32 shape, different omega -> runtime path
+]
+
+
+@pytest.mark.parametrize("ps", RT_SETS)
+def test_runtime_params_all_modes(oracle, reference, ps):
+    p = xg.GeneratorParams(*ps)
+    op = Params(*ps)
+    assert xg.gpu_supported(p)
+    e = xg.BlockEnsemble(p, 77, 11, 32)
+    o = oracle.ensemble(77, 11, op)
+    assert np.array_equal(np_u32(e.fill_u32(1000)), o.fill_u32(1000))
+    assert np.array_equal(np_u32(e.fill_f32(257)).view(np.uint32), o.fill_f32(257).view(np.uint32))
+    assert np.array_equal(np_u32(e.fill_f64(129)).view(np.uint64), o.fill_f64(129).view(np.uint64))
+    assert int(e.mc_pi(320).item()) == int(o.mc_hits(320).sum())
+    assert np.array_equal(np_u32(e.fill_raw_u32(300)), o.fill_raw_u32(300))
+    assert np.array_equal(np_u32(e.fill_u32(64)), o.fill_u32(64))
+    # and the reference sources themselves, stream 0
+    assert np.array_equal(np_u32(xg.BlockEnsemble(p, 5, 1, 32).fill_u32(2000))[0],
+                          reference.stream(5, 2000, op).astype(np.uint32))
+
+
+def test_many_streams_seeding_sampled(oracle):
+    """2^20 streams: seeding + a fill, sampled streams word-for-word."""
+    P, n = 1 << 20, 256
+    e = xg.BlockEnsemble(GP32, 12345, P, 63)
+    out = e.fill_u32(n)
+    rng = np.random.default_rng(3)
+    for g in [0, 1, P - 1, *rng.integers(0, P, 20).tolist()]:
+        assert np.array_equal(np_u32(out[g]), oracle.stream(12345 + g, n)), g
+
+
+def test_generate_host_chunked_matches_device_fill(oracle):
+    """xg_generate_host streams P x per through two 2^26-word staging slots
+    (several chunks here) and must equal a device fill of a twin ensemble."""
+    P, per = 4096, 1 << 15
+    a = xg.BlockEnsemble(GP32, 9, P, 63)
+    b = xg.BlockEnsemble(GP32, 9, P, 63)
+    host = a.generate(per)
+    dev = np_u32(b.fill_u32(per))
+    assert np.array_equal(host, dev)
+    for g in (0, 2047, 2048, P - 1):
+        assert np.array_equal(host[g], oracle.stream(9 + g, per))
+    assert np.array_equal(a.generate(100), np_u32(b.fill_u32(100)))
+
+
+def test_independent_handles_on_separate_streams(oracle):
+    """Handles are single-owner but independent: two ensembles filling on two
+    CUDA streams concurrently give the same words as the oracle."""
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    a = xg.BlockEnsemble(GP32, 100, 64, 63)
+    b = xg.BlockEnsemble(GP32, 200, 64, 63)
+    oa = torch.empty((64, 4096), dtype=torch.uint32, device="cuda")
+    ob = torch.empty((64, 4096), dtype=torch.uint32, device="cuda")
+    torch.cuda.synchronize()
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            a.fill_u32(4096, out=oa, stream=s1)
+        with torch.cuda.stream(s2):
+            b.fill_u32(4096, out=ob, stream=s2)
+    torch.cuda.synchronize()
+    ea, eb = oracle.ensemble(100, 64), oracle.ensemble(200, 64)
+    for _ in range(2):
+        ea.fill_u32(4096)
+        eb.fill_u32(4096)
+    assert np.array_equal(np_u32(oa), ea.fill_u32(4096))
+    assert np.array_equal(np_u32(ob), eb.fill_u32(4096))
+
+
+def test_kernel_launch_accounting():
+    e = xg.BlockEnsemble(GP32, 1, 16, 63)
+    n0 = xg.kernel_launches()
+    e.fill_u32(100)
+    e.fill_f32(100)
+    e.mc_pi(64)
+    torch.cuda.synchronize()
+    assert xg.kernel_launches() - n0 == 3
