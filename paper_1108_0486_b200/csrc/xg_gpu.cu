@@ -120,10 +120,10 @@ int cuda_rc(cudaError_t e) {
 
 unsigned grid_for(uint32_t n) { return (n + kWarpsPerBlock - 1) / kWarpsPerBlock; }
 
-// Shift-placement variant of the GP32 kernels (xg_kernels.cuh, VAR mask):
-// bit 0 Weyl >> gamma, bit 1 t >> b, bit 2 t >> d as IMAD.HI on the FMA pipe.
-// Chosen per mode from the measurements in profiles/README.md; XG_VARIANT
-// overrides (experiments only).
+// Instruction-placement variant of the GP32 kernels (xg_kernels.cuh, VAR
+// mask): 16 (shared-memory s-tap) for every mode, from the measurements in
+// profiles/README.md; XG_VARIANT = 0, 1, 16 or 144 selects another for
+// experiments.
 constexpr int kDefaultVar[6] = {16, 16, 16, 16, 16, 16};
 
 int variant_for(int mode) {
@@ -159,11 +159,8 @@ int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t wor
     case kGP32:
         switch (variant_for(MODE)) {
         case 0: return launch_fill_v<MODE, 0>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-        case 3: return launch_fill_v<MODE, 3>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-        case 5: return launch_fill_v<MODE, 5>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-        case 7: return launch_fill_v<MODE, 7>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         case 16: return launch_fill_v<MODE, 16>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-        case 17: return launch_fill_v<MODE, 17>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        case 144: return launch_fill_v<MODE, 144>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         default: return launch_fill_v<MODE, 1>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         }
     case kRtJ1:

@@ -17,11 +17,15 @@
 // the output is ((w ^ (w >> gamma)) + x) mod 2^32 (xorgens.hpp:58-62).
 //
 // Issue-slot budget (measured, profiles/README.md): the loop is integer-ALU
-// bound, so right shifts can be moved from the ALU pipe (SHF) to the FMA pipe
-// as IMAD.HI by a runtime power of two (x >> k == umulhi(x, 2^(32-k))); the
-// VAR template mask selects which (bit 0: Weyl >> gamma, bit 1: t >> b,
-// bit 2: t >> d).  The multipliers are kernel arguments, not immediates, so
-// ptxas cannot strength-reduce them back to SHF.
+// bound.  The VAR template mask selects instruction-placement variants that
+// were measured (XG_VARIANT overrides the default, 16):
+//   bit 0/1/2  Weyl >> gamma, t >> b, t >> d as IMAD.HI by a runtime power of
+//              two on the FMA pipe (slower: IMAD.HI is half rate and co-issues
+//              badly with LOP3);
+//   bit 4      s-tap through a shared-memory ring instead of SEL + SHFL (the
+//              default: one ALU op less per word);
+//   bit 7      left shifts forced onto the ALU pipe as SHF.L (slower: ptxas's
+//              IMAD.SHL keeps the ALU pipe free).
 //
 // Each warp step emits one contiguous, 128-byte aligned line of the
 // block-major output (out[g*per_stream + k], parallel.cpp:97-135), stored with
@@ -73,6 +77,19 @@ __device__ __forceinline__ uint32_t shr(uint32_t x, unsigned k, uint32_t mul) {
     else return x >> k;
 }
 
+// Left shift; FUNNEL forces SHF.L on the ALU pipe (ptxas otherwise picks
+// IMAD.SHL on the FMA pipe for immediate shifts).
+template <bool FUNNEL>
+__device__ __forceinline__ uint32_t shl(uint32_t x, unsigned k) {
+    if constexpr (FUNNEL) {
+        uint32_t r;
+        asm("shf.l.clamp.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(0u), "r"(x), "r"(k));
+        return r;
+    } else {
+        return x << k;
+    }
+}
+
 // 32-bit funnel: low word of (hi:lo) >> s, s in 0..63 (one SHF.R.U64).
 __device__ __forceinline__ uint32_t funnel_r(uint32_t lo, uint32_t hi, uint32_t s) {
     return static_cast<uint32_t>(((static_cast<uint64_t>(hi) << 32) | lo) >> s);
@@ -108,8 +125,8 @@ __device__ __forceinline__ uint32_t warp_step(uint32_t (&R)[4], const P& p, cons
         y = __shfl_sync(kFull, give, ln.src);
     }
     const uint32_t x = R[i0];
-    const uint32_t t1 = x ^ (x << p.a);
-    const uint32_t t2 = y ^ (y << p.c);
+    const uint32_t t1 = x ^ shl<(VAR & 128) != 0>(x, p.a);
+    const uint32_t t2 = y ^ shl<(VAR & 128) != 0>(y, p.c);
     const uint32_t v = t1 ^ shr<(VAR & 2) != 0>(t1, p.b, m.b) ^ t2 ^ shr<(VAR & 4) != 0>(t2, p.d, m.d);
     R[i0] = v;  // newest block; the old block 0 is no longer needed
     if constexpr ((VAR & 16) != 0) {
