@@ -121,9 +121,9 @@ int cuda_rc(cudaError_t e) {
 unsigned grid_for(uint32_t n) { return (n + kWarpsPerBlock - 1) / kWarpsPerBlock; }
 
 // Instruction-placement variant of the GP32 kernels (xg_kernels.cuh, VAR
-// mask): 16 (shared-memory s-tap) for every mode, from the measurements in
-// profiles/README.md; XG_VARIANT = 0, 1, 16 or 144 selects another for
-// experiments.
+// mask): 16 (shared-memory s-tap) for every mode and parameter kind, from the
+// measurements in profiles/README.md; XG_VARIANT = 0, 1 or 144 selects another
+// GP32 variant for experiments.
 constexpr int kDefaultVar[6] = {16, 16, 16, 16, 16, 16};
 
 int variant_for(int mode) {
@@ -159,14 +159,14 @@ int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t wor
     case kGP32:
         switch (variant_for(MODE)) {
         case 0: return launch_fill_v<MODE, 0>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-        case 16: return launch_fill_v<MODE, 16>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        case 1: return launch_fill_v<MODE, 1>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         case 144: return launch_fill_v<MODE, 144>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-        default: return launch_fill_v<MODE, 1>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        default: return launch_fill_v<MODE, 16>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         }
     case kRtJ1:
-        return launch_fill_v<MODE, 1>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s);
+        return launch_fill_v<MODE, 16>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s);
     default:
-        return launch_fill_v<MODE, 1>(rt_params<2>(h->params), h, g_begin, g_count, words, out, hits, s);
+        return launch_fill_v<MODE, 16>(rt_params<2>(h->params), h, g_begin, g_count, words, out, hits, s);
     }
 }
 
