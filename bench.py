@@ -174,7 +174,8 @@ def max_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -185,7 +186,8 @@ def max_over_ranks(x: float, world: int) -> float:
 # wall-clocked around generate() as measure_ensemble_throughput does.
 # --------------------------------------------------------------------------
 
-def reference_rate(streams: int, per_block: int, trials: int, warmup: int = 1, budget_s: float = 30.0):
+def reference_rate(streams: int, per_block: int, trials: int, warmup: int = 1, budget_s: float = 30.0,
+                   min_trials: int = 3):
     from oracle import REF_SO, Oracle, Reference
 
     threads = os.cpu_count() or 1
@@ -199,7 +201,7 @@ def reference_rate(streams: int, per_block: int, trials: int, warmup: int = 1, b
             secs, _ = ref.generate_timed(h, per_block, threads)
             if i >= warmup:
                 rates.append(streams * per_block / secs)
-            if time.perf_counter() - t0 > budget_s and len(rates) >= 1:
+            if time.perf_counter() - t0 > budget_s and len(rates) >= min_trials:
                 break
         ref.destroy(h)
         kind = "reference"
@@ -253,6 +255,27 @@ def run_reference_arm(args):
 # --------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------
+
+def workload_geometry(wl: str, world: int, rank: int):
+    """Per-rank stream slice and per-stream length of each workload, and the
+    words the whole job consumes per step.  Weak scaling: every rank owns
+    2^14 streams of its own (global ids rank*2^14 ...), 2^30 values per GPU.
+    Strong scaling: one global ensemble split by xg_partition."""
+    import paper_1108_0486_b200 as xg
+
+    if wl in ("fill_u32", "fill_f32", "fill_f64", "skip"):
+        P, per = 1 << 14, 1 << 16
+        words = P * per * (2 if wl == "fill_f64" else 1)
+        return rank * P, P, per, "weak", words * world
+    if wl == "fill_2p34":
+        first, count = xg.partition(1 << 18, world, rank)
+        return first, count, 1 << 16, "strong", 1 << 34
+    if wl == "mc_pi":
+        total_streams = 1 << 17
+        first, count = xg.partition(total_streams, world, rank)
+        return first, count, (1 << 40) // total_streams, "strong", 1 << 41
+    raise ValueError(wl)
+
 
 def timed_loop(fn, stream, steps, warmup, world, flush=None):
     """W warm-ups, then K timed steps bracketed by barrier + synchronize;
@@ -311,20 +334,7 @@ def main():
     wl = args.workload
     hbm_peak, peak_src = load_peaks()
 
-    # workload geometry (per rank)
-    if wl in ("fill_u32", "fill_f32", "fill_f64", "skip"):
-        P, per = 1 << 14, 1 << 16                       # 2^30 values per GPU (weak scaling)
-        first, count = rank * P, P
-        scaling = "weak"
-    elif wl == "fill_2p34":
-        total_streams, per = 1 << 18, 1 << 16           # 2^34 words over the job (strong scaling)
-        first, count = xg.partition(total_streams, world, rank)
-        scaling = "strong"
-    else:  # mc_pi: 2^40 samples over the job
-        total_streams = 1 << 17
-        first, count = xg.partition(total_streams, world, rank)
-        per = (1 << 40) // total_streams               # samples per stream = 2^23
-        scaling = "strong"
+    first, count, per, scaling, job_words_per_step = workload_geometry(wl, world, rank)
     ens = xg.BlockEnsemble(p, 1, count, 63, first_stream=first, device=local)
 
     out = None
@@ -354,9 +364,7 @@ def main():
         total_ms, step_ms = timed_loop(fn, stream, args.steps, args.warmup, world)
     launches = xg.kernel_launches() - launches0 - args.warmup * (1 if wl != "mc_pi" else 1)
     t_max = max_over_ranks(total_ms, world)
-    job_words = words_per_step * world if scaling == "weak" else (
-        (1 << 34) if wl == "fill_2p34" else (1 << 41))
-    value = job_words * args.steps / (t_max / 1e3)
+    value = job_words_per_step * args.steps / (t_max / 1e3)
     kern_ms = statistics.mean(step_ms)
     state_bytes = 2 * count * 129 * 4                     # window + weyl read and written back
     alg_bytes = vals_per_step * bytes_per_val + state_bytes
@@ -438,9 +446,18 @@ def main():
         del host
     if rank == 0 and world == 1 and not args.no_cpu and wl in ("fill_u32", "fill_f32", "fill_f64"):
         try:
-            result["cpu_baseline"] = reference_rate(1 << 14, 1 << 13, trials=5, budget_s=30.0)
+            cb = reference_rate(1 << 14, 1 << 14, trials=100, budget_s=10.0)
             for k in ("trials", "min", "max"):
-                result["cpu_baseline"].pop(k, None)
+                cb.pop(k, None)
+            # BASELINE config 1: one serial stream on one core, the reference's
+            # measure_throughput method (proj/src/bench.cpp:67-93), seed 1, 10^8 words.
+            try:
+                from oracle import Reference
+
+                cb["serial_1core_rn_per_s"] = Reference().serial_rate(1, 10**8, 20)
+            except Exception:  # noqa: BLE001
+                pass
+            result["cpu_baseline"] = cb
         except Exception as e:  # noqa: BLE001
             result["cpu_baseline"] = {"value": None, "unavailable": str(e)}
     if rank == 0:
