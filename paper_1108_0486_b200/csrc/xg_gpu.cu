@@ -536,8 +536,9 @@ int xg_next_u32(xg_ensemble_t h, uint32_t* out) {
     }
     DeviceGuard dg(h->device);
     if (!dg.ok) return XG_ECUDA;
-    int rc = XG_OK;
-    if (!h->d_snap) rc = cuda_rc(cudaMalloc(&h->d_snap, (kR + 4) * sizeof(uint32_t)));
+    // Host-synchronous call: order after any fill the caller queued on any stream.
+    int rc = cuda_rc(cudaDeviceSynchronize());
+    if (!rc && !h->d_snap) rc = cuda_rc(cudaMalloc(&h->d_snap, (kR + 4) * sizeof(uint32_t)));
     if (!rc && !h->d_scratch) rc = cuda_rc(cudaMalloc(&h->d_scratch, kNextBuf * sizeof(uint32_t)));
     if (rc) return rc;
     cudaStream_t s = nullptr;
