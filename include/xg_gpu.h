@@ -159,6 +159,14 @@ int xg_state_export(xg_ensemble_t h, uint32_t index, uint64_t* buffer, uint64_t*
 /* Replace stream `index` with from_raw(params, buffer, weyl). */
 int xg_state_import(xg_ensemble_t h, uint32_t index, const uint64_t* buffer, uint64_t weyl);
 
+/* Checkpoint / resume of a whole ensemble: the device
+ * state of every stream, host_window[g*r + i] = logical_buffer()[i] of stream
+ * g (oldest first) and host_weyl[g] = weyl_value(), as 32-bit words (w = 32).
+ * Importing into an ensemble with the same parameters and stream count
+ * resumes every stream exactly. */
+int xg_state_export_all(xg_ensemble_t h, uint32_t* host_window, uint32_t* host_weyl);
+int xg_state_import_all(xg_ensemble_t h, const uint32_t* host_window, const uint32_t* host_weyl);
+
 /* ---- multi-GPU partitioner (host only) ----------------------------------- */
 
 /* Contiguous, balanced split of global streams [0, total) over `world`

@@ -603,6 +603,32 @@ int xg_state_import(xg_ensemble_t h, uint32_t index, const uint64_t* buffer, uin
     return rc;
 }
 
+int xg_state_export_all(xg_ensemble_t h, uint32_t* host_window, uint32_t* host_weyl) {
+    if (!h || !host_window || !host_weyl) return XG_EINVAL;
+    DeviceGuard dg(h->device);
+    if (!dg.ok) return XG_ECUDA;
+    int rc = cuda_rc(cudaDeviceSynchronize());
+    if (!rc) rc = settle_next(h, nullptr);
+    const size_t n = h->num_streams;
+    if (!rc) rc = cuda_rc(cudaMemcpy(host_window, h->d_win, n * kR * 4, cudaMemcpyDeviceToHost));
+    if (!rc) rc = cuda_rc(cudaMemcpy(host_weyl, h->d_weyl, n * 4, cudaMemcpyDeviceToHost));
+    return rc;
+}
+
+int xg_state_import_all(xg_ensemble_t h, const uint32_t* host_window, const uint32_t* host_weyl) {
+    if (!h || !host_window || !host_weyl) return XG_EINVAL;
+    DeviceGuard dg(h->device);
+    if (!dg.ok) return XG_ECUDA;
+    int rc = cuda_rc(cudaDeviceSynchronize());
+    if (!rc) rc = settle_next(h, nullptr);
+    h->nbuf.clear();
+    h->npos = 0;
+    const size_t n = h->num_streams;
+    if (!rc) rc = cuda_rc(cudaMemcpy(h->d_win, host_window, n * kR * 4, cudaMemcpyHostToDevice));
+    if (!rc) rc = cuda_rc(cudaMemcpy(h->d_weyl, host_weyl, n * 4, cudaMemcpyHostToDevice));
+    return rc;
+}
+
 int xg_partition(uint64_t total_streams, uint32_t world, uint32_t rank, uint64_t* first,
                  uint32_t* count) {
     if (!first || !count || world == 0) return XG_EINVAL;

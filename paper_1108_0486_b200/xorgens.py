@@ -391,6 +391,43 @@ class BlockEnsemble:
         _raise(lib.xg_state_import(self._h.ptr, i, arr, int(weyl) & ((1 << 64) - 1)), "state_import")
 
 
+    # -- checkpoint / resume of the whole ensemble ---------------------------
+    def state_dict(self) -> dict:
+        """Every stream's (window, weyl) plus the identity of the ensemble."""
+        win = np.empty((self._n, self._params.r), dtype=np.uint32)
+        wy = np.empty(self._n, dtype=np.uint32)
+        _raise(lib.xg_state_export_all(self._h.ptr, win.ctypes.data_as(ctypes.c_void_p),
+                                       wy.ctypes.data_as(ctypes.c_void_p)), "state_export_all")
+        p = self._params
+        return {"params": np.array([p.r, p.s, p.a, p.b, p.c, p.d, p.w, p.omega, p.gamma],
+                                   dtype=np.uint64),
+                "base_seed": np.uint64(self._base_seed), "first_stream": np.uint64(self._first),
+                "window": win, "weyl": wy}
+
+    def load_state_dict(self, sd: dict) -> None:
+        p = self._params
+        if tuple(int(v) for v in sd["params"]) != (p.r, p.s, p.a, p.b, p.c, p.d, p.w, p.omega, p.gamma):
+            raise ValueError("checkpoint parameters differ from the ensemble's")
+        win = np.ascontiguousarray(sd["window"], dtype=np.uint32)
+        wy = np.ascontiguousarray(sd["weyl"], dtype=np.uint32)
+        if win.shape != (self._n, p.r) or wy.shape != (self._n,):
+            raise ValueError("checkpoint stream count differs from the ensemble's")
+        _raise(lib.xg_state_import_all(self._h.ptr, win.ctypes.data_as(ctypes.c_void_p),
+                                       wy.ctypes.data_as(ctypes.c_void_p)), "state_import_all")
+
+    def save(self, path: str) -> None:
+        np.savez(path, **self.state_dict())
+
+    @classmethod
+    def load(cls, path: str, lanes: int = 1, *, device: Optional[int] = None) -> "BlockEnsemble":
+        sd = dict(np.load(path))
+        p = GeneratorParams(*[int(v) for v in sd["params"]])
+        ens = cls(p, int(sd["base_seed"]), int(sd["window"].shape[0]), lanes,
+                  first_stream=int(sd["first_stream"]), device=device)
+        ens.load_state_dict(sd)
+        return ens
+
+
 class XorgensState:
     """One serial stream (proj/include/xg/xorgens.hpp:20-96) on the GPU.
 
