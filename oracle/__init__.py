@@ -192,6 +192,30 @@ class OracleEnsemble:
         return out
 
 
+BATTERY_SO = os.path.join(HERE, "_ref", "libxgref_battery.so")
+
+
+class Battery:
+    """The reference's statistical battery (proj/src/stattests/*) over a buffer
+    of 32-bit words, through oracle/_ref/libxgref_battery.so."""
+
+    VERDICTS = {0: "pass", 1: "suspect", 2: "fail", 3: "not_applicable", -1: "error"}
+
+    def __init__(self, path: str = BATTERY_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} not built (needs the reference tree + json.hpp)")
+        self.lib = ctypes.CDLL(path)
+        self.lib.xgref_battery_on_words.argtypes = [_vp, _u64, _int, ctypes.c_char_p,
+                                                    ctypes.c_char_p, _u64]
+
+    def run(self, words: np.ndarray, quick: bool = False, label: str = "gpu"):
+        w = np.ascontiguousarray(words, dtype=np.uint32).reshape(-1)
+        buf = ctypes.create_string_buffer(1 << 16)
+        v = self.lib.xgref_battery_on_words(_ptr(w), w.size, int(quick), label.encode(), buf,
+                                            len(buf))
+        return self.VERDICTS.get(v, str(v)), buf.value.decode()
+
+
 class Reference:
     """The reference sources themselves (oracle/_ref/libxgref.so)."""
 

@@ -1,0 +1,47 @@
+// ref_battery_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// Runs the reference's own statistical battery (proj/src/stattests/*, via
+// xg::stats::run_battery, proj/src/stattests/battery.cpp:72-112) over a
+// caller-supplied buffer of 32-bit words -- e.g. words the GPU generated --
+// through the reference's CallbackSource (proj/include/xg/stream.hpp:67-78).
+// Built into oracle/_ref/libxgref_battery.so by oracle/Makefile.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "xg/stattests/battery.hpp"
+#include "xg/stream.hpp"
+
+extern "C" {
+
+// Returns the overall verdict (0 pass, 1 suspect, 2 fail, 3 n/a) or -1 when
+// the buffer ran out / the run failed; the JSON report is copied to json_out.
+int xgref_battery_on_words(const std::uint32_t* words, std::uint64_t n, int quick,
+                           const char* label, char* json_out, std::uint64_t cap) {
+    std::uint64_t pos = 0;
+    xg::CallbackSource src(
+        [&]() -> std::uint64_t {
+            if (pos >= n) throw std::runtime_error("word buffer exhausted");
+            return words[pos++];
+        },
+        32);
+    try {
+        auto cfg = quick ? xg::stats::BatteryConfig::quick() : xg::stats::BatteryConfig::defaults();
+        auto report = xg::stats::run_battery(src, cfg, label, "GPU-generated words", 0);
+        std::string js = xg::stats::to_json(report);
+        if (json_out && cap) {
+            std::strncpy(json_out, js.c_str(), cap - 1);
+            json_out[cap - 1] = 0;
+        }
+        return static_cast<int>(report.overall);
+    } catch (const std::exception& e) {
+        if (json_out && cap) {
+            std::strncpy(json_out, e.what(), cap - 1);
+            json_out[cap - 1] = 0;
+        }
+        return -1;
+    }
+}
+
+}  // extern "C"
