@@ -476,12 +476,23 @@ int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     int rc = settle_next(h, s);
     if (rc) return rc;
-    // Two staging slots of up to 64 Mi words; chunk i is generated on `s`
-    // while chunk i-1 is copied on a second stream.
+    // Two staging slots of up to 64 Mi words.  The (streams x words) output is
+    // cut into tiles: groups of whole streams when a stream fits a slot,
+    // otherwise groups of 2048 streams advanced in word chunks (each stream's
+    // chunks in order, so the continuation is exact).  Tile i is generated on
+    // `s` while tile i-1 is copied (2D, into the block-major host layout) on a
+    // second stream.
     constexpr uint64_t kSlotWords = 1ull << 26;
-    uint64_t streams_per_chunk = std::max<uint64_t>(1, kSlotWords / per_stream);
-    streams_per_chunk = std::min<uint64_t>(streams_per_chunk, h->num_streams);
-    const uint64_t slot_words = streams_per_chunk * per_stream;
+    constexpr uint64_t kGroup = 2048;
+    uint64_t cnt_max, m_max;
+    if (per_stream <= kSlotWords) {
+        m_max = per_stream;
+        cnt_max = std::min<uint64_t>(std::max<uint64_t>(1, kSlotWords / per_stream), h->num_streams);
+    } else {
+        cnt_max = std::min<uint64_t>(kGroup, h->num_streams);
+        m_max = (kSlotWords / cnt_max) & ~uint64_t{127};
+    }
+    const uint64_t slot_words = cnt_max * m_max;
     if (h->stage_words < 2 * slot_words) {
         cudaFree(h->d_stage);
         h->d_stage = nullptr;
@@ -499,23 +510,22 @@ int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,
         cudaEventCreateWithFlags(&copy_done[i], cudaEventDisableTiming);
         cudaEventRecord(copy_done[i], cs);
     }
-    uint32_t g = 0;
     int slot = 0;
-    while (g < h->num_streams && !rc) {
-        const uint32_t cnt = static_cast<uint32_t>(
-            std::min<uint64_t>(streams_per_chunk, h->num_streams - g));
-        uint32_t* d = h->d_stage + slot * slot_words;
-        cudaStreamWaitEvent(s, copy_done[slot], 0);
-        rc = launch_fill<kU32>(h, g, cnt, per_stream, d, nullptr, s);
-        if (rc) break;
-        cudaEventRecord(gen_done[slot], s);
-        cudaStreamWaitEvent(cs, gen_done[slot], 0);
-        rc = cuda_rc(cudaMemcpyAsync(host_out + static_cast<size_t>(g) * per_stream, d,
-                                     static_cast<size_t>(cnt) * per_stream * sizeof(uint32_t),
-                                     cudaMemcpyDeviceToHost, cs));
-        cudaEventRecord(copy_done[slot], cs);
-        g += cnt;
-        slot ^= 1;
+    for (uint64_t g0 = 0; g0 < h->num_streams && !rc; g0 += cnt_max) {
+        const uint32_t cnt = static_cast<uint32_t>(std::min<uint64_t>(cnt_max, h->num_streams - g0));
+        for (uint64_t k0 = 0; k0 < per_stream && !rc; k0 += m_max) {
+            const uint64_t m = std::min<uint64_t>(m_max, per_stream - k0);
+            uint32_t* d = h->d_stage + slot * slot_words;
+            cudaStreamWaitEvent(s, copy_done[slot], 0);
+            rc = launch_fill<kU32>(h, static_cast<uint32_t>(g0), cnt, m, d, nullptr, s);
+            if (rc) break;
+            cudaEventRecord(gen_done[slot], s);
+            cudaStreamWaitEvent(cs, gen_done[slot], 0);
+            rc = cuda_rc(cudaMemcpy2DAsync(host_out + g0 * per_stream + k0, per_stream * 4, d, m * 4,
+                                           m * 4, cnt, cudaMemcpyDeviceToHost, cs));
+            cudaEventRecord(copy_done[slot], cs);
+            slot ^= 1;
+        }
     }
     const int rc2 = cuda_rc(cudaStreamSynchronize(cs));
     const int rc3 = cuda_rc(cudaStreamSynchronize(s));

@@ -463,3 +463,17 @@ def test_cuda_graph_capture_replays_continue_streams(oracle):
         assert np.array_equal(np_u32(out), o.fill_u32(1024))
         want_hits += int(o.mc_hits(64).sum())
         assert int(hits.item()) == want_hits
+
+
+def test_generate_host_streams_longer_than_a_slot(oracle):
+    """per_stream > 2^26 words: tiles of 2048 streams advanced in word chunks,
+    copied 2D into the block-major host layout (continuation inside a call)."""
+    P, per = 3, (1 << 26) + 1000
+    e = xg.BlockEnsemble(GP32, 77, P, 63)
+    host = e.generate(per)
+    for g in range(P):
+        x, s = oracle.ensemble(77 + g, 1).checksums(per)
+        w = host[g].astype(np.uint64)
+        assert int(np.bitwise_xor.reduce(host[g])) == int(x[0])
+        assert int(np.sum(w * np.arange(1, per + 1, dtype=np.uint64), dtype=np.uint64)) == int(s[0])
+    assert np.array_equal(e.generate(64), oracle.ensemble(77, P).fill_u32(per + 64)[:, per:])
