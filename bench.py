@@ -30,9 +30,6 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-L2_BYTES = 126 * 2**20
-
-
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -41,6 +38,14 @@ def load_peaks():
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_ncu(workload: str) -> dict:
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f).get(workload, {})
+    except Exception:
+        return {}
 
 
 def load_traffic(workload: str):
@@ -277,7 +282,7 @@ def workload_geometry(wl: str, world: int, rank: int):
     raise ValueError(wl)
 
 
-def timed_loop(fn, stream, steps, warmup, world, flush=None):
+def timed_loop(fn, stream, steps, warmup, world):
     """W warm-ups, then K timed steps bracketed by barrier + synchronize;
     per-step CUDA events on the launching stream.  Returns (total_ms, [step_ms])."""
     import torch
@@ -292,8 +297,6 @@ def timed_loop(fn, stream, steps, warmup, world, flush=None):
     end = torch.cuda.Event(enable_timing=True)
     start.record(stream)
     for i in range(steps):
-        if flush is not None:
-            flush()
         evs[2 * i].record(stream)
         fn()
         evs[2 * i + 1].record(stream)
@@ -307,7 +310,8 @@ def timed_loop(fn, stream, steps, warmup, world, flush=None):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=1,
+                    help="GPUs in the job; N>1 runs under torchrun (one rank per GPU)")
     ap.add_argument("--steps", type=int, default=None,
                     help="timed steps (default: 200 for fills, 5 for mc_pi)")
     ap.add_argument("--warmup", type=int, default=5)
@@ -329,6 +333,9 @@ def main():
     import paper_1108_0486_b200 as xg
 
     world, rank, local = dist_setup()
+    if args.gpus != world and rank == 0:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with torchrun",
+              file=sys.stderr)
     stream = torch.cuda.current_stream()
     p = xg.xorgensgp32_params()
     wl = args.workload
@@ -425,8 +432,15 @@ def main():
         samples = (args.steps + args.warmup) * (1 << 40)
         result["mc"] = {"hits": hits_v, "samples": samples, "pi_estimate": 4.0 * hits_v / samples,
                         "kernel_ms_mean": kern_ms}
-        result["roofline"] = {"bound": "int-issue", "achieved": value / world, "peak": None,
-                              "unit": "RN/s per GPU", "frac": None, "traffic": load_traffic(wl)}
+        # In-register consumer: no HBM roofline.  The ceiling is the integer
+        # pipes; report their ncu utilisation (profiles/ncu_summary.json).
+        pipes = load_ncu(wl)
+        result["roofline"] = {
+            "bound": "int-issue", "achieved": value / world, "peak": None, "unit": "RN/s per GPU",
+            "frac": None, "traffic": load_traffic(wl),
+            "alu_pipe_pct": pipes.get("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+            "issue_active_pct": pipes.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "pipe_source": "profiles/ncu_summary.json (ncu --set full)"}
 
     # e2e through the public host API (generate into pinned host memory)
     if not args.no_e2e and wl == "fill_u32":
