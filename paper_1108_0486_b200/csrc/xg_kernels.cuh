@@ -100,26 +100,30 @@ struct Lane {
     unsigned src;      // shuffle source lane for the s-tap
     bool gives_J;      // this lane provides register J (else J+1) to the s-tap shuffle
     uint32_t sh_own;   // 32 on odd lanes, 0 on even: funnel shift for the pair consumers
-    // VAR bit 4 (shared-memory s-tap): the warp's 128-word ring mirrors the
-    // register window, block j of rotation position S at ring slot (S+j)&3;
-    // the s-tap W[(r-s)+l] is ring[(32S + (r-s) + l) & 127].
-    uint32_t* ring;
-    unsigned ld[4];
-    uint32_t* stage;   // f64 with VAR bit 4: 2 x 64-word output staging for word pairs
+    // VAR bit 4 (shared-memory s-tap): the block produced at step T (mod 8)
+    // lives in slot T of an 8-slot, 256-word ring, with slot 0 mirrored at
+    // words 256..287 so a read never wraps.  At step T the window's block j
+    // was produced at step T-4+j, so W[32J + delta + l] is ring word
+    // A_T + delta + l with the compile-time A_T = 32(T-4+J) mod 256.
+    uint32_t* ring_w;  // ring + lane (stores)
+    uint32_t* ring_r;  // ring + delta + lane (s-tap loads)
+    uint32_t* stage;   // f64 with VAR bit 4: 2 x 128-word output staging for word pairs
 };
 
-// One warp step on the register window.  S is the position in the 4-step
-// rotation: logical block j of the window lives in R[(S + j) & 3].
-// xorshift_transform (proj/include/xg/xorgens.hpp:13-18) twice, then xor.
-template <int S, int VAR, class P>
+// One warp step on the register window.  T is the step index mod 8; the
+// register rotation uses T mod 4: logical block j of the window lives in
+// R[(T + j) & 3].  xorshift_transform (proj/include/xg/xorgens.hpp:13-18)
+// twice, then xor.
+template <int T, int VAR, class P>
 __device__ __forceinline__ uint32_t warp_step(uint32_t (&R)[4], const P& p, const HiMul& m,
                                               const Lane& ln) {
-    constexpr int i0 = S & 3;
-    constexpr int iJ = (S + P::J) & 3;
-    constexpr int iJ1 = (S + P::J + 1) & 3;
+    constexpr int i0 = T & 3;
+    constexpr int iJ = (T + P::J) & 3;
+    constexpr int iJ1 = (T + P::J + 1) & 3;
     uint32_t y;
     if constexpr ((VAR & 16) != 0) {
-        y = ln.ring[ln.ld[S & 3]];  // written >= 2 steps ago, published by __syncwarp
+        constexpr int kA = (32 * (T - 4 + P::J)) & 255;
+        y = ln.ring_r[kA];
     } else {
         const uint32_t give = ln.gives_J ? R[iJ] : R[iJ1];
         y = __shfl_sync(kFull, give, ln.src);
@@ -130,10 +134,15 @@ __device__ __forceinline__ uint32_t warp_step(uint32_t (&R)[4], const P& p, cons
     const uint32_t v = t1 ^ shr<(VAR & 2) != 0>(t1, p.b, m.b) ^ t2 ^ shr<(VAR & 4) != 0>(t2, p.d, m.d);
     R[i0] = v;  // newest block; the old block 0 is no longer needed
     if constexpr ((VAR & 16) != 0) {
-        ln.ring[32 * (S & 3) + (threadIdx.x & 31u)] = v;
-        // Reads at step S see writes of steps <= S-2, so publishing after
-        // every odd step suffices.
-        if constexpr ((S & 1) == 1) __syncwarp();
+        ln.ring_w[32 * (T & 7)] = v;
+        if constexpr ((T & 7) == 0) ln.ring_w[256] = v;  // mirror of slot 0
+        // Hazards: a slot is rewritten 8 steps after it was written and read
+        // at most 3 steps after (WAR: always separated by a sync).  The s-tap
+        // reads blocks produced 2 and 3 steps earlier when J = 1 (xorgensgp32),
+        // 1 and 2 steps earlier when J = 2, so publishing every second step
+        // (J = 1) or every step (J = 2) covers RAW.  compute-sanitizer
+        // racecheck reports no hazards.
+        if constexpr (P::J != 1 || (T & 1) == 1) __syncwarp();
     }
     return v;
 }
@@ -211,10 +220,10 @@ __device__ __forceinline__ Lane make_lane(unsigned delta, unsigned q) {  // q = 
     ln.gives_J = lane >= delta;
     const bool odd = lane & 1u;
     ln.sh_own = odd ? 32u : 0u;
-    ln.ring = nullptr;
+    ln.ring_w = nullptr;
+    ln.ring_r = nullptr;
     ln.stage = nullptr;
-#pragma unroll
-    for (int S = 0; S < 4; ++S) ln.ld[S] = (32u * S + q + lane) & 127u;
+    (void)q;
     return ln;
 }
 
@@ -259,21 +268,23 @@ __device__ __forceinline__ void* advance(void* o, int n) {
 }
 
 // Four warp steps (one full register rotation) = 128 words of the stream.
-// Emits at cursor o (single-word modes: o[0], o[32], o[64], o[96]; pair modes:
-// o[0], o[32]) when EMIT; the tail variant masks by `limit` (values of this
-// body that are still wanted).
-template <int MODE, int VAR, bool TAIL, int BUF = 0, class P>
+// PH is the body's parity: its steps are T = 4*PH .. 4*PH+3 (mod 8) of the
+// shared-memory ring, and it selects the f64 stage buffer.  Emits at cursor o
+// (single-word modes: o[0], o[32], o[64], o[96]; pair modes: o[0], o[32]);
+// the tail variant masks by `limit` (values of this body still wanted).
+template <int MODE, int VAR, bool TAIL, int PH, class P>
 __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul& m, const Lane& ln,
                                       uint32_t& wl, uint32_t w_step, void* o, uint32_t& hits,
                                       unsigned limit) {
     constexpr bool kW = MODE != kRaw;  // Weyl output stage applied
-    const uint32_t v0 = warp_step<0, VAR>(R, p, m, ln);
+    constexpr int BUF = PH;
+    const uint32_t v0 = warp_step<4 * PH + 0, VAR>(R, p, m, ln);
     const uint32_t o0 = kW ? weyl_out<VAR>(wl, v0, p, m) : v0;
-    const uint32_t v1 = warp_step<1, VAR>(R, p, m, ln);
+    const uint32_t v1 = warp_step<4 * PH + 1, VAR>(R, p, m, ln);
     const uint32_t o1 = kW ? weyl_out<VAR>(wl + w_step, v1, p, m) : v1;
-    const uint32_t v2 = warp_step<2, VAR>(R, p, m, ln);
+    const uint32_t v2 = warp_step<4 * PH + 2, VAR>(R, p, m, ln);
     const uint32_t o2 = kW ? weyl_out<VAR>(wl + 2u * w_step, v2, p, m) : v2;
-    const uint32_t v3 = warp_step<3, VAR>(R, p, m, ln);
+    const uint32_t v3 = warp_step<4 * PH + 3, VAR>(R, p, m, ln);
     const uint32_t o3 = kW ? weyl_out<VAR>(wl + 3u * w_step, v3, p, m) : v3;
     wl += 4u * w_step;
     const unsigned lane = threadIdx.x & 31u;
@@ -350,10 +361,12 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
     const uint32_t w_step = 32u * p.omega;
     Lane ln = make_lane(p.delta, 32u * P::J + p.delta);
     if constexpr ((VAR & 16) != 0) {
-        __shared__ uint32_t ring[kWarpsPerBlock][kR];
-        ln.ring = ring[threadIdx.x >> 5];
+        __shared__ uint32_t ring[kWarpsPerBlock][256 + 32];
+        ln.ring_w = ring[threadIdx.x >> 5] + lane;
+        ln.ring_r = ring[threadIdx.x >> 5] + p.delta + lane;
+        // the window's blocks 0..3 count as produced at steps -4..-1: slots 4..7
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ln.ring[32 * j + lane] = R[j];
+        for (int j = 0; j < 4; ++j) ln.ring_w[32 * (4 + j)] = R[j];
         __syncwarp();
         if constexpr (MODE == kF64) {
             __shared__ __align__(16) uint32_t stage[kWarpsPerBlock][256];
@@ -387,11 +400,19 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
             body4<MODE, VAR, false, 1>(R, p, m, ln, wl, w_step, advance<MODE>(o, 3 * kValsPerBody), hits, 0);
             o = advance<MODE>(o, 4 * kValsPerBody);
         }
-        if constexpr (MODE == kF64) __syncwarp();  // retire stage reads before reuse
-#pragma unroll 1
-        for (; i < n; ++i) {
+        // 0-3 remaining bodies keep the parity sequence 0, 1, 0 (a chunk of
+        // 2^30 bodies is a multiple of 4, so every chunk starts at parity 0).
+        const uint32_t rem = n - i;
+        if (rem >= 1) {
             body4<MODE, VAR, false, 0>(R, p, m, ln, wl, w_step, o, hits, 0);
-            if constexpr (MODE == kF64) __syncwarp();
+            o = advance<MODE>(o, kValsPerBody);
+        }
+        if (rem >= 2) {
+            body4<MODE, VAR, false, 1>(R, p, m, ln, wl, w_step, o, hits, 0);
+            o = advance<MODE>(o, kValsPerBody);
+        }
+        if (rem >= 3) {
+            body4<MODE, VAR, false, 0>(R, p, m, ln, wl, w_step, o, hits, 0);
             o = advance<MODE>(o, kValsPerBody);
         }
     }
@@ -400,10 +421,12 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
     if (tail != 0) {
         // One more (full) 4-step body; only the first `tail` words are
         // emitted.  The state saved below ends exactly at word `words`.
-        if constexpr (MODE == kF64) __syncwarp();
         const uint32_t O[4] = {R[0], R[1], R[2], R[3]};
-        body4<MODE, VAR, true>(R, p, m, ln, wl, w_step, o, hits,
-                               MODE == kMC ? tail >> 6 : (kPairs ? tail >> 1 : tail));
+        const unsigned lim = MODE == kMC ? tail >> 6 : (kPairs ? tail >> 1 : tail);
+        if ((words >> 7) & 1)
+            body4<MODE, VAR, true, 1>(R, p, m, ln, wl, w_step, o, hits, lim);
+        else
+            body4<MODE, VAR, true, 0>(R, p, m, ln, wl, w_step, o, hits, lim);
         // New logical window = words [words-128, words): positions tail..tail+127
         // of the 256 words held in O (old window) followed by R (new block).
 #pragma unroll

@@ -1,0 +1,32 @@
+#!/usr/bin/env python3
+"""Small calls through every kernel mode, for compute-sanitizer
+(memcheck / racecheck / synccheck).  Checks results against the oracle too."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1108_0486_b200 as xg  # noqa: E402
+from oracle import Oracle  # noqa: E402
+
+o = Oracle()
+p = xg.xorgensgp32_params()
+for var_params in (p, xg.GeneratorParams(128, 95, 17, 12, 13, 15, 32, 2654435769, 16),
+                   xg.GeneratorParams(128, 33, 11, 7, 9, 19, 32, 0x6A09E667 | 1, 11)):
+    e = xg.BlockEnsemble(var_params, 3, 13, 32)
+    oe = o.ensemble(3, 13, o.params(var_params.r, var_params.s, var_params.a, var_params.b,
+                                    var_params.c, var_params.d, var_params.w, var_params.omega,
+                                    var_params.gamma))
+    for n in (1, 130, 515):
+        assert np.array_equal(e.fill_u32(n).cpu().numpy(), oe.fill_u32(n))
+        assert np.array_equal(e.fill_f32(n).cpu().numpy().view(np.uint32), oe.fill_f32(n).view(np.uint32))
+        assert np.array_equal(e.fill_f64(n).cpu().numpy().view(np.uint64), oe.fill_f64(n).view(np.uint64))
+        assert np.array_equal(e.fill_raw_u32(n).cpu().numpy(), oe.fill_raw_u32(n))
+        assert int(e.mc_pi(96).item()) == int(oe.mc_hits(96).sum())
+    st = xg.XorgensState(var_params, 9)
+    [st.next_word() for _ in range(50)]
+    e.generate(300)
+torch.cuda.synchronize()
+print("sanitize smoke ok")
