@@ -144,6 +144,17 @@ public:
         if (buf.size() != r_) throw std::invalid_argument("buffer size must equal r");
         check(xg_state_import(h_, i, buf.data(), weyl));
     }
+    // Whole-ensemble checkpoint: r window words per block (oldest first) + weyl.
+    void export_state(std::vector<std::uint32_t>& window, std::vector<std::uint32_t>& weyl) const {
+        window.resize(static_cast<std::size_t>(n_) * r_);
+        weyl.resize(n_);
+        check(xg_state_export_all(h_, window.data(), weyl.data()));
+    }
+    void import_state(const std::vector<std::uint32_t>& window, const std::vector<std::uint32_t>& weyl) {
+        if (window.size() != static_cast<std::size_t>(n_) * r_ || weyl.size() != n_)
+            throw std::invalid_argument("checkpoint size differs from the ensemble");
+        check(xg_state_import_all(h_, window.data(), weyl.data()));
+    }
     xg_ensemble_t handle() const noexcept { return h_; }
 
 protected:

@@ -42,6 +42,20 @@ int main() {
     auto rr = xg::XorgensState::from_raw(p, rs.logical_buffer(), rs.weyl_value());
     auto gr = xg::gpu::XorgensState::from_raw(p, rs.logical_buffer(), rs.weyl_value());
     for (int i = 0; i < 3000; ++i) CHECK(rr.next_word() == gr.next_word());
+    // Checkpoint / resume continues every block exactly.
+    {
+        xg::gpu::BlockEnsemble a(p, 11, 4, 63);
+        a.generate(1000);
+        std::vector<std::uint32_t> win, wy;
+        a.export_state(win, wy);
+        auto next_a = a.generate(500);
+        xg::gpu::BlockEnsemble b(p, 0, 4, 63);
+        b.import_state(win, wy);
+        CHECK(b.generate(500) == next_a);
+        xg::BlockEnsemble ref(p, 11, 4, 63);
+        ref.generate(1000);
+        CHECK(ref.generate(500) == next_a);
+    }
     // Same exception classes.
     bool threw = false;
     try { xg::gpu::BlockEnsemble bad(p, 0, 1, 64); } catch (const std::out_of_range&) { threw = true; }
