@@ -118,7 +118,9 @@ int cuda_rc(cudaError_t e) {
     return XG_ECUDA;
 }
 
-unsigned grid_for(uint32_t n) { return (n + kWarpsPerBlock - 1) / kWarpsPerBlock; }
+unsigned grid_for(uint32_t n) {
+    return static_cast<unsigned>((static_cast<uint64_t>(n) + kWarpsPerBlock - 1) / kWarpsPerBlock);
+}
 
 // Instruction-placement variant of the GP32 kernels (xg_kernels.cuh, VAR
 // mask): 16 (shared-memory s-tap) for every mode and parameter kind, from the
