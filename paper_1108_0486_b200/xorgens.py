@@ -339,6 +339,8 @@ class BlockEnsemble:
                               device=f"cuda:{self._h.device}")
         if out.numel() < self._n * vals_per_block or not out.is_contiguous():
             raise ValueError("output buffer too small or not contiguous")
+        if out.element_size() != torch.empty(0, dtype=torch_dtype).element_size() or not out.is_cuda:
+            raise ValueError(f"output buffer must be a CUDA tensor of {torch_dtype} width")
         _raise(fn(self._h.ptr, per_block, ctypes.c_void_p(out.data_ptr()), self._stream(stream)))
         return out
 
