@@ -9,10 +9,12 @@
 //
 //   x_{i+l} = T(W[l], a, b) ^ T(W[(r-s)+l], c, d)          (xorgens.hpp:39-47)
 //
-// W[l] is the lane's own R[0]; W[(r-s)+l] lives in lane (l+delta)&31 in
-// register J or J+1 ((r-s) = 32*J + delta), so it costs one select + one
-// shuffle.  The new word replaces R[0] and the window rotates by renaming
-// registers (4-step unroll), so there are no moves.  The Weyl term of lane l in
+// W[l] is the lane's own R[0].  W[(r-s)+l] ((r-s) = 32*J + delta) belongs to
+// another lane: by default it is read from a per-warp shared-memory ring that
+// mirrors the window (one STS of the new block + one LDS per step), or, in the
+// VAR 0 form, taken from lane (l+delta)&31's register J or J+1 with one
+// select + one shuffle.  The new word replaces R[0] and the window rotates by
+// renaming registers (4-step unroll), so there are no moves.  The Weyl term of lane l in
 // step k is weyl + (32k + l + 1)*omega (closed form, parallel.cpp:33-39), and
 // the output is ((w ^ (w >> gamma)) + x) mod 2^32 (xorgens.hpp:58-62).
 //
@@ -193,9 +195,9 @@ __device__ __forceinline__ void pair_f64(uint32_t a, uint32_t b, const Lane& ln,
 // 32 samples (w[64j+i], w[64j+32+i]), i = 0..31, with
 // no data movement between lanes.  Each word, read as a signed 32-bit integer,
 // is a coordinate in [-2^31, 2^31); the sample hits the disc iff
-// x^2 + y^2 < 2^62 (exact: q = x^2 - 2^62 + y^2 lies in [-2^62, 2^62]).
-// Returns 1 for a HIT (the sign bit of q).  Per sample: IMAD.WIDE, IMAD.HI and
-// one add -- no shifts, no selects.
+// x^2 + y^2 < 2^62 (exact).  Returns 1 for a hit.  Per sample ptxas emits
+// IMAD.WIDE + IMAD.HI (the high word of x^2 + y^2), one VIADD and a LEA.HI
+// that accumulates the sign bit -- no shifts, no selects.
 __device__ __forceinline__ uint32_t mc_hit(uint32_t a, uint32_t b) {
     const int64_t x = static_cast<int32_t>(a), y = static_cast<int32_t>(b);
     // x^2 + y^2 <= 2^63 fits in uint64; hit iff its high word is < 2^30,
@@ -213,7 +215,7 @@ __device__ __forceinline__ uint64_t splitmix_draw(uint64_t seed, uint64_t k) {
     return z ^ (z >> 31);
 }
 
-__device__ __forceinline__ Lane make_lane(unsigned delta, unsigned q) {  // q = r - s
+__device__ __forceinline__ Lane make_lane(unsigned delta) {
     Lane ln;
     const unsigned lane = threadIdx.x & 31u;
     ln.src = (lane + delta) & 31u;
@@ -223,7 +225,6 @@ __device__ __forceinline__ Lane make_lane(unsigned delta, unsigned q) {  // q = 
     ln.ring_w = nullptr;
     ln.ring_r = nullptr;
     ln.stage = nullptr;
-    (void)q;
     return ln;
 }
 
@@ -246,7 +247,7 @@ seed_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
     const uint32_t w0 = static_cast<uint32_t>(splitmix_draw(seed, kR + 1));
     const bool any = __any_sync(kFull, (R[0] | R[1] | R[2] | R[3]) != 0u);
     if (!any && lane == 0) R[0] = 0x7f4a7c15u;  // 0x9e3779b97f4a7c15 & mask (xorgens.cpp:28-29)
-    const Lane ln = make_lane(p.delta, 32u * P::J + p.delta);
+    const Lane ln = make_lane(p.delta);
 #pragma unroll 1
     for (int it = 0; it < 4; ++it) {  // 16 steps = 4r words
         warp_step<0, 0>(R, p, m, ln);
@@ -359,7 +360,7 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
     const uint32_t weyl0 = weyl[g];
     uint32_t wl = weyl0 + (lane + 1u) * p.omega;
     const uint32_t w_step = 32u * p.omega;
-    Lane ln = make_lane(p.delta, 32u * P::J + p.delta);
+    Lane ln = make_lane(p.delta);
     if constexpr ((VAR & 16) != 0) {
         __shared__ uint32_t ring[kWarpsPerBlock][256 + 32];
         ln.ring_w = ring[threadIdx.x >> 5] + lane;
