@@ -104,8 +104,8 @@ public:
     std::vector<std::vector<std::uint64_t>> generate(std::size_t per_block,
                                                      unsigned workers = 0) {
         (void)workers;  // the device schedule never changes the output
-        std::vector<std::uint32_t> flat(static_cast<std::size_t>(n_) * per_block);
-        if (per_block) check(xg_generate_host(h_, per_block, flat.data(), nullptr));
+        std::vector<std::uint64_t> flat(static_cast<std::size_t>(n_) * per_block);
+        if (per_block) check(xg_generate_host_words(h_, per_block, flat.data(), nullptr));
         std::vector<std::vector<std::uint64_t>> out(n_);
         for (unsigned i = 0; i < n_; ++i)
             out[i].assign(flat.begin() + static_cast<std::ptrdiff_t>(i * per_block),
@@ -187,8 +187,8 @@ public:
     }
 
     std::uint64_t next_word() {
-        std::uint32_t v;
-        check(xg_next_u32(h_, &v));
+        std::uint64_t v;
+        check(xg_next_word(h_, &v));
         return v;
     }
     std::uint64_t next_u64() {

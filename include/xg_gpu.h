@@ -19,8 +19,11 @@
  *                            [1, lane_bound], zero streams, stream index)
  *   XG_EINVAL                std::invalid_argument (NULL / misaligned buffer,
  *                            size overflow, wrong handle kind)
- *   XG_EUNSUPPORTED          valid parameters the GPU path does not implement
- *                            (it needs w = 32, r = 128, lane_bound >= 32)
+ *   XG_EUNSUPPORTED          the call is not defined for these parameters: the
+ *                            u64/f32/f64/MC conventions and whole-ensemble
+ *                            checkpoints need the w = 32, r = 128,
+ *                            lane_bound >= 32 kernels; 32-bit outputs need
+ *                            w <= 32; r > 16384 is not supported
  *   XG_ECUDA / XG_ENOMEM     CUDA runtime failure / device allocation failure
  */
 #ifndef XG_GPU_H
@@ -78,9 +81,13 @@ xg_params_t xg_params_xorgensgp32(void);
 xg_params_t xg_params_tiny_r2w8(void);
 xg_params_t xg_params_tiny_r2w16(void);
 xg_params_t xg_params_tiny_r4w16(void);
-/* XG_OK when the GPU kernels implement `p`, else the check_params code or
- * XG_EUNSUPPORTED. */
+/* XG_OK when the GPU can generate `p` (every valid set with r <= 16384), else
+ * the check_params code or XG_EUNSUPPORTED. */
 int xg_gpu_supported(const xg_params_t* p);
+/* 1 when `p` runs on the register-window kernels (w = 32, r = 128,
+ * lane_bound >= 32: xorgensgp32 and every set shaped like it), 0 when it runs
+ * on the general-parameter kernels (correct for any valid set, not tuned). */
+int xg_fast_path(const xg_params_t* p);
 
 /* ---- ensembles ----------------------------------------------------------- */
 
@@ -115,6 +122,11 @@ int xg_ensemble_info(xg_ensemble_t h, uint32_t* num_streams, uint64_t* base_seed
  * Byte-identical to `xgen gen --format raw-le --blocks`
  * (proj/tools/xgen.cpp:51-57,94-98). */
 int xg_fill_u32(xg_ensemble_t h, uint64_t per_stream, uint32_t* dev_out, xg_stream_t stream);
+/* Every word as a uint64 (the w-bit value zero-extended): exactly the element
+ * type and layout of BlockEnsemble::generate()'s result
+ * (proj/include/xg/parallel.hpp:46-47).  Works for every parameter set,
+ * including w = 64. */
+int xg_fill_words(xg_ensemble_t h, uint64_t per_stream, uint64_t* dev_out, xg_stream_t stream);
 /* Two consecutive words per value, lo = first: value = w[2k] | w[2k+1] << 32
  * (the raw-le stream read as little-endian uint64).  Not in the reference. */
 int xg_fill_u64(xg_ensemble_t h, uint64_t per_stream, uint64_t* dev_out, xg_stream_t stream);
@@ -147,11 +159,17 @@ int xg_skip(xg_ensemble_t h, uint64_t words, xg_stream_t stream);
  * overlapping generation.  host_out should be pinned for full speed. */
 int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,
                      xg_stream_t stream);
+/* The same with every word in the reference's uint64 container -- exactly
+ * the element type of generate()'s result; any w, including 64. */
+int xg_generate_host_words(xg_ensemble_t h, uint64_t per_stream, uint64_t* host_out,
+                           xg_stream_t stream);
 /* XorgensState::next_word (proj/include/xg/xorgens.hpp:58-62) on a
- * one-stream handle, served from device-generated refills; interleaving with
- * fills / exports keeps the exact serial stream. */
+ * one-stream handle: the w-bit word in a uint64, served from device-generated
+ * refills; interleaving with fills / exports keeps the exact serial stream. */
+int xg_next_word(xg_ensemble_t h, uint64_t* out);
+/* next_word as uint32 (w <= 32). */
 int xg_next_u32(xg_ensemble_t h, uint32_t* out);
-/* Two next_u32 values, lo = first. */
+/* w = 32: two words, lo = first; w = 64: one word. */
 int xg_next_u64(xg_ensemble_t h, uint64_t* out);
 /* logical_buffer() + weyl_value() of stream `index`
  * (proj/include/xg/xorgens.hpp:72-76): r words oldest first. */

@@ -60,7 +60,7 @@ class Oracle:
         L.xgo_stream_u32.argtypes = [ctypes.POINTER(Params), _u64, _u64, _vp]
         L.xgo_ensemble_seed.argtypes = [_vp, ctypes.POINTER(Params), _u64, _u64, _u32, _int]
         for n in ("xgo_ensemble_fill_u32", "xgo_ensemble_fill_f32", "xgo_ensemble_fill_f64",
-                  "xgo_ensemble_mc_pi", "xgo_ensemble_fill_raw_u32"):
+                  "xgo_ensemble_mc_pi", "xgo_ensemble_fill_raw_u32", "xgo_ensemble_fill_words"):
             getattr(L, n).argtypes = [_vp, _u32, _u64, _vp, _int]
         L.xgo_ensemble_checksums.argtypes = [_vp, _u32, _u64, _vp, _vp, _int]
         L.xgo_batch_step.argtypes = [_vp, ctypes.c_uint, _vp]
@@ -148,6 +148,11 @@ class OracleEnsemble:
     def fill_u32(self, per_stream: int) -> np.ndarray:
         out = np.empty((self.n, per_stream), dtype=np.uint32)
         self.o.lib.xgo_ensemble_fill_u32(self.buf, self.n, per_stream, _ptr(out), self.o.threads)
+        return out
+
+    def fill_words(self, per_stream: int) -> np.ndarray:
+        out = np.empty((self.n, per_stream), dtype=np.uint64)
+        self.o.lib.xgo_ensemble_fill_words(self.buf, self.n, per_stream, _ptr(out), self.o.threads)
         return out
 
     def fill_raw_u32(self, per_stream: int) -> np.ndarray:

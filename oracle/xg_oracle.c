@@ -260,7 +260,7 @@ typedef struct {
     uint32_t t, used;
 } job_t;
 
-enum { J_SEED, J_U32, J_F32, J_F64, J_MC, J_SUM, J_RAW };
+enum { J_SEED, J_U32, J_F32, J_F64, J_MC, J_SUM, J_RAW, J_WORDS };
 
 static void run_one(job_t* j, uint32_t g) {
     xgo_state* st = &j->states[g];
@@ -273,6 +273,12 @@ static void run_one(job_t* j, uint32_t g) {
     case J_U32: {
         uint32_t* o = (uint32_t*)j->out + (size_t)g * j->n;
         for (uint64_t k = 0; k < j->n; ++k) o[k] = (uint32_t)xgo_next_word(st);
+        break;
+    }
+    case J_WORDS: {
+        /* next_word() values in their uint64 container (BlockEnsemble::generate) */
+        uint64_t* o = (uint64_t*)j->out + (size_t)g * j->n;
+        for (uint64_t k = 0; k < j->n; ++k) o[k] = xgo_next_word(st);
         break;
     }
     case J_RAW: {
@@ -392,6 +398,10 @@ static int fill(int kind, xgo_state* states, uint32_t num_streams, uint64_t n, v
 int xgo_ensemble_fill_u32(xgo_state* states, uint32_t num_streams, uint64_t per_stream,
                           uint32_t* out, int threads) {
     return fill(J_U32, states, num_streams, per_stream, out, NULL, threads);
+}
+int xgo_ensemble_fill_words(xgo_state* states, uint32_t num_streams, uint64_t per_stream,
+                             uint64_t* out, int threads) {
+    return fill(J_WORDS, states, num_streams, per_stream, out, NULL, threads);
 }
 int xgo_ensemble_fill_raw_u32(xgo_state* states, uint32_t num_streams, uint64_t per_stream,
                               uint32_t* out, int threads) {

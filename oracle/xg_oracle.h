@@ -79,6 +79,9 @@ int xgo_ensemble_seed(xgo_state* states, const xgo_params* p, uint64_t base_seed
 /* Block-major fill, continuing each state: out[g*per_stream + k]. */
 int xgo_ensemble_fill_u32(xgo_state* states, uint32_t num_streams, uint64_t per_stream,
                           uint32_t* out, int threads);
+/* Words in the reference's uint64 container (any w). */
+int xgo_ensemble_fill_words(xgo_state* states, uint32_t num_streams, uint64_t per_stream,
+                            uint64_t* out, int threads);
 /* Weyl-ablated linear stream (RawXorgens, proj/include/xg/baselines.hpp:60-71). */
 int xgo_ensemble_fill_raw_u32(xgo_state* states, uint32_t num_streams, uint64_t per_stream,
                               uint32_t* out, int threads);

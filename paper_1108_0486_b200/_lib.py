@@ -50,6 +50,7 @@ SIGNATURES = {
     "xg_params_tiny_r2w16": (xg_params_t, []),
     "xg_params_tiny_r4w16": (xg_params_t, []),
     "xg_gpu_supported": (_int, [_P(xg_params_t)]),
+    "xg_fast_path": (_int, [_P(xg_params_t)]),
     "xg_ensemble_create": (_int, [_P(xg_params_t), _u64, _u64, _u32, ctypes.c_uint, _int, _vp,
                                   _P(_vp)]),
     "xg_ensemble_create_from_raw": (_int, [_P(xg_params_t), _u32, _P(_u64), _P(_u64), _int, _vp,
@@ -58,12 +59,15 @@ SIGNATURES = {
     "xg_ensemble_info": (_int, [_vp, _P(_u32), _P(_u64), _P(_u64), _P(ctypes.c_uint), _P(_int)]),
     "xg_fill_u32": (_int, [_vp, _u64, _vp, _vp]),
     "xg_fill_u64": (_int, [_vp, _u64, _vp, _vp]),
+    "xg_fill_words": (_int, [_vp, _u64, _vp, _vp]),
     "xg_fill_f32": (_int, [_vp, _u64, _vp, _vp]),
     "xg_fill_raw_u32": (_int, [_vp, _u64, _vp, _vp]),
     "xg_fill_f64": (_int, [_vp, _u64, _vp, _vp]),
     "xg_mc_pi": (_int, [_vp, _u64, _vp, _vp]),
     "xg_skip": (_int, [_vp, _u64, _vp]),
     "xg_generate_host": (_int, [_vp, _u64, _vp, _vp]),
+    "xg_generate_host_words": (_int, [_vp, _u64, _vp, _vp]),
+    "xg_next_word": (_int, [_vp, _P(_u64)]),
     "xg_next_u32": (_int, [_vp, _P(_u32)]),
     "xg_next_u64": (_int, [_vp, _P(_u64)]),
     "xg_state_export": (_int, [_vp, _u32, _P(_u64), _P(_u64)]),

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "xg_gpu.h"
+#include "xg_generic.cuh"
 #include "xg_kernels.cuh"
 
 using namespace xgk;
@@ -26,9 +27,12 @@ namespace {
 std::atomic<uint64_t> g_launches{0};
 
 constexpr uint32_t kMask32 = 0xffffffffu;
-constexpr size_t kNextBuf = 1u << 14;  // words per next_u32 refill
+constexpr size_t kNextBuf = 1u << 14;  // words per next_word refill
+constexpr unsigned kGenMaxR = 16384;   // generic path: r words of state in shared memory
 
-enum Kind { kGP32 = 0, kRtJ1 = 1, kRtJ2 = 2 };
+// kGP32 / kRtJ*: register-window kernels (w = 32, r = 128, lane_bound >= 32);
+// kGeneric: any other valid set (xg_generic.cuh).
+enum Kind { kGP32 = 0, kRtJ1 = 1, kRtJ2 = 2, kGeneric = 3 };
 
 struct DeviceGuard {
     int prev = -1;
@@ -53,14 +57,16 @@ struct xg_ensemble {
     unsigned lanes = 0;
     uint32_t* d_win = nullptr;   // [num_streams][128] logical window, oldest first
     uint32_t* d_weyl = nullptr;  // [num_streams] Weyl accumulator
-    // next_u32 service (one-stream handles)
-    std::vector<uint32_t> nbuf;
+    uint64_t* d_win64 = nullptr;   // generic path: [num_streams][r] words, oldest first
+    uint64_t* d_weyl64 = nullptr;  // generic path: [num_streams]
+    // next_word service (one-stream handles)
+    std::vector<uint64_t> nbuf;
     size_t npos = 0;
-    uint32_t* d_snap = nullptr;  // 129-word state snapshot taken before a refill
-    uint32_t* d_scratch = nullptr;
+    void* d_snap = nullptr;  // state snapshot taken before a refill
+    uint64_t* d_scratch = nullptr;
     // xg_generate_host staging
-    uint32_t* d_stage = nullptr;
-    size_t stage_words = 0;
+    void* d_stage = nullptr;
+    size_t stage_words = 0;  // bytes
 };
 
 namespace {
@@ -89,7 +95,11 @@ bool is_gp32(const xg_params_t* p) {
 int classify(const xg_params_t* p, Kind* kind) {
     int e = check_params_impl(p);
     if (e) return e;
-    if (p->w != 32 || p->r != kR || lane_bound_impl(p) < 32) return XG_EUNSUPPORTED;
+    if (p->w != 32 || p->r != kR || lane_bound_impl(p) < 32) {
+        if (p->r > kGenMaxR) return XG_EUNSUPPORTED;
+        *kind = kGeneric;
+        return XG_OK;
+    }
     if (is_gp32(p)) {
         *kind = kGP32;
     } else {
@@ -153,10 +163,56 @@ int launch_fill_v(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count
     return cuda_rc(cudaGetLastError());
 }
 
+GenParams gen_params(const xg_params_t& p) {
+    GenParams g;
+    g.r = p.r; g.s = p.s; g.a = p.a; g.b = p.b; g.c = p.c; g.d = p.d; g.w = p.w;
+    g.gamma = p.gamma;
+    g.lanes = std::min(32u, lane_bound_impl(&p));
+    g.omega = p.omega;
+    g.mask = p.w >= 64 ? ~0ull : ((1ull << p.w) - 1);
+    return g;
+}
+
+size_t gen_smem(const xg_params_t& p) { return static_cast<size_t>(p.r) * sizeof(uint64_t); }
+
+template <class K>
+int gen_smem_attr(K kernel, size_t smem) {
+    if (smem <= 48 * 1024) return XG_OK;
+    return cuda_rc(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+}
+
+template <int GM>
+int launch_gen(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t words, void* out,
+               cudaStream_t s) {
+    const size_t smem = gen_smem(h->params);
+    int rc = gen_smem_attr(gen_fill_kernel<GM>, smem);
+    if (rc) return rc;
+    gen_fill_kernel<GM><<<g_count, 32, smem, s>>>(gen_params(h->params), h->d_win64, h->d_weyl64,
+                                                   g_begin, g_count, words, out);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cuda_rc(cudaGetLastError());
+}
+
 template <int MODE>
 int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t words, void* out,
                 unsigned long long* hits, cudaStream_t s) {
     if (words == 0 || g_count == 0) return XG_OK;
+    if (h->kind == kGeneric) {
+        // The conversions (f32/f64/u64 pairs) and the MC predicate are defined
+        // on 32-bit words; the generic path offers the words themselves.
+        const bool narrow = h->params.w <= 32;
+        if constexpr (MODE == kU32) {
+            if (narrow) return launch_gen<kGenU32>(h, g_begin, g_count, words, out, s);
+        } else if constexpr (MODE == kRaw) {
+            if (narrow) return launch_gen<kGenRawU32>(h, g_begin, g_count, words, out, s);
+        } else if constexpr (MODE == kWide) {
+            return launch_gen<kGenWide>(h, g_begin, g_count, words, out, s);
+        } else if constexpr (MODE == kSkip) {
+            return launch_gen<kGenSkip>(h, g_begin, g_count, words, out, s);
+        }
+        return XG_EUNSUPPORTED;
+    }
     switch (h->kind) {
     case kGP32:
         switch (variant_for(MODE)) {
@@ -176,6 +232,14 @@ int launch_seed(xg_ensemble* h, uint64_t seed0, cudaStream_t s) {
     const unsigned grid = grid_for(h->num_streams);
     const HiMul m = himul(h->params);
     switch (h->kind) {
+    case kGeneric: {
+        const size_t smem = gen_smem(h->params);
+        int rc = gen_smem_attr(gen_seed_kernel, smem);
+        if (rc) return rc;
+        gen_seed_kernel<<<h->num_streams, 32, smem, s>>>(gen_params(h->params), h->d_win64,
+                                                        h->d_weyl64, h->num_streams, seed0);
+        break;
+    }
     case kGP32:
         seed_kernel<<<grid, kThreads, 0, s>>>(GP32{}, m, h->d_win, h->d_weyl, h->num_streams, seed0);
         break;
@@ -194,6 +258,11 @@ int launch_seed(xg_ensemble* h, uint64_t seed0, cudaStream_t s) {
 
 int alloc_state(xg_ensemble* h) {
     const size_t n = static_cast<size_t>(h->num_streams);
+    if (h->kind == kGeneric) {
+        int rc = cuda_rc(cudaMalloc(&h->d_win64, n * h->params.r * sizeof(uint64_t)));
+        if (rc) return rc;
+        return cuda_rc(cudaMalloc(&h->d_weyl64, n * sizeof(uint64_t)));
+    }
     int rc = cuda_rc(cudaMalloc(&h->d_win, n * kR * sizeof(uint32_t)));
     if (rc) return rc;
     return cuda_rc(cudaMalloc(&h->d_weyl, n * sizeof(uint32_t)));
@@ -205,6 +274,8 @@ void free_handle(xg_ensemble* h) {
         DeviceGuard dg(h->device);
         cudaFree(h->d_win);
         cudaFree(h->d_weyl);
+        cudaFree(h->d_win64);
+        cudaFree(h->d_weyl64);
         cudaFree(h->d_snap);
         cudaFree(h->d_scratch);
         cudaFree(h->d_stage);
@@ -212,7 +283,27 @@ void free_handle(xg_ensemble* h) {
     delete h;
 }
 
-// Buffered next_u32 words that were generated but not served are given back:
+// Device-side copy of stream 0's whole state to / from a snapshot buffer.
+size_t state_bytes(const xg_ensemble* h, size_t* win_bytes) {
+    *win_bytes = h->kind == kGeneric ? h->params.r * sizeof(uint64_t) : kR * sizeof(uint32_t);
+    return *win_bytes + sizeof(uint64_t);
+}
+
+int copy_state(xg_ensemble* h, void* snap, bool to_snapshot, cudaStream_t s) {
+    size_t wb;
+    state_bytes(h, &wb);
+    char* sn = static_cast<char*>(snap);
+    void* win = h->kind == kGeneric ? static_cast<void*>(h->d_win64) : static_cast<void*>(h->d_win);
+    void* wy = h->kind == kGeneric ? static_cast<void*>(h->d_weyl64) : static_cast<void*>(h->d_weyl);
+    const size_t wyb = h->kind == kGeneric ? sizeof(uint64_t) : sizeof(uint32_t);
+    const cudaMemcpyKind k = cudaMemcpyDeviceToDevice;
+    int rc = cuda_rc(to_snapshot ? cudaMemcpyAsync(sn, win, wb, k, s) : cudaMemcpyAsync(win, sn, wb, k, s));
+    if (rc) return rc;
+    return cuda_rc(to_snapshot ? cudaMemcpyAsync(sn + wb, wy, wyb, k, s)
+                               : cudaMemcpyAsync(wy, sn + wb, wyb, k, s));
+}
+
+// Buffered next_word values that were generated but not served are given back:
 // restore the pre-refill snapshot and re-advance by the served count, so the
 // device state is exactly "after the last word the caller saw".
 int settle_next(xg_ensemble* h, cudaStream_t s) {
@@ -221,11 +312,7 @@ int settle_next(xg_ensemble* h, cudaStream_t s) {
     h->nbuf.clear();
     h->npos = 0;
     if (served == held) return XG_OK;
-    int rc = cuda_rc(cudaMemcpyAsync(h->d_win, h->d_snap, kR * sizeof(uint32_t),
-                                     cudaMemcpyDeviceToDevice, s));
-    if (rc) return rc;
-    rc = cuda_rc(cudaMemcpyAsync(h->d_weyl, h->d_snap + kR, sizeof(uint32_t),
-                                 cudaMemcpyDeviceToDevice, s));
+    int rc = copy_state(h, h->d_snap, /*to_snapshot=*/false, s);
     if (rc) return rc;
     return launch_fill<kSkip>(h, 0, 1, served, nullptr, nullptr, s);
 }
@@ -250,6 +337,7 @@ int fill_common(xg_ensemble_t h, uint64_t per_stream, void* dev_out, size_t alig
     case kU32: return launch_fill<kU32>(h, 0, h->num_streams, per_stream, dev_out, nullptr, s);
     case kF32: return launch_fill<kF32>(h, 0, h->num_streams, per_stream, dev_out, nullptr, s);
     case kRaw: return launch_fill<kRaw>(h, 0, h->num_streams, per_stream, dev_out, nullptr, s);
+    case kWide: return launch_fill<kWide>(h, 0, h->num_streams, per_stream, dev_out, nullptr, s);
     case kF64: {
         uint64_t words;
         if (mul_overflows(per_stream, 2, &words)) return XG_EINVAL;
@@ -277,7 +365,7 @@ const char* xg_strerror(int code) {
     case XG_EPARAM_EVEN_WEYL_INCREMENT: return "Weyl increment omega must be odd";
     case XG_ERANGE: return "argument out of range";
     case XG_EINVAL: return "invalid argument";
-    case XG_EUNSUPPORTED: return "parameters not supported by the GPU path (needs w=32, r=128, lane_bound>=32)";
+    case XG_EUNSUPPORTED: return "not available for these parameters (the f32/f64/u64/MC conventions need w=32, r=128, lane_bound>=32; r <= 16384)";
     case XG_ECUDA: return "CUDA runtime error";
     case XG_ENOMEM: return "device memory allocation failed";
     default: return "unknown error";
@@ -315,6 +403,11 @@ xg_params_t xg_params_tiny_r4w16(void) { return make_set(4, 3, 1, 2, 5, 8, 16); 
 int xg_gpu_supported(const xg_params_t* p) {
     Kind k;
     return classify(p, &k);
+}
+
+int xg_fast_path(const xg_params_t* p) {
+    Kind k;
+    return classify(p, &k) == XG_OK && k != kGeneric ? 1 : 0;
 }
 
 int xg_ensemble_create(const xg_params_t* p, uint64_t base_seed, uint64_t first_stream,
@@ -373,11 +466,19 @@ int xg_ensemble_create_from_raw(const xg_params_t* p, uint32_t num_streams,
     h->num_streams = num_streams;
     h->lanes = lane_bound_impl(p);
     int rc = alloc_state(h);
-    if (!rc) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (!rc && kind == kGeneric) {
+        const uint64_t mask = p->w >= 64 ? ~0ull : ((1ull << p->w) - 1);
+        std::vector<uint64_t> win(static_cast<size_t>(num_streams) * p->r), wy(num_streams);
+        for (size_t i = 0; i < win.size(); ++i) win[i] = buffers[i] & mask;
+        for (size_t i = 0; i < wy.size(); ++i) wy[i] = weyls[i] & mask;
+        rc = cuda_rc(cudaMemcpyAsync(h->d_win64, win.data(), win.size() * 8, cudaMemcpyHostToDevice, s));
+        if (!rc) rc = cuda_rc(cudaMemcpyAsync(h->d_weyl64, wy.data(), wy.size() * 8, cudaMemcpyHostToDevice, s));
+        if (!rc) rc = cuda_rc(cudaStreamSynchronize(s));
+    } else if (!rc) {
         std::vector<uint32_t> win(static_cast<size_t>(num_streams) * kR), wy(num_streams);
         for (size_t i = 0; i < win.size(); ++i) win[i] = static_cast<uint32_t>(buffers[i] & kMask32);
         for (size_t i = 0; i < wy.size(); ++i) wy[i] = static_cast<uint32_t>(weyls[i] & kMask32);
-        cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
         rc = cuda_rc(cudaMemcpyAsync(h->d_win, win.data(), win.size() * 4, cudaMemcpyHostToDevice, s));
         if (!rc) rc = cuda_rc(cudaMemcpyAsync(h->d_weyl, wy.data(), wy.size() * 4, cudaMemcpyHostToDevice, s));
         if (!rc) rc = cuda_rc(cudaStreamSynchronize(s));
@@ -411,7 +512,12 @@ int xg_fill_u32(xg_ensemble_t h, uint64_t per_stream, uint32_t* dev_out, xg_stre
     return fill_common(h, per_stream, dev_out, 4, kU32, stream);
 }
 
+int xg_fill_words(xg_ensemble_t h, uint64_t per_stream, uint64_t* dev_out, xg_stream_t stream) {
+    return fill_common(h, per_stream, dev_out, 8, kWide, stream);
+}
+
 int xg_fill_u64(xg_ensemble_t h, uint64_t per_stream, uint64_t* dev_out, xg_stream_t stream) {
+    if (h && h->kind == kGeneric) return XG_EUNSUPPORTED;
     uint64_t words;
     if (mul_overflows(per_stream, 2, &words)) return XG_EINVAL;
     if (reinterpret_cast<uintptr_t>(dev_out) % 8 != 0) return XG_EINVAL;
@@ -466,8 +572,14 @@ int xg_skip(xg_ensemble_t h, uint64_t words, xg_stream_t stream) {
     return launch_fill<kSkip>(h, 0, h->num_streams, words, nullptr, nullptr, s);
 }
 
-int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,
-                     xg_stream_t stream) {
+}  // extern "C"
+
+namespace {
+
+// BlockEnsemble::generate into host memory, element T (uint32 words or the
+// reference's uint64 container), produced by kernel mode MODE.
+template <int MODE, class T>
+int generate_host_impl(xg_ensemble_t h, uint64_t per_stream, T* host_out, xg_stream_t stream) {
     if (!h) return XG_EINVAL;
     uint64_t total;
     if (mul_overflows(per_stream, h->num_streams, &total)) return XG_EINVAL;
@@ -484,7 +596,7 @@ int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,
     // chunks in order, so the continuation is exact).  Tile i is generated on
     // `s` while tile i-1 is copied (2D, into the block-major host layout) on a
     // second stream.
-    constexpr uint64_t kSlotWords = 1ull << 26;
+    constexpr uint64_t kSlotWords = (1ull << 28) / sizeof(T);  // 256 MiB per staging slot
     constexpr uint64_t kGroup = 2048;
     uint64_t cnt_max, m_max;
     if (per_stream <= kSlotWords) {
@@ -495,13 +607,13 @@ int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,
         m_max = (kSlotWords / cnt_max) & ~uint64_t{127};
     }
     const uint64_t slot_words = cnt_max * m_max;
-    if (h->stage_words < 2 * slot_words) {
+    if (h->stage_words < 2 * slot_words * sizeof(T)) {
         cudaFree(h->d_stage);
         h->d_stage = nullptr;
         h->stage_words = 0;
-        rc = cuda_rc(cudaMalloc(&h->d_stage, 2 * slot_words * sizeof(uint32_t)));
+        rc = cuda_rc(cudaMalloc(&h->d_stage, 2 * slot_words * sizeof(T)));
         if (rc) return rc;
-        h->stage_words = 2 * slot_words;
+        h->stage_words = 2 * slot_words * sizeof(T);
     }
     cudaStream_t cs;
     rc = cuda_rc(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -517,14 +629,15 @@ int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,
         const uint32_t cnt = static_cast<uint32_t>(std::min<uint64_t>(cnt_max, h->num_streams - g0));
         for (uint64_t k0 = 0; k0 < per_stream && !rc; k0 += m_max) {
             const uint64_t m = std::min<uint64_t>(m_max, per_stream - k0);
-            uint32_t* d = h->d_stage + slot * slot_words;
+            T* d = reinterpret_cast<T*>(h->d_stage) + slot * slot_words;
             cudaStreamWaitEvent(s, copy_done[slot], 0);
-            rc = launch_fill<kU32>(h, static_cast<uint32_t>(g0), cnt, m, d, nullptr, s);
+            rc = launch_fill<MODE>(h, static_cast<uint32_t>(g0), cnt, m, d, nullptr, s);
             if (rc) break;
             cudaEventRecord(gen_done[slot], s);
             cudaStreamWaitEvent(cs, gen_done[slot], 0);
-            rc = cuda_rc(cudaMemcpy2DAsync(host_out + g0 * per_stream + k0, per_stream * 4, d, m * 4,
-                                           m * 4, cnt, cudaMemcpyDeviceToHost, cs));
+            rc = cuda_rc(cudaMemcpy2DAsync(host_out + g0 * per_stream + k0, per_stream * sizeof(T), d,
+                                           m * sizeof(T), m * sizeof(T), cnt,
+                                           cudaMemcpyDeviceToHost, cs));
             cudaEventRecord(copy_done[slot], cs);
             slot ^= 1;
         }
@@ -539,7 +652,24 @@ int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,
     return rc ? rc : (rc2 ? rc2 : rc3);
 }
 
-int xg_next_u32(xg_ensemble_t h, uint32_t* out) {
+}  // namespace
+
+extern "C" {
+
+int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,
+                     xg_stream_t stream) {
+    if (h && h->params.w > 32) return XG_EUNSUPPORTED;  // xg_generate_host_words for w = 64
+    return generate_host_impl<kU32>(h, per_stream, host_out, stream);
+}
+
+int xg_generate_host_words(xg_ensemble_t h, uint64_t per_stream, uint64_t* host_out,
+                           xg_stream_t stream) {
+    return generate_host_impl<kWide>(h, per_stream, host_out, stream);
+}
+
+// XorgensState::next_word (proj/include/xg/xorgens.hpp:58-62): the w-bit
+// word in a uint64, served from device-generated refills of kNextBuf words.
+int xg_next_word(xg_ensemble_t h, uint64_t* out) {
     if (!h || !out) return XG_EINVAL;
     if (h->num_streams != 1) return XG_EINVAL;
     if (h->npos < h->nbuf.size()) {
@@ -550,15 +680,16 @@ int xg_next_u32(xg_ensemble_t h, uint32_t* out) {
     if (!dg.ok) return XG_ECUDA;
     // Host-synchronous call: order after any fill the caller queued on any stream.
     int rc = cuda_rc(cudaDeviceSynchronize());
-    if (!rc && !h->d_snap) rc = cuda_rc(cudaMalloc(&h->d_snap, (kR + 4) * sizeof(uint32_t)));
-    if (!rc && !h->d_scratch) rc = cuda_rc(cudaMalloc(&h->d_scratch, kNextBuf * sizeof(uint32_t)));
+    size_t wb;
+    const size_t snap_bytes = state_bytes(h, &wb);
+    if (!rc && !h->d_snap) rc = cuda_rc(cudaMalloc(&h->d_snap, snap_bytes));
+    if (!rc && !h->d_scratch) rc = cuda_rc(cudaMalloc(&h->d_scratch, kNextBuf * sizeof(uint64_t)));
     if (rc) return rc;
     cudaStream_t s = nullptr;
-    rc = cuda_rc(cudaMemcpyAsync(h->d_snap, h->d_win, kR * 4, cudaMemcpyDeviceToDevice, s));
-    if (!rc) rc = cuda_rc(cudaMemcpyAsync(h->d_snap + kR, h->d_weyl, 4, cudaMemcpyDeviceToDevice, s));
-    if (!rc) rc = launch_fill<kU32>(h, 0, 1, kNextBuf, h->d_scratch, nullptr, s);
+    rc = copy_state(h, h->d_snap, /*to_snapshot=*/true, s);
+    if (!rc) rc = launch_fill<kWide>(h, 0, 1, kNextBuf, h->d_scratch, nullptr, s);
     h->nbuf.assign(kNextBuf, 0);
-    if (!rc) rc = cuda_rc(cudaMemcpy(h->nbuf.data(), h->d_scratch, kNextBuf * 4, cudaMemcpyDeviceToHost));
+    if (!rc) rc = cuda_rc(cudaMemcpy(h->nbuf.data(), h->d_scratch, kNextBuf * 8, cudaMemcpyDeviceToHost));
     if (rc) {
         h->nbuf.clear();
         h->npos = 0;
@@ -569,14 +700,25 @@ int xg_next_u32(xg_ensemble_t h, uint32_t* out) {
     return XG_OK;
 }
 
+int xg_next_u32(xg_ensemble_t h, uint32_t* out) {
+    if (!h || !out) return XG_EINVAL;
+    if (h->params.w > 32) return XG_EUNSUPPORTED;
+    uint64_t v;
+    int rc = xg_next_word(h, &v);
+    if (!rc) *out = static_cast<uint32_t>(v);
+    return rc;
+}
+
 int xg_next_u64(xg_ensemble_t h, uint64_t* out) {
-    if (!out) return XG_EINVAL;
-    uint32_t lo, hi;
-    int rc = xg_next_u32(h, &lo);
+    if (!h || !out) return XG_EINVAL;
+    if (h->params.w == 64) return xg_next_word(h, out);
+    if (h->params.w != 32) return XG_EUNSUPPORTED;
+    uint64_t lo, hi;
+    int rc = xg_next_word(h, &lo);
     if (rc) return rc;
-    rc = xg_next_u32(h, &hi);
+    rc = xg_next_word(h, &hi);
     if (rc) return rc;
-    *out = static_cast<uint64_t>(lo) | (static_cast<uint64_t>(hi) << 32);
+    *out = lo | (hi << 32);
     return XG_OK;
 }
 
@@ -588,6 +730,13 @@ int xg_state_export(xg_ensemble_t h, uint32_t index, uint64_t* buffer, uint64_t*
     int rc = cuda_rc(cudaDeviceSynchronize());
     if (!rc) rc = settle_next(h, nullptr);
     if (rc) return rc;
+    if (h->kind == kGeneric) {
+        const unsigned r = h->params.r;
+        rc = cuda_rc(cudaMemcpy(buffer, h->d_win64 + static_cast<size_t>(index) * r, r * 8,
+                                cudaMemcpyDeviceToHost));
+        if (!rc) rc = cuda_rc(cudaMemcpy(weyl, h->d_weyl64 + index, 8, cudaMemcpyDeviceToHost));
+        return rc;
+    }
     uint32_t win[kR], wy;
     rc = cuda_rc(cudaMemcpy(win, h->d_win + static_cast<size_t>(index) * kR, sizeof win,
                             cudaMemcpyDeviceToHost));
@@ -606,6 +755,17 @@ int xg_state_import(xg_ensemble_t h, uint32_t index, const uint64_t* buffer, uin
     int rc = cuda_rc(cudaDeviceSynchronize());
     if (!rc) rc = settle_next(h, nullptr);
     if (rc) return rc;
+    if (h->kind == kGeneric) {
+        const unsigned r = h->params.r;
+        const uint64_t mask = h->params.w >= 64 ? ~0ull : ((1ull << h->params.w) - 1);
+        std::vector<uint64_t> win(buffer, buffer + r);
+        for (auto& v : win) v &= mask;
+        const uint64_t wy = weyl & mask;
+        rc = cuda_rc(cudaMemcpy(h->d_win64 + static_cast<size_t>(index) * r, win.data(), r * 8,
+                                cudaMemcpyHostToDevice));
+        if (!rc) rc = cuda_rc(cudaMemcpy(h->d_weyl64 + index, &wy, 8, cudaMemcpyHostToDevice));
+        return rc;
+    }
     uint32_t win[kR];
     for (unsigned i = 0; i < kR; ++i) win[i] = static_cast<uint32_t>(buffer[i] & kMask32);
     const uint32_t wy = static_cast<uint32_t>(weyl & kMask32);
@@ -617,6 +777,7 @@ int xg_state_import(xg_ensemble_t h, uint32_t index, const uint64_t* buffer, uin
 
 int xg_state_export_all(xg_ensemble_t h, uint32_t* host_window, uint32_t* host_weyl) {
     if (!h || !host_window || !host_weyl) return XG_EINVAL;
+    if (h->kind == kGeneric) return XG_EUNSUPPORTED;
     DeviceGuard dg(h->device);
     if (!dg.ok) return XG_ECUDA;
     int rc = cuda_rc(cudaDeviceSynchronize());
@@ -629,6 +790,7 @@ int xg_state_export_all(xg_ensemble_t h, uint32_t* host_window, uint32_t* host_w
 
 int xg_state_import_all(xg_ensemble_t h, const uint32_t* host_window, const uint32_t* host_weyl) {
     if (!h || !host_window || !host_weyl) return XG_EINVAL;
+    if (h->kind == kGeneric) return XG_EUNSUPPORTED;
     DeviceGuard dg(h->device);
     if (!dg.ok) return XG_ECUDA;
     int rc = cuda_rc(cudaDeviceSynchronize());

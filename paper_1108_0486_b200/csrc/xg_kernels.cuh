@@ -71,7 +71,9 @@ struct HiMul {
 // kRaw: the linear recurrence alone (RawXorgens::next = step_linear,
 // proj/include/xg/baselines.hpp:60-71, registry id "xorgens-raw"): emits x_i
 // and leaves the Weyl accumulator untouched.
-enum Mode : int { kU32 = 0, kF32 = 1, kF64 = 2, kMC = 3, kSkip = 4, kRaw = 5 };
+// kWide: each word zero-extended to uint64 -- the element type of the
+// reference's generate() result (proj/include/xg/parallel.hpp:46-47).
+enum Mode : int { kU32 = 0, kF32 = 1, kF64 = 2, kMC = 3, kSkip = 4, kRaw = 5, kWide = 6 };
 
 template <bool HI>
 __device__ __forceinline__ uint32_t shr(uint32_t x, unsigned k, uint32_t mul) {
@@ -264,6 +266,7 @@ seed_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
 template <int MODE>
 __device__ __forceinline__ void* advance(void* o, int n) {
     if constexpr (MODE == kF64) return static_cast<double*>(o) + n;
+    else if constexpr (MODE == kWide) return static_cast<unsigned long long*>(o) + n;
     else if constexpr (MODE == kU32 || MODE == kF32 || MODE == kRaw) return static_cast<uint32_t*>(o) + n;
     else return o;
 }
@@ -299,6 +302,12 @@ __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul&
                 else __stcs(reinterpret_cast<float*>(u) + 32 * j, u32_to_f32(ov[j]));
             }
         }
+    } else if constexpr (MODE == kWide) {
+        unsigned long long* u = static_cast<unsigned long long*>(o);
+        const uint32_t ov[4] = {o0, o1, o2, o3};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (!TAIL || lane + 32u * j < limit) __stcs(u + 32 * j, static_cast<unsigned long long>(ov[j]));
     } else if constexpr (MODE == kF64 && (VAR & 16) != 0) {
         // Pairs through shared memory: the 64 outputs of two steps are staged
         // in order, then lane l reads words (2l, 2l+1) with one LDS.64 --
@@ -378,11 +387,12 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
     // Output cursor: single-word modes index words, pair modes index pairs.
     const uint64_t per_stream_vals = kPairs ? (words >> 1) : words;
     void* o = out;
-    if constexpr (MODE == kU32 || MODE == kF32 || MODE == kF64 || MODE == kRaw) {
+    if constexpr (MODE == kU32 || MODE == kF32 || MODE == kF64 || MODE == kRaw || MODE == kWide) {
         constexpr bool kShuffledPairs = kPairs && (VAR & 16) == 0;
         const uint64_t first = static_cast<uint64_t>(gl) * per_stream_vals +
                                (kShuffledPairs ? ((lane >> 1) + ((lane & 1u) << 4)) : lane);
         if constexpr (MODE == kF64) o = static_cast<double*>(out) + first;
+        else if constexpr (MODE == kWide) o = static_cast<unsigned long long*>(out) + first;
         else o = static_cast<uint32_t*>(out) + first;
     }
     constexpr int kValsPerBody = kPairs ? 64 : 128;

@@ -6,10 +6,11 @@
 //   0 success, 64 unknown generator, 65 lanes or blocks out of range,
 //   66 I/O error, 67 invalid arguments   (proj/tools/xgen.cpp:4-8,26-32)
 //
-// Generators: xorgensgp32 (Weyl output) and xorgens-raw (linear part only),
-// as registered in proj/src/registry.cpp:27-30.  The statistical battery
-// (`test`) and the CPU baselines are out of scope for the GPU backend
-// (DESIGN.md section 6): `test` and other ids exit 64/67 with a message.
+// Generators: every xorgens id of the reference registry
+// (proj/src/registry.cpp:27-42): xorgensgp32, xorgens-raw (linear part only),
+// tiny:r2w8, tiny:r2w16, tiny:r4w16 and their tiny-raw: forms.  The
+// statistical battery (`test`) and the CPU baselines (xorwow, mt19937) are not
+// part of the GPU backend: they exit 67 / 64.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -36,11 +37,28 @@ constexpr int exit_bad_args = 67;
 struct Gen {
     std::string id;
     bool weyl;
+    xg_params_t p;
+    const char* note;
 };
 
 bool find_generator(const std::string& id, Gen* g) {
-    if (id == "xorgensgp32") { *g = {id, true}; return true; }
-    if (id == "xorgens-raw") { *g = {id, false}; return true; }
+    struct Row { const char* id; bool weyl; xg_params_t (*params)(); const char* note; };
+    static const Row rows[] = {  // proj/src/registry.cpp:27-42
+        {"xorgensgp32", true, xg_params_xorgensgp32, "nominal; primitivity not re-verified"},
+        {"xorgens-raw", false, xg_params_xorgensgp32, "linear part only (Weyl ablated); nominal"},
+        {"tiny:r2w8", true, xg_params_tiny_r2w8,
+         "exact: (2^16-1)*2^8 = 16776960, verified by exhaustive iteration"},
+        {"tiny:r2w16", true, xg_params_tiny_r2w16, "linear period 2^32-1 verified by matrix-order search"},
+        {"tiny:r4w16", true, xg_params_tiny_r4w16, "linear period 2^64-1 verified by matrix-order search"},
+        {"tiny-raw:r2w8", false, xg_params_tiny_r2w8, "exact: 2^16-1 = 65535, verified by exhaustive iteration"},
+        {"tiny-raw:r2w16", false, xg_params_tiny_r2w16, "exact: 2^32-1, verified by matrix-order search"},
+        {"tiny-raw:r4w16", false, xg_params_tiny_r4w16, "exact: 2^64-1, verified by matrix-order search"},
+    };
+    for (const Row& r : rows)
+        if (id == r.id) {
+            *g = {id, r.weyl, r.params(), r.note};
+            return true;
+        }
     return false;
 }
 
@@ -106,20 +124,25 @@ int parse(int argc, char** argv, Args* a) {
     return exit_ok;
 }
 
-// proj/tools/xgen.cpp:51-66
-void emit(std::ostream& out, const uint32_t* w, size_t n, const std::string& format) {
-    if (format == "raw-le") {
-        // a little-endian uint32 buffer IS the raw-le byte stream
-        out.write(reinterpret_cast<const char*>(w), static_cast<std::streamsize>(n * 4));
-        return;
-    }
+// proj/tools/xgen.cpp:51-66: raw-le = w/8 little-endian bytes per word, hex
+// = w/4 digits, u32-lines = decimal.
+void emit(std::ostream& out, const uint64_t* w, size_t n, unsigned bits, const std::string& format) {
     std::string buf;
-    buf.reserve(n * 11);
-    char tmp[24];
-    for (size_t i = 0; i < n; ++i) {
-        int len = format == "hex" ? std::snprintf(tmp, sizeof tmp, "%08x\n", w[i])
-                                  : std::snprintf(tmp, sizeof tmp, "%u\n", w[i]);
-        buf.append(tmp, static_cast<size_t>(len));
+    if (format == "raw-le") {
+        buf.resize(n * (bits / 8));
+        char* d = buf.data();
+        for (size_t i = 0; i < n; ++i)
+            for (unsigned b = 0; b < bits / 8; ++b) *d++ = static_cast<char>((w[i] >> (8 * b)) & 0xff);
+    } else {
+        buf.reserve(n * 21);
+        char tmp[32];
+        for (size_t i = 0; i < n; ++i) {
+            int len = format == "hex"
+                          ? std::snprintf(tmp, sizeof tmp, "%0*llx\n", static_cast<int>(bits / 4),
+                                          static_cast<unsigned long long>(w[i]))
+                          : std::snprintf(tmp, sizeof tmp, "%llu\n", static_cast<unsigned long long>(w[i]));
+            buf.append(tmp, static_cast<size_t>(len));
+        }
     }
     out.write(buf.data(), static_cast<std::streamsize>(buf.size()));
 }
@@ -129,15 +152,23 @@ int fail(const char* msg, int code) {
     return code;
 }
 
-// Fills `per` words for `n` streams starting at global stream `first` into
-// host memory (block-major), continuing the handle's streams.
-int fill_host(xg_ensemble_t h, bool weyl, uint64_t per, uint32_t n, uint32_t* dev,
-              uint32_t* host) {
-    int rc = weyl ? xg_fill_u32(h, per, dev, nullptr) : xg_fill_raw_u32(h, per, dev, nullptr);
+// Fills `per` words for the handle's `n` streams into host memory as uint64
+// (block-major), continuing the streams.  The raw (Weyl-ablated) generators
+// are 32-bit-or-narrower, so their u32 words are widened here.
+int fill_host(xg_ensemble_t h, bool weyl, uint64_t per, uint32_t n, uint64_t* dev,
+              uint64_t* host) {
+    const size_t cnt = static_cast<size_t>(n) * per;
+    if (weyl) {
+        int rc = xg_fill_words(h, per, dev, nullptr);
+        if (rc) return rc;
+        return cudaMemcpy(host, dev, cnt * 8, cudaMemcpyDeviceToHost) == cudaSuccess ? XG_OK : XG_ECUDA;
+    }
+    uint32_t* d32 = reinterpret_cast<uint32_t*>(dev);
+    int rc = xg_fill_raw_u32(h, per, d32, nullptr);
     if (rc) return rc;
-    if (cudaMemcpy(host, dev, static_cast<size_t>(n) * per * 4, cudaMemcpyDeviceToHost) !=
-        cudaSuccess)
-        return XG_ECUDA;
+    uint32_t* h32 = reinterpret_cast<uint32_t*>(host) + cnt;  // upper half of the buffer
+    if (cudaMemcpy(h32, d32, cnt * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return XG_ECUDA;
+    for (size_t i = 0; i < cnt; ++i) host[i] = h32[i];
     return XG_OK;
 }
 
@@ -146,7 +177,7 @@ int cmd_gen(const Args& a) {
     if (!find_generator(a.generator, &g))
         return fail(("unknown generator: " + a.generator).c_str(), exit_unknown_generator);
     if (!a.have_count) return fail("--count is required", exit_bad_args);
-    const xg_params_t p = xg_params_xorgensgp32();
+    const xg_params_t p = g.p;
     const unsigned blocks = std::max(1u, a.blocks);
     const unsigned lanes = std::max(1u, a.lanes);
     if (a.blocks > 1 || a.lanes > 1) {
@@ -168,14 +199,14 @@ int cmd_gen(const Args& a) {
     // Block-major output: blocks are produced in groups whose whole per-block
     // output fits a 256 MiB staging buffer; a single block longer than that is
     // produced in continuation chunks.
-    constexpr uint64_t kStageWords = 1ull << 26;
+    constexpr uint64_t kStageWords = 1ull << 25;
     const uint64_t chunk = std::min<uint64_t>(per_block, kStageWords);
     const uint32_t group = static_cast<uint32_t>(
         std::max<uint64_t>(1, std::min<uint64_t>(blocks, kStageWords / chunk)));
-    uint32_t* dev = nullptr;
-    if (cudaMalloc(&dev, static_cast<size_t>(group) * chunk * 4) != cudaSuccess)
+    uint64_t* dev = nullptr;
+    if (cudaMalloc(&dev, static_cast<size_t>(group) * chunk * 8) != cudaSuccess)
         return fail("device allocation failed", exit_io);
-    std::vector<uint32_t> host(static_cast<size_t>(group) * chunk);
+    std::vector<uint64_t> host(static_cast<size_t>(group) * chunk);
     int rc = exit_ok;
     for (uint32_t b0 = 0; b0 < blocks && rc == exit_ok; b0 += group) {
         const uint32_t n = std::min(group, blocks - b0);
@@ -186,13 +217,13 @@ int cmd_gen(const Args& a) {
         if (chunk == per_block) {
             e = fill_host(h, g.weyl, per_block, n, dev, host.data());
             if (e) rc = fail(xg_strerror(e), exit_io);
-            else emit(*out, host.data(), static_cast<size_t>(n) * per_block, a.format);
+            else emit(*out, host.data(), static_cast<size_t>(n) * per_block, p.w, a.format);
         } else {  // n == 1
             for (uint64_t done = 0; done < per_block && rc == exit_ok; done += chunk) {
                 const uint64_t m = std::min(chunk, per_block - done);
                 e = fill_host(h, g.weyl, m, 1, dev, host.data());
                 if (e) rc = fail(xg_strerror(e), exit_io);
-                else emit(*out, host.data(), m, a.format);
+                else emit(*out, host.data(), m, p.w, a.format);
             }
         }
         xg_ensemble_destroy(h);
@@ -209,7 +240,8 @@ int cmd_bench(const Args& a) {
     Gen g;
     if (!find_generator(a.generator, &g))
         return fail(("unknown generator: " + a.generator).c_str(), exit_unknown_generator);
-    const xg_params_t p = xg_params_xorgensgp32();
+    const xg_params_t p = g.p;
+    if (p.w != 32) return fail("bench measures the 32-bit generators", exit_bad_args);
     const uint64_t count = a.have_count ? a.count : 100000000ull;
     if (count < 1000000) return fail("throughput trials need count >= 1e6", exit_bad_args);
     if (a.trials < 3) return fail("throughput needs >= 3 trials", exit_bad_args);
@@ -272,7 +304,7 @@ int cmd_params(const Args& a) {
     Gen g;
     if (!find_generator(id, &g))
         return fail(("unknown generator: " + id).c_str(), exit_unknown_generator);
-    const xg_params_t p = xg_params_xorgensgp32();
+    const xg_params_t p = g.p;
     std::cout << "generator:    " << id << "\n"
               << "r,s:          " << p.r << "," << p.s << "\n"
               << "a,b,c,d:      " << p.a << "," << p.b << "," << p.c << "," << p.d << "\n"
@@ -286,10 +318,7 @@ int cmd_params(const Args& a) {
               << (g.weyl ? "~2^" + std::to_string(p.r * p.w + p.w)
                          : "2^" + std::to_string(p.r * p.w) + "-1")
               << "\n"
-              << "period note:  "
-              << (g.weyl ? "nominal; primitivity not re-verified"
-                         : "linear part only (Weyl ablated); nominal")
-              << "\n"
+              << "period note:  " << g.note << "\n"
               << "backend:      " << xg_build_info() << "\n";
     return exit_ok;
 }

@@ -40,7 +40,7 @@ __all__ = [
     "UnsupportedParamsError", "check_params", "validate_params", "lane_bound",
     "recommended_weyl_increment", "default_output_shift", "period_description",
     "PeriodDescription", "xorgensgp32_params", "tiny_r2w8_params", "tiny_r2w16_params",
-    "tiny_r4w16_params", "gpu_supported", "XorgensState", "seed_state", "batch_step",
+    "tiny_r4w16_params", "gpu_supported", "fast_path", "XorgensState", "seed_state", "batch_step",
     "BlockEnsemble", "XorgensSource", "partition", "kernel_launches",
 ]
 
@@ -183,7 +183,14 @@ def tiny_r4w16_params() -> GeneratorParams:
 
 
 def gpu_supported(p: GeneratorParams) -> bool:
+    """True when the GPU can generate `p` (every valid set with r <= 16384)."""
     return lib.xg_gpu_supported(ctypes.byref(p._c())) == 0
+
+
+def fast_path(p: GeneratorParams) -> bool:
+    """True when `p` runs on the register-window kernels (w=32, r=128,
+    lane_bound >= 32); other valid sets run on the general-parameter kernels."""
+    return bool(lib.xg_fast_path(ctypes.byref(p._c())))
 
 
 def partition(total_streams: int, world: int, rank: int) -> Tuple[int, int]:
@@ -317,13 +324,16 @@ class BlockEnsemble:
     # -- generation ----------------------------------------------------------
     def generate(self, per_block: int, workers: int = 0) -> np.ndarray:
         """BlockEnsemble::generate (proj/src/parallel.cpp:97-135) into host
-        memory: a (num_blocks, per_block) uint32 array, block-major, continuing
-        each block's stream.  ``workers`` is accepted for API parity only."""
+        memory: a (num_blocks, per_block) array, block-major, continuing each
+        block's stream -- uint32 for w <= 32, uint64 for w = 64.  ``workers``
+        is accepted for API parity only."""
         del workers
-        out = np.empty((self._n, per_block), dtype=np.uint32)
+        wide = self._params.w > 32
+        out = np.empty((self._n, per_block), dtype=np.uint64 if wide else np.uint32)
         if per_block:
-            _raise(lib.xg_generate_host(self._h.ptr, per_block, out.ctypes.data_as(ctypes.c_void_p),
-                                        self._stream()), "generate")
+            fn = lib.xg_generate_host_words if wide else lib.xg_generate_host
+            _raise(fn(self._h.ptr, per_block, out.ctypes.data_as(ctypes.c_void_p), self._stream()),
+                   "generate")
         return out
 
     def generate_into_host(self, per_block: int, host_out, stream=None) -> None:
@@ -347,6 +357,10 @@ class BlockEnsemble:
     def fill_u32(self, per_block: int, out=None, stream=None):
         """Device fill, out[g, k] = word k of block g (continuing)."""
         return self._fill(lib.xg_fill_u32, per_block, out, _torch().uint32, per_block, stream)
+
+    def fill_words(self, per_block: int, out=None, stream=None):
+        """Every word as uint64 (the reference generate() element type); any w."""
+        return self._fill(lib.xg_fill_words, per_block, out, _torch().uint64, per_block, stream)
 
     def fill_raw_u32(self, per_block: int, out=None, stream=None):
         """Weyl-ablated linear stream (RawXorgens::next, registry "xorgens-raw")."""
@@ -467,8 +481,8 @@ class XorgensState:
         return self._params.r + 1
 
     def next_word(self) -> int:
-        v = ctypes.c_uint32()
-        _raise(lib.xg_next_u32(self._ens.handle, ctypes.byref(v)), "next_u32")
+        v = ctypes.c_uint64()
+        _raise(lib.xg_next_word(self._ens.handle, ctypes.byref(v)), "next_word")
         return v.value
 
     def next_u64(self) -> int:

@@ -56,8 +56,12 @@ def test_params_and_sets():
         xg.recommended_weyl_increment(12)
     assert ei.value.code() == xg.ParamError.bad_word_size
     assert xg.period_description(p).display == "~2^4128"
-    assert xg.gpu_supported(p)
-    assert not xg.gpu_supported(xg.tiny_r2w8_params())
+    assert xg.gpu_supported(p) and xg.fast_path(p)
+    # every valid set is generated on the GPU; only w=32/r=128/lane_bound>=32
+    # sets take the register-window kernels
+    assert xg.gpu_supported(xg.tiny_r2w8_params()) and not xg.fast_path(xg.tiny_r2w8_params())
+    big = xg.GeneratorParams(16385, 2, 1, 1, 1, 1, 32, 2654435769, 16)
+    assert xg.check_params(big) is None and not xg.gpu_supported(big)
 
 
 def _mk(r, s, a, b, c, d, w, omega=None, gamma=None):
@@ -108,11 +112,11 @@ def test_create_validation_order_without_gpu():
     assert lib.xg_ensemble_create(ctypes.byref(gp), 0, 0, 0, 1, 0, None, ctypes.byref(h)) == _lib.XG_ERANGE
     assert lib.xg_ensemble_create(ctypes.byref(gp), 0, 0, 1, 64, 0, None, ctypes.byref(h)) == _lib.XG_ERANGE
     assert lib.xg_ensemble_create(ctypes.byref(gp), 0, 0, 1, 0, 0, None, ctypes.byref(h)) == _lib.XG_ERANGE
-    tiny = lib.xg_params_tiny_r2w8()
-    assert lib.xg_ensemble_create(ctypes.byref(tiny), 0, 0, 1, 1, 0, None, ctypes.byref(h)) == _lib.XG_EUNSUPPORTED
     w64 = P(64, 53, 33, 26, 27, 29, 64, 11400714819323198485, 32)  # PAPER.md:448-449, lane_bound 11
     assert lib.xg_params_check(ctypes.byref(w64)) == 0
-    assert lib.xg_ensemble_create(ctypes.byref(w64), 0, 0, 1, 11, 0, None, ctypes.byref(h)) == _lib.XG_EUNSUPPORTED
+    assert lib.xg_ensemble_create(ctypes.byref(w64), 0, 0, 1, 12, 0, None, ctypes.byref(h)) == _lib.XG_ERANGE
+    big = P(16385, 2, 1, 1, 1, 1, 32, 2654435769, 16)
+    assert lib.xg_ensemble_create(ctypes.byref(big), 0, 0, 1, 1, 0, None, ctypes.byref(h)) == _lib.XG_EUNSUPPORTED
     assert h.value is None
     assert lib.xg_ensemble_create(ctypes.byref(gp), 0, 0, 1, 1, 0, None, None) == _lib.XG_EINVAL
     assert lib.xg_ensemble_destroy(None) == _lib.XG_EINVAL

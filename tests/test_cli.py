@@ -102,7 +102,7 @@ def test_gen_raw_le_matches_oracle(oracle, golden, tmp_path):
 
 @gpu
 def test_gen_long_single_block_chunks(oracle, tmp_path):
-    # longer than the 2^26-word staging buffer: produced in continuation chunks
+    # longer than the 2^25-word staging buffer: produced in continuation chunks
     n = (1 << 26) + 777
     path = tmp_path / "long.bin"
     rc, _ = run("gen", "--seed", "9", "--count", str(n), "--format", "raw-le", "-o", str(path),
@@ -119,3 +119,28 @@ def test_bench_reports():
     assert rc == 0 and b"RN/s" in out
     rc, out = run("bench", "--count", "16777216", "--blocks", "4096", "--trials", "3", "--json")
     assert rc == 0 and b'"mean"' in out
+
+
+@gpu
+@pytest.mark.parametrize("gid,ps,weyl", [
+    ("tiny:r2w8", (2, 1, 1, 1, 5, 7, 8, 159, 4), True),
+    ("tiny:r4w16", (4, 3, 1, 2, 5, 8, 16, 40503, 8), True),
+    ("tiny-raw:r2w16", (2, 1, 1, 1, 6, 11, 16, 40503, 8), False),
+])
+def test_gen_tiny_generators(oracle, gid, ps, weyl, tmp_path):
+    """Every xorgens registry id (proj/src/registry.cpp:27-42): w/4 hex digits,
+    w/8 raw-le bytes per word, on the general-parameter kernels."""
+    from oracle import Params
+
+    o = oracle.ensemble(11, 1, Params(*ps))
+    want = o.fill_words(500)[0] if weyl else o.fill_raw_u32(500)[0].astype(np.uint64)
+    rc, out = run("gen", "-g", gid, "--seed", "11", "--count", "500", "--format", "hex")
+    assert rc == 0
+    lines = out.decode().split()
+    assert all(len(x) == ps[6] // 4 for x in lines)
+    assert [int(x, 16) for x in lines] == want.tolist()
+    path = tmp_path / "t.bin"
+    rc, _ = run("gen", "-g", gid, "--seed", "11", "--count", "500", "--format", "raw-le", "-o", str(path))
+    assert rc == 0
+    dt = {8: "<u1", 16: "<u2"}[ps[6]]
+    assert np.array_equal(np.fromfile(path, dtype=dt).astype(np.uint64), want)

@@ -232,8 +232,8 @@ def test_empty_and_errors():
         xg.BlockEnsemble(GP32, 0, 0, 1)
     with pytest.raises(xg.OutOfRangeError):
         xg.BlockEnsemble(GP32, 0, 1, 64)
-    with pytest.raises(xg.UnsupportedParamsError):
-        xg.BlockEnsemble(xg.tiny_r4w16_params(), 0, 1, 1)
+    with pytest.raises(xg.UnsupportedParamsError):  # conventions defined on w = 32 words
+        xg.BlockEnsemble(xg.tiny_r4w16_params(), 0, 1, 1).fill_f32(10)
     with pytest.raises(ValueError):
         e.fill_u32(10, out=torch.empty(3, dtype=torch.uint32, device="cuda"))
     with pytest.raises(xg.OutOfRangeError):
@@ -477,3 +477,46 @@ def test_generate_host_streams_longer_than_a_slot(oracle):
         assert int(np.bitwise_xor.reduce(host[g])) == int(x[0])
         assert int(np.sum(w * np.arange(1, per + 1, dtype=np.uint64), dtype=np.uint64)) == int(s[0])
     assert np.array_equal(e.generate(64), oracle.ensemble(77, P).fill_u32(per + 64)[:, per:])
+
+
+
+# ---- general-parameter kernels (every set the reference accepts) ------------
+
+GENERIC_SETS = [
+    ("tiny_r2w8", (2, 1, 1, 1, 5, 7, 8, 159, 4)),
+    ("tiny_r2w16", (2, 1, 1, 1, 6, 11, 16, 40503, 8)),
+    ("tiny_r4w16", (4, 3, 1, 2, 5, 8, 16, 40503, 8)),
+    ("w64_paper", (64, 53, 33, 26, 27, 29, 64, 11400714819323198485, 32)),
+    ("r128_lb3", (128, 125, 15, 14, 12, 17, 32, 2654435769, 16)),           # lane_bound 3
+    ("r64_w32", (64, 37, 13, 7, 11, 19, 32, 2654435769, 16)),               # lane_bound 27
+    ("r1024", (1024, 511, 9, 23, 5, 27, 32, 2654435769, 16)),               # 8 KiB state per stream
+]
+
+
+@pytest.mark.parametrize("name,ps", GENERIC_SETS, ids=[n for n, _ in GENERIC_SETS])
+def test_generic_params_vs_oracle_and_reference(oracle, reference, name, ps):
+    p = xg.GeneratorParams(*ps)
+    op = Params(*ps)
+    assert xg.gpu_supported(p) and not xg.fast_path(p)
+    lanes = xg.lane_bound(p)
+    e = xg.BlockEnsemble(p, 2**64 - 2, 5, lanes)          # seeds wrap through 0
+    o = oracle.ensemble(2**64 - 2, 5, op)
+    for n in (1, 33, 700):
+        assert np.array_equal(np_u32(e.fill_words(n)), o.fill_words(n)), n
+    if p.w <= 32:
+        assert np.array_equal(np_u32(e.fill_u32(100)), o.fill_words(100).astype(np.uint32))
+        assert np.array_equal(np_u32(e.fill_raw_u32(50)), o.fill_raw_u32(50))
+        assert np.array_equal(e.generate(77), o.fill_words(77).astype(np.uint32))
+    else:
+        assert np.array_equal(e.generate(77), o.fill_words(77))
+    for i in (0, 4):
+        b, w = e.block_state(i)
+        assert np.array_equal(np.array(b, dtype=np.uint64), o.logical_buffer(i)) and w == o.weyl(i)
+    # the reference sources themselves: one stream, and next_word served from refills
+    st = xg.XorgensState(p, 123)
+    ref = reference.stream(123, 3000, op)
+    got = [st.next_word() for _ in range(1000)]
+    got += np_u32(st.ensemble.fill_words(2000))[0].tolist()
+    assert np.array_equal(np.array(got, dtype=np.uint64), ref)
+    with pytest.raises(xg.UnsupportedParamsError):
+        e.mc_pi(32)
