@@ -79,7 +79,7 @@ public:
     BlockEnsemble(const Params& params, std::uint64_t base_seed, unsigned num_blocks,
                   unsigned lanes, std::uint64_t first_stream = 0, int device = 0,
                   xg_stream_t stream = nullptr)
-        : base_seed_(base_seed), lanes_(lanes), r_(params.r) {
+        : base_seed_(base_seed), lanes_(lanes), r_(params.r), w_(params.w) {
         const xg_params_t c = to_c(params);
         check(xg_ensemble_create(&c, base_seed, first_stream, num_blocks, lanes, device, stream,
                                  &h_));
@@ -94,6 +94,7 @@ public:
         base_seed_ = o.base_seed_;
         lanes_ = o.lanes_;
         r_ = o.r_;
+        w_ = o.w_;
         return *this;
     }
     ~BlockEnsemble() {
@@ -132,6 +133,7 @@ public:
 
     unsigned num_blocks() const noexcept { return n_; }
     unsigned lanes() const noexcept { return lanes_; }
+    unsigned word_bits() const noexcept { return w_; }
     std::uint64_t base_seed() const noexcept { return base_seed_; }
 
     std::pair<std::vector<std::uint64_t>, std::uint64_t> block_state(unsigned i) const {
@@ -164,6 +166,7 @@ protected:
     std::uint64_t base_seed_ = 0;
     unsigned lanes_ = 0;
     unsigned r_ = 0;
+    unsigned w_ = 32;
 };
 
 // One serial stream (proj/include/xg/xorgens.hpp:20-96), served from device refills.
@@ -182,6 +185,7 @@ public:
         check(xg_ensemble_create_from_raw(&c, 1, buffer.data(), &weyl, device, nullptr, &st.h_));
         st.n_ = 1;
         st.r_ = params.r;
+        st.w_ = params.w;
         st.lanes_ = lane_bound(params);
         return st;
     }
@@ -210,6 +214,24 @@ inline std::vector<std::uint64_t> batch_step(XorgensState& st, unsigned lanes) {
     for (auto& v : out) v = st.next_word();
     return out;
 }
+
+// XorgensSource (proj/include/xg/stream.hpp:25-35) over device refills.
+// Templated on the consumer's WordSource base so this header needs no
+// reference header: `xg::gpu::XorgensSource<xg::WordSource> src(params, seed)`
+// plugs into anything that takes an `xg::WordSource&` (the battery, bench).
+template <class WordSourceBase>
+class XorgensSource final : public WordSourceBase {
+public:
+    template <class Params>
+    XorgensSource(const Params& params, std::uint64_t seed, int device = 0)
+        : state_(params, seed, device) {}
+    std::uint64_t next() override { return state_.next_word(); }
+    unsigned word_bits() const override { return state_.word_bits(); }
+    XorgensState& state() noexcept { return state_; }
+
+private:
+    XorgensState state_;
+};
 
 }  // namespace gpu
 }  // namespace xg

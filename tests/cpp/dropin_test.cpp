@@ -12,6 +12,7 @@
 #include "xg/gpu.hpp"
 #include "xg/parallel.hpp"
 #include "xg/params.hpp"
+#include "xg/stream.hpp"
 #include "xg/xorgens.hpp"
 
 static int failures = 0;
@@ -42,6 +43,14 @@ int main() {
     auto rr = xg::XorgensState::from_raw(p, rs.logical_buffer(), rs.weyl_value());
     auto gr = xg::gpu::XorgensState::from_raw(p, rs.logical_buffer(), rs.weyl_value());
     for (int i = 0; i < 3000; ++i) CHECK(rr.next_word() == gr.next_word());
+    // WordSource adapter (stream.hpp:25-35) behind the reference's virtual base.
+    {
+        xg::XorgensSource rsrc(p, 77);
+        xg::gpu::XorgensSource<xg::WordSource> gsrc(p, 77);
+        xg::WordSource& as_base = gsrc;
+        CHECK(as_base.word_bits() == rsrc.word_bits());
+        for (int i = 0; i < 40000; ++i) CHECK(rsrc.next() == as_base.next());
+    }
     // Checkpoint / resume continues every block exactly.
     {
         xg::gpu::BlockEnsemble a(p, 11, 4, 63);
@@ -55,6 +64,24 @@ int main() {
         xg::BlockEnsemble ref(p, 11, 4, 63);
         ref.generate(1000);
         CHECK(ref.generate(500) == next_a);
+    }
+    // Non-production parameter sets (general-parameter kernels): the tiny
+    // verification sets of params.hpp:89-91 and the w = 64 set.
+    {
+        xg::GeneratorParams w64 = p;
+        w64.r = 64; w64.s = 53; w64.a = 33; w64.b = 26; w64.c = 27; w64.d = 29; w64.w = 64;
+        w64.gamma = 32; w64.omega = 0x9E3779B97F4A7C15ull;
+        const xg::GeneratorParams sets[] = {xg::tiny_r2w8_params(), xg::tiny_r2w16_params(),
+                                            xg::tiny_r4w16_params(), w64};
+        for (const auto& q : sets) {
+            const unsigned lanes = xg::lane_bound(q) < 4 ? xg::lane_bound(q) : 4;
+            xg::BlockEnsemble ref(q, 3, 3, lanes);
+            xg::gpu::BlockEnsemble gpu(q, 3, 3, lanes);
+            for (int call = 0; call < 2; ++call) CHECK(ref.generate(333) == gpu.generate(333));
+            xg::XorgensState rq(q, 9);
+            xg::gpu::XorgensState gq(q, 9);
+            for (int i = 0; i < 2000; ++i) CHECK(rq.next_word() == gq.next_word());
+        }
     }
     // Same exception classes.
     bool threw = false;
