@@ -219,6 +219,13 @@ int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t wor
         case 0: return launch_fill_v<MODE, 0>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         case 1: return launch_fill_v<MODE, 1>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         case 144: return launch_fill_v<MODE, 144>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        case 48:
+            // bulk-copy stores: 512-byte bodies need 16-byte aligned rows
+            if constexpr (MODE == kU32 || MODE == kF32 || MODE == kRaw) {
+                if ((reinterpret_cast<uintptr_t>(out) & 15u) == 0 && (words & 3u) == 0)
+                    return launch_fill_v<MODE, 48>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+            }
+            return launch_fill_v<MODE, 16>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         default: return launch_fill_v<MODE, 16>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         }
     case kRtJ1:

@@ -26,6 +26,9 @@
 //              badly with LOP3);
 //   bit 4      s-tap through a shared-memory ring instead of SEL + SHFL (the
 //              default: one ALU op less per word);
+//   bit 5      u32/f32/raw outputs staged in shared memory and written by the
+//              bulk-copy engine (cp.async.bulk, 1 KB per two bodies) instead
+//              of one STG per step;
 //   bit 7      left shifts forced onto the ALU pipe as SHF.L (slower: ptxas's
 //              IMAD.SHL keeps the ALU pipe free).
 //
@@ -111,7 +114,7 @@ struct Lane {
     // A_T + delta + l with the compile-time A_T = 32(T-4+J) mod 256.
     uint32_t* ring_w;  // ring + lane (stores)
     uint32_t* ring_r;  // ring + delta + lane (s-tap loads)
-    uint32_t* stage;   // f64 with VAR bit 4: 2 x 128-word output staging for word pairs
+    uint32_t* stage;   // f64 with VAR bit 4: 2 x 128-word pair staging; VAR bit 5: 2 x 256-word bulk stage
 };
 
 // One warp step on the register window.  T is the step index mod 8; the
@@ -149,6 +152,25 @@ __device__ __forceinline__ uint32_t warp_step(uint32_t (&R)[4], const P& p, cons
         if constexpr (P::J != 1 || (T & 1) == 1) __syncwarp();
     }
     return v;
+}
+
+// VAR bit 5: bulk-copy (TMA engine) stores.  A body's 128 output values are
+// staged in shared memory with four STS; after every second body the lanes
+// fence the generic->async proxy and lane 0 issues one 1 KB cp.async.bulk to
+// HBM.  Two 1 KB stage buffers per warp alternate; a buffer is rewritten
+// only after the copy that read it has retired (wait_group.read 1).
+__device__ __forceinline__ void bulk_fence() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(ssrc));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+                 "cp.async.bulk.commit_group;"
+                 :: "l"(gdst), "r"(s), "r"(bytes) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory");
 }
 
 // Output stage (xorgens.hpp:58-62): ((w ^ (w >> gamma)) + x) mod 2^32.
@@ -276,7 +298,7 @@ __device__ __forceinline__ void* advance(void* o, int n) {
 // shared-memory ring, and it selects the f64 stage buffer.  Emits at cursor o
 // (single-word modes: o[0], o[32], o[64], o[96]; pair modes: o[0], o[32]);
 // the tail variant masks by `limit` (values of this body still wanted).
-template <int MODE, int VAR, bool TAIL, int PH, class P>
+template <int MODE, int VAR, bool TAIL, int PH, int BB = 0, class P>
 __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul& m, const Lane& ln,
                                       uint32_t& wl, uint32_t w_step, void* o, uint32_t& hits,
                                       unsigned limit) {
@@ -292,7 +314,27 @@ __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul&
     const uint32_t o3 = kW ? weyl_out<VAR>(wl + 3u * w_step, v3, p, m) : v3;
     wl += 4u * w_step;
     const unsigned lane = threadIdx.x & 31u;
-    if constexpr (MODE == kU32 || MODE == kF32 || MODE == kRaw) {
+    if constexpr ((MODE == kU32 || MODE == kF32 || MODE == kRaw) && (VAR & 32) != 0 && !TAIL) {
+        // Bodies go in pairs (PH 0, 1) into stage buffer BB (256 words); the
+        // PH 1 body issues one 1 KB copy for both.  o is this lane's slot, so
+        // lane 0's o is the body's first value.
+        uint32_t* st = ln.stage + 256 * BB + 128 * PH;
+        if constexpr (PH == 0) {
+            if (lane == 0) bulk_wait_read<1>();  // the copy out of buffer BB (two pairs ago) has read it
+            __syncwarp();
+        }
+        const uint32_t ov[4] = {o0, o1, o2, o3};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if constexpr (MODE == kF32) reinterpret_cast<float*>(st)[32 * j + lane] = u32_to_f32(ov[j]);
+            else st[32 * j + lane] = ov[j];
+        }
+        if constexpr (PH == 1) {
+            bulk_fence();
+            __syncwarp();
+            if (lane == 0) bulk_store(static_cast<uint32_t*>(o) - 128, ln.stage + 256 * BB, 1024);
+        }
+    } else if constexpr (MODE == kU32 || MODE == kF32 || MODE == kRaw) {
         uint32_t* u = static_cast<uint32_t*>(o);
         const uint32_t ov[4] = {o0, o1, o2, o3};
 #pragma unroll
@@ -383,6 +425,11 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
             ln.stage = stage[threadIdx.x >> 5];
         }
     }
+    constexpr bool kBulk = (VAR & 32) != 0 && (MODE == kU32 || MODE == kF32 || MODE == kRaw);
+    if constexpr (kBulk) {
+        __shared__ __align__(128) uint32_t bstage[kWarpsPerBlock][512];
+        ln.stage = bstage[threadIdx.x >> 5];
+    }
 
     // Output cursor: single-word modes index words, pair modes index pairs.
     const uint64_t per_stream_vals = kPairs ? (words >> 1) : words;
@@ -407,8 +454,8 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
         for (; i + 4 <= n; i += 4) {
             body4<MODE, VAR, false, 0>(R, p, m, ln, wl, w_step, o, hits, 0);
             body4<MODE, VAR, false, 1>(R, p, m, ln, wl, w_step, advance<MODE>(o, kValsPerBody), hits, 0);
-            body4<MODE, VAR, false, 0>(R, p, m, ln, wl, w_step, advance<MODE>(o, 2 * kValsPerBody), hits, 0);
-            body4<MODE, VAR, false, 1>(R, p, m, ln, wl, w_step, advance<MODE>(o, 3 * kValsPerBody), hits, 0);
+            body4<MODE, VAR, false, 0, 1>(R, p, m, ln, wl, w_step, advance<MODE>(o, 2 * kValsPerBody), hits, 0);
+            body4<MODE, VAR, false, 1, 1>(R, p, m, ln, wl, w_step, advance<MODE>(o, 3 * kValsPerBody), hits, 0);
             o = advance<MODE>(o, 4 * kValsPerBody);
         }
         // 0-3 remaining bodies keep the parity sequence 0, 1, 0 (a chunk of
@@ -423,8 +470,16 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
             o = advance<MODE>(o, kValsPerBody);
         }
         if (rem >= 3) {
-            body4<MODE, VAR, false, 0>(R, p, m, ln, wl, w_step, o, hits, 0);
+            body4<MODE, VAR, false, 0, 1>(R, p, m, ln, wl, w_step, o, hits, 0);
             o = advance<MODE>(o, kValsPerBody);
+        }
+        if constexpr (kBulk) {
+            if (rem & 1u) {  // a lone PH 0 body: copy its half-buffer out now
+                bulk_fence();
+                __syncwarp();
+                if (lane == 0)
+                    bulk_store(static_cast<uint32_t*>(o) - 128, ln.stage + (rem == 3 ? 256 : 0), 512);
+            }
         }
     }
 
@@ -450,6 +505,9 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
         for (int j = 0; j < 4; ++j) w[32 * j + lane] = R[j];
     }
     if (MODE != kRaw && lane == 0) weyl[g] = weyl0 + static_cast<uint32_t>(words) * p.omega;
+    if constexpr (kBulk) {
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
 
     if constexpr (MODE == kMC) {
         unsigned long long t = hits;

@@ -19,7 +19,7 @@ for var_params in (p, xg.GeneratorParams(128, 95, 17, 12, 13, 15, 32, 2654435769
     oe = o.ensemble(3, 13, o.params(var_params.r, var_params.s, var_params.a, var_params.b,
                                     var_params.c, var_params.d, var_params.w, var_params.omega,
                                     var_params.gamma))
-    for n in (1, 130, 515):
+    for n in (1, 128, 130, 384, 515, 516, 1280):
         assert np.array_equal(e.fill_u32(n).cpu().numpy(), oe.fill_u32(n))
         assert np.array_equal(e.fill_f32(n).cpu().numpy().view(np.uint32), oe.fill_f32(n).view(np.uint32))
         assert np.array_equal(e.fill_f64(n).cpu().numpy().view(np.uint64), oe.fill_f64(n).view(np.uint64))

@@ -70,7 +70,7 @@ def test_golden_alt_params_runtime_kernels(golden, idx):
 
 
 @pytest.mark.parametrize("streams", [1, 7, 8, 9, 257])
-@pytest.mark.parametrize("per", [1, 17, 31, 32, 33, 127, 128, 129, 1000, 4101])
+@pytest.mark.parametrize("per", [1, 17, 31, 32, 33, 127, 128, 129, 256, 640, 1000, 2048, 4101])
 def test_fill_u32_vs_oracle(oracle, streams, per):
     base = 0x1234_5678_9ABC + streams * 1000 + per
     e = xg.BlockEnsemble(GP32, base, streams, 63)
