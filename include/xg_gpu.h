@@ -140,10 +140,10 @@ int xg_fill_f32(xg_ensemble_t h, uint64_t per_stream, float* dev_out, xg_stream_
 /* Uniform [0,1): f64 = (u64 >> 11) * 2^-53 with u64 as in xg_fill_u64. Exact. */
 int xg_fill_f64(xg_ensemble_t h, uint64_t per_stream, double* dev_out, xg_stream_t stream);
 /* Fused in-register Monte Carlo pi.  samples_per_stream must be a multiple
- * of 32 (XG_EINVAL otherwise): each stream supplies 2*samples_per_stream words
- * in blocks of 64, block j giving the 32 samples (w[64j+i], w[64j+32+i]) --
- * the two words one lane holds after two consecutive warp steps, so no word
- * moves between lanes.  Each word read as a signed 32-bit coordinate in
+ * of 32 (XG_EINVAL otherwise): each stream supplies 2*samples_per_stream words,
+ * sample m being the consecutive pair (w[2m], w[2m+1]) -- the pair one lane
+ * of the pair-lane kernel holds after a double step, so no word moves between
+ * lanes.  Each word read as a signed 32-bit coordinate in
  * [-2^31, 2^31); hit iff x^2 + y^2 < 2^62 (exact integer test, the unit disc
  * in the square [-1, 1)^2, P(hit) = pi/4).  The hit count over all streams is ADDED to
  * *dev_hits (a device uint64).  No HBM traffic. */

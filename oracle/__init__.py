@@ -109,10 +109,10 @@ class Oracle:
         return (u >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
 
     def mc_hits(self, words: np.ndarray) -> int:
-        """Hits over a stream prefix of 64k words: block j gives samples
-        (w[64j+i], w[64j+32+i])."""
-        w = words.astype(np.uint32).view(np.int32).astype(np.int64).reshape(-1, 2, 32)
-        x, y = w[:, 0, :], w[:, 1, :]
+        """Hits over a stream prefix of 2k words: sample m is the consecutive
+        pair (w[2m], w[2m+1])."""
+        w = words.astype(np.uint32).view(np.int32).astype(np.int64).reshape(-1, 2)
+        x, y = w[:, 0], w[:, 1]
         q = (x * x).astype(np.uint64) + (y * y).astype(np.uint64)
         return int(np.count_nonzero(q < np.uint64(1 << 62)))
 

@@ -302,13 +302,13 @@ static void run_one(job_t* j, uint32_t g) {
         break;
     }
     case J_MC: {
-        /* blocks of 64 words, sample i of a block is
-         * (w[i], w[32+i]); samples_per_stream is a multiple of 32. */
+        /* sample m is the consecutive word pair
+         * (w[2m], w[2m+1]); samples_per_stream is a multiple of 32. */
         uint64_t hits = 0;
-        uint32_t blk[64];
-        for (uint64_t k = 0; k < j->n / 32; ++k) {
-            for (int i = 0; i < 64; ++i) blk[i] = (uint32_t)xgo_next_word(st);
-            for (int i = 0; i < 32; ++i) hits += (uint64_t)xgo_mc_hit(blk[i], blk[32 + i]);
+        for (uint64_t k = 0; k < j->n; ++k) {
+            uint32_t x = (uint32_t)xgo_next_word(st);
+            uint32_t y = (uint32_t)xgo_next_word(st);
+            hits += (uint64_t)xgo_mc_hit(x, y);
         }
         ((uint64_t*)j->out)[g] = hits;
         break;

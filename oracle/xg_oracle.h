@@ -90,7 +90,7 @@ int xgo_ensemble_fill_f32(xgo_state* states, uint32_t num_streams, uint64_t per_
 int xgo_ensemble_fill_f64(xgo_state* states, uint32_t num_streams, uint64_t per_stream,
                           double* out, int threads);
 /* Monte Carlo pi: per-stream hit counts over samples_per_stream samples
- * (a multiple of 32; block j of 64 words gives samples (w[64j+i], w[64j+32+i])). */
+ * (a multiple of 32; sample m is the consecutive pair (w[2m], w[2m+1])). */
 int xgo_ensemble_mc_pi(xgo_state* states, uint32_t num_streams, uint64_t samples_per_stream,
                        uint64_t* hits_per_stream, int threads);
 /* Per-stream checksums of the next n words (continuing): xor and

@@ -19,6 +19,7 @@
 #include "xg_gpu.h"
 #include "xg_generic.cuh"
 #include "xg_kernels.cuh"
+#include "xg_pairs.cuh"
 
 using namespace xgk;
 
@@ -132,18 +133,38 @@ unsigned grid_for(uint32_t n) {
     return static_cast<unsigned>((static_cast<uint64_t>(n) + kWarpsPerBlock - 1) / kWarpsPerBlock);
 }
 
-// Instruction-placement variant of the GP32 kernels (xg_kernels.cuh, VAR
-// mask): 16 (shared-memory s-tap) for every mode and parameter kind, from the
-// measurements in profiles/README.md; XG_VARIANT = 0, 1 or 144 selects another
-// GP32 variant for experiments.
-constexpr int kDefaultVar[6] = {16, 16, 16, 16, 16, 16};
+// Kernel choice for the register-window sets: 512 (default) = the pair-lane
+// kernel (xg_pairs.cuh) wherever it applies (r - s < 64 and aligned output
+// rows), else the word-per-lane kernel with the shared-memory s-tap (VAR 16,
+// xg_kernels.cuh).  XG_VARIANT = 0, 1, 16, 48 or 144 forces a word-per-lane
+// variant for experiments (measurements in profiles/README.md).
+constexpr int kPairs = 512;
 
-int variant_for(int mode) {
+int variant_for(int) {
     static int forced = [] {
         const char* e = getenv("XG_VARIANT");
         return e ? atoi(e) : -1;
     }();
-    return forced >= 0 ? forced : kDefaultVar[mode];
+    return forced >= 0 ? forced : kPairs;
+}
+
+// The pair-lane kernel stores 8-byte word pairs (16 for the zero-extended
+// u64 words): every output row must start on that boundary.
+template <int MODE>
+bool pair_aligned(const void* out, uint64_t words) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(out);
+    if constexpr (MODE == kU32 || MODE == kF32 || MODE == kRaw) return (a & 7u) == 0 && (words & 1u) == 0;
+    else if constexpr (MODE == kWide) return (a & 15u) == 0 && (words & 1u) == 0;
+    else return true;  // f64 (8-byte values, words even), MC, skip
+}
+
+template <int MODE, class P>
+int launch_pair(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t words,
+                void* out, unsigned long long* hits, cudaStream_t s) {
+    pair_kernel<P, MODE><<<grid_for(g_count), kThreads, 0, s>>>(p, h->d_win, h->d_weyl, g_begin,
+                                                                g_count, words, out, hits);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cuda_rc(cudaGetLastError());
 }
 
 HiMul himul(const xg_params_t& p) {
@@ -213,9 +234,14 @@ int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t wor
         }
         return XG_EUNSUPPORTED;
     }
+    const int var = variant_for(MODE);
+    if (var == kPairs && h->kind != kRtJ2 && pair_aligned<MODE>(out, words)) {
+        if (h->kind == kGP32) return launch_pair<MODE>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        return launch_pair<MODE>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s);
+    }
     switch (h->kind) {
     case kGP32:
-        switch (variant_for(MODE)) {
+        switch (var) {
         case 0: return launch_fill_v<MODE, 0>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         case 1: return launch_fill_v<MODE, 1>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         case 144: return launch_fill_v<MODE, 144>(GP32{}, h, g_begin, g_count, words, out, hits, s);

@@ -206,22 +206,28 @@ __device__ __forceinline__ double pair_to_f64(uint32_t lo_shr11, uint32_t hi) {
 // lanes pair 16 + l/2 of B, exchanging one word with the xor-1 partner.
 // Even lane: (lo, hi) = (a_l, a_{l+1}); odd lane: (b_{l-1}, b_l).  The
 // selects are exact funnel shifts by 0 or 32 (one SHF.R.U64 each).
-__device__ __forceinline__ void pair_f64(uint32_t a, uint32_t b, const Lane& ln, uint32_t& lo11,
-                                         uint32_t& hi) {
+__device__ __forceinline__ void pair_words(uint32_t a, uint32_t b, const Lane& ln, uint32_t& lo,
+                                           uint32_t& hi) {
     const uint32_t give = funnel_r(b, a, ln.sh_own);   // odd: a, even: b
     const uint32_t got = __shfl_xor_sync(kFull, give, 1);
     hi = funnel_r(got, b, ln.sh_own);                  // odd: b, even: got
-    lo11 = funnel_r(a, got, ln.sh_own) >> 11;          // odd: got, even: a
+    lo = funnel_r(a, got, ln.sh_own);                  // odd: got, even: a
 }
 
-// Monte Carlo consumer, in-register: a lane pairs the two words it holds
-// after two consecutive warp steps, so block j of 64 stream words gives the
-// 32 samples (w[64j+i], w[64j+32+i]), i = 0..31, with
-// no data movement between lanes.  Each word, read as a signed 32-bit integer,
-// is a coordinate in [-2^31, 2^31); the sample hits the disc iff
-// x^2 + y^2 < 2^62 (exact).  Returns 1 for a hit.  Per sample ptxas emits
-// IMAD.WIDE + IMAD.HI (the high word of x^2 + y^2), one VIADD and a LEA.HI
-// that accumulates the sign bit -- no shifts, no selects.
+__device__ __forceinline__ void pair_f64(uint32_t a, uint32_t b, const Lane& ln, uint32_t& lo11,
+                                         uint32_t& hi) {
+    uint32_t lo;
+    pair_words(a, b, ln, lo, hi);
+    lo11 = lo >> 11;
+}
+
+// Monte Carlo predicate.  A sample is a pair of CONSECUTIVE words
+// (w[2m], w[2m+1]) of the stream -- in the pair-lane
+// kernel (xg_pairs.cuh) exactly the pair a lane holds.  Each word, read as a
+// signed 32-bit integer, is a coordinate in [-2^31, 2^31); the sample hits
+// the disc iff x^2 + y^2 < 2^62 (exact).  Returns 1 for a hit.  Per sample
+// ptxas emits IMAD.WIDE + IMAD.HI (the high word of x^2 + y^2), one VIADD and
+// a LEA.HI that accumulates the sign bit -- no shifts, no selects.
 __device__ __forceinline__ uint32_t mc_hit(uint32_t a, uint32_t b) {
     const int64_t x = static_cast<int32_t>(a), y = static_cast<int32_t>(b);
     // x^2 + y^2 <= 2^63 fits in uint64; hit iff its high word is < 2^30,
@@ -373,15 +379,27 @@ __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul&
         if (!TAIL || mpair < limit) __stcs(static_cast<double*>(o), pair_to_f64(lo11, hi));
         pair_f64(o2, o3, ln, lo11, hi);
         if (!TAIL || mpair + 32u < limit) __stcs(static_cast<double*>(o) + 32, pair_to_f64(lo11, hi));
+    } else if constexpr (MODE == kMC && (VAR & 16) != 0) {
+        // Samples are consecutive word pairs (2m, 2m+1): staged like f64.
+        uint32_t* st = ln.stage + 128 * BUF;
+        st[lane] = o0;
+        st[32 + lane] = o1;
+        st[64 + lane] = o2;
+        st[96 + lane] = o3;
+        __syncwarp();
+        const uint2 pa = reinterpret_cast<const uint2*>(st)[lane];
+        const uint2 pb = reinterpret_cast<const uint2*>(st + 64)[lane];
+        // limit (TAIL) = wanted 64-word blocks of this body (0 or 1): pairs 0..31
+        if (!TAIL || limit > 0u) hits += mc_hit(pa.x, pa.y);
+        if (!TAIL) hits += mc_hit(pb.x, pb.y);
     } else if constexpr (MODE == kMC) {
-        const uint32_t h0 = mc_hit(o0, o1);
-        const uint32_t h1 = mc_hit(o2, o3);
-        if (!TAIL) {
-            hits += h0 + h1;
-        } else {
-            // limit = wanted 64-word blocks of this body (0 or 1).
-            hits += (limit > 0u ? h0 : 0u);
-        }
+        // Consecutive pairs by shuffle (as pair_f64): a lane pairs words of
+        // steps 0-1 (words 0..63 of the body) and of steps 2-3 (64..127).
+        uint32_t lo, hi;
+        pair_words(o0, o1, ln, lo, hi);
+        if (!TAIL || limit > 0u) hits += mc_hit(lo, hi);
+        pair_words(o2, o3, ln, lo, hi);
+        if (!TAIL) hits += mc_hit(lo, hi);
     }
 }
 
@@ -420,7 +438,7 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
 #pragma unroll
         for (int j = 0; j < 4; ++j) ln.ring_w[32 * (4 + j)] = R[j];
         __syncwarp();
-        if constexpr (MODE == kF64) {
+        if constexpr (MODE == kF64 || MODE == kMC) {
             __shared__ __align__(16) uint32_t stage[kWarpsPerBlock][256];
             ln.stage = stage[threadIdx.x >> 5];
         }

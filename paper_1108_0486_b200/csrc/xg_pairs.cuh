@@ -1,0 +1,227 @@
+// xg_pairs.cuh -- the pair-lane generation kernel (sm_100a), default for
+// every w = 32, r = 128 set with r - s < 64 (xorgensgp32 and the J = 1
+// runtime sets).
+//
+// Layout.  The 128-word window is held as 64 word PAIRS: lane l owns pair l
+// (words 2l, 2l+1: "A") and pair 32 + l (words 64 + 2l, 65 + 2l: "B").  One
+// "double step" makes the next 64 words, lane l producing the pair
+//
+//   N.x = T(W[2l],   a, b) ^ T(W[2l + q],     c, d)      q = r - s
+//   N.y = T(W[2l+1], a, b) ^ T(W[2l + q + 1], c, d)      (xorgens.hpp:39-47)
+//
+// Every operand predates the step iff 63 + q < 128, i.e. s >= 64 -- one more
+// than the reference's lane bound min(s, r-s) = 63 needs, because the window
+// is not an in-place circular buffer (proj/src/parallel.cpp:8-42 writes its
+// results back into the slots it reads; here the new pair only replaces A
+// after both operands are read).  For xorgensgp32 (q = 63):
+//   W[2l + 63] = .y of pair l + 31: lane l-1's B.y, or lane 31's A.y for l = 0
+//   W[2l + 64] = .x of pair l + 32: the lane's OWN B.x
+// so a double step needs ONE shuffle (and one select of the giver's register)
+// for 64 words, against one shared-memory load + store per 32 words in the
+// word-per-lane kernel (xg_kernels.cuh).  N then becomes B and B becomes A by
+// register renaming (2-step unroll), so there are no moves.
+//
+// Outputs.  A lane holds two consecutive words of the stream, so every store
+// is one 64-bit (u32/f32 pairs, one f64) or 128-bit (zero-extended u64
+// words) coalesced, evict-first store: one STG.64 writes 256 contiguous bytes
+// per warp.  f64 = (u64 >> 11) * 2^-53 of the lane's own (lo, hi) pair, and
+// the Monte Carlo sample is the lane's own pair -- no data movement between
+// lanes for either.
+#pragma once
+
+#include <cstdint>
+#include <type_traits>
+
+#include "xg_kernels.cuh"
+
+namespace xgk {
+
+__device__ __forceinline__ uint32_t xs(uint32_t x, unsigned l, unsigned r) {
+    const uint32_t t = x ^ (x << l);
+    return t ^ (t >> r);
+}
+
+struct PairLane {
+    unsigned m;         // q = 2m + 1
+    unsigned src1, src2;  // shuffle sources of pair l+m (.y) and pair l+m+1 (.x)
+    bool a1, a2;        // this lane gives A (else B) to shuffle 1 / 2
+};
+
+__device__ __forceinline__ PairLane make_pair_lane(unsigned delta) {
+    PairLane pl;
+    const unsigned lane = threadIdx.x & 31u;
+    pl.m = 16u + (delta - 1u) / 2u;  // q = 32 + delta (J = 1), delta odd
+    pl.src1 = (lane + pl.m) & 31u;
+    pl.src2 = (lane + pl.m + 1u) & 31u;
+    // Giver lane L serves reader L - m (A) when L >= m, else reader L + 32 - m (B).
+    pl.a1 = lane >= pl.m;
+    pl.a2 = lane >= pl.m + 1u;
+    return pl;
+}
+
+// One double step: the next 64 words from the window (A, B); returns the
+// lane's new pair.
+template <class P>
+__device__ __forceinline__ uint2 double_step(const uint2 A, const uint2 B, const P& p,
+                                             const PairLane& pl) {
+    uint32_t ty, tx;
+    if constexpr (std::is_same_v<P, GP32>) {
+        const unsigned lane = threadIdx.x & 31u;
+        const uint32_t give = lane == 31u ? A.y : B.y;
+        ty = __shfl_sync(kFull, give, (lane + 31u) & 31u);
+        tx = B.x;
+    } else {
+        ty = __shfl_sync(kFull, pl.a1 ? A.y : B.y, pl.src1);
+        tx = __shfl_sync(kFull, pl.a2 ? A.x : B.x, pl.src2);
+    }
+    uint2 n;
+    n.x = xs(A.x, p.a, p.b) ^ xs(ty, p.c, p.d);
+    n.y = xs(A.y, p.a, p.b) ^ xs(tx, p.c, p.d);
+    return n;
+}
+
+template <class P>
+__device__ __forceinline__ uint32_t weyl_mix(uint32_t w, uint32_t v, const P& p) {
+    return (w ^ (w >> p.gamma)) + v;  // xorgens.hpp:58-62
+}
+
+// Emit double step `j` (0 or 1) of a body (128 words).  o is the lane's output
+// cursor at the body start; `limit` (TAIL only) = values of this body wanted.
+template <int MODE, bool TAIL>
+__device__ __forceinline__ void pair_emit(uint2 v, void* o, int j, unsigned limit,
+                                          uint32_t& hits) {
+    const unsigned lane = threadIdx.x & 31u;
+    if constexpr (MODE == kU32 || MODE == kRaw) {
+        if (!TAIL || 64u * j + 2u * lane < limit) __stcs(static_cast<uint2*>(o) + 32 * j, v);
+    } else if constexpr (MODE == kF32) {
+        if (!TAIL || 64u * j + 2u * lane < limit)
+            __stcs(static_cast<float2*>(o) + 32 * j, make_float2(u32_to_f32(v.x), u32_to_f32(v.y)));
+    } else if constexpr (MODE == kWide) {
+        if (!TAIL || 64u * j + 2u * lane < limit)
+            __stcs(static_cast<ulonglong2*>(o) + 32 * j, make_ulonglong2(v.x, v.y));
+    } else if constexpr (MODE == kF64) {
+        if (!TAIL || 32u * j + lane < limit) __stcs(static_cast<double*>(o) + 32 * j, raw_pair_to_f64(v.x, v.y));
+    } else if constexpr (MODE == kMC) {
+        if (!TAIL || 32u * j + lane < limit) hits += mc_hit(v.x, v.y);
+    }
+}
+
+template <int MODE>
+__device__ __forceinline__ void* pair_advance(void* o) {  // one body
+    if constexpr (MODE == kU32 || MODE == kRaw) return static_cast<uint2*>(o) + 64;
+    else if constexpr (MODE == kF32) return static_cast<float2*>(o) + 64;
+    else if constexpr (MODE == kWide) return static_cast<ulonglong2*>(o) + 64;
+    else if constexpr (MODE == kF64) return static_cast<double*>(o) + 64;
+    else return o;
+}
+
+// One body = two double steps = 128 words; (A, B) := (N0, N1).
+template <int MODE, bool TAIL, class P>
+__device__ __forceinline__ void pair_body(uint2& A, uint2& B, const P& p, const PairLane& pl,
+                                          uint32_t& wl, uint32_t w64, void* o, uint32_t& hits,
+                                          unsigned limit) {
+    constexpr bool kW = MODE != kRaw;
+    const uint2 n0 = double_step(A, B, p, pl);
+    const uint2 n1 = double_step(B, n0, p, pl);
+    if constexpr (MODE != kSkip) {
+        uint2 o0 = n0, o1 = n1;
+        if constexpr (kW) {
+            const uint32_t w1 = wl + w64;
+            o0.x = weyl_mix(wl, n0.x, p);
+            o0.y = weyl_mix(wl + p.omega, n0.y, p);
+            o1.x = weyl_mix(w1, n1.x, p);
+            o1.y = weyl_mix(w1 + p.omega, n1.y, p);
+        }
+        pair_emit<MODE, TAIL>(o0, o, 0, limit, hits);
+        pair_emit<MODE, TAIL>(o1, o, 1, limit, hits);
+    }
+    wl += 2u * w64;
+    A = n0;
+    B = n1;
+}
+
+// Fill / conversion / Monte Carlo / skip for streams [g_begin, g_begin +
+// g_count), `words` words per stream, continuing from and saving back each
+// stream's state (same contract as fill_kernel in xg_kernels.cuh).
+// Requirements checked by the host: u32/f32/raw rows 8-byte aligned (even
+// `words`), u64 rows 16-byte aligned, f64 `words` even, MC `words` a
+// multiple of 64.
+// GP32 fits 32 registers (full occupancy); the runtime-parameter sets keep
+// their extra shift registers rather than spill.
+template <class P, int MODE>
+__global__ void __launch_bounds__(kThreads, std::is_same_v<P, GP32> ? 8 : 5)
+pair_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32_t g_begin,
+            uint32_t g_count, uint64_t words, void* __restrict__ out,
+            unsigned long long* __restrict__ hits_out) {
+    const unsigned lane = threadIdx.x & 31u;
+    const uint32_t gl = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (gl >= g_count) return;
+    const uint32_t g = g_begin + gl;
+    const PairLane pl = make_pair_lane(p.delta);
+
+    uint32_t* w = win + static_cast<size_t>(g) * kR;
+    uint2 A = reinterpret_cast<const uint2*>(w)[lane];
+    uint2 B = reinterpret_cast<const uint2*>(w)[32 + lane];
+    const uint32_t weyl0 = weyl[g];
+    uint32_t wl = weyl0 + (2u * lane + 1u) * p.omega;  // Weyl term of word 2l (parallel.cpp:33-39)
+    const uint32_t w64 = 64u * p.omega;
+
+    void* o = out;
+    if constexpr (MODE == kU32 || MODE == kRaw || MODE == kF32)
+        o = static_cast<uint32_t*>(out) + static_cast<uint64_t>(gl) * words + 2u * lane;
+    else if constexpr (MODE == kWide)
+        o = static_cast<unsigned long long*>(out) + static_cast<uint64_t>(gl) * words + 2u * lane;
+    else if constexpr (MODE == kF64)
+        o = static_cast<double*>(out) + static_cast<uint64_t>(gl) * (words >> 1) + lane;
+    uint32_t hits = 0;
+
+    uint64_t left = words >> 7;  // bodies of 128 words
+    while (left != 0) {
+        const uint32_t n = static_cast<uint32_t>(left < (1ull << 30) ? left : (1ull << 30));
+        left -= n;
+        uint32_t i = 0;
+#pragma unroll 1
+        for (; i + 4 <= n; i += 4) {
+            pair_body<MODE, false>(A, B, p, pl, wl, w64, o, hits, 0);
+            pair_body<MODE, false>(A, B, p, pl, wl, w64, pair_advance<MODE>(o), hits, 0);
+            o = pair_advance<MODE>(pair_advance<MODE>(o));
+            pair_body<MODE, false>(A, B, p, pl, wl, w64, o, hits, 0);
+            pair_body<MODE, false>(A, B, p, pl, wl, w64, pair_advance<MODE>(o), hits, 0);
+            o = pair_advance<MODE>(pair_advance<MODE>(o));
+        }
+#pragma unroll 1
+        for (; i < n; ++i) {
+            pair_body<MODE, false>(A, B, p, pl, wl, w64, o, hits, 0);
+            o = pair_advance<MODE>(o);
+        }
+    }
+
+    const unsigned tail = static_cast<unsigned>(words & 127u);
+    if (tail != 0) {
+        // One more full body; only the first `tail` words are emitted and the
+        // saved window ends exactly at word `words`: positions tail..tail+127
+        // of (old window, new 128 words).
+        const uint2 OA = A, OB = B;
+        const unsigned lim = (MODE == kF64 || MODE == kMC) ? tail >> 1 : tail;
+        pair_body<MODE, true>(A, B, p, pl, wl, w64, o, hits, lim);
+        const uint32_t v[8] = {OA.x, OA.y, OB.x, OB.y, A.x, A.y, B.x, B.y};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const unsigned q = 64u * (k >> 1) + 2u * lane + (k & 1);
+            if (q >= tail && q < tail + kR) w[q - tail] = v[k];
+        }
+    } else {
+        reinterpret_cast<uint2*>(w)[lane] = A;
+        reinterpret_cast<uint2*>(w)[32 + lane] = B;
+    }
+    if (MODE != kRaw && lane == 0) weyl[g] = weyl0 + static_cast<uint32_t>(words) * p.omega;
+
+    if constexpr (MODE == kMC) {
+        unsigned long long t = hits;
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) t += __shfl_xor_sync(kFull, t, s);
+        if (lane == 0 && t != 0) atomicAdd(hits_out, t);
+    }
+}
+
+}  // namespace xgk

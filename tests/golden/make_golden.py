@@ -87,9 +87,9 @@ def main() -> None:
     f32 = ((w.astype(np.uint32) >> 8).astype(np.float32) * np.float32(2.0 ** -24))
     u64 = w[0::2] | (w[1::2] << np.uint64(32))
     f64 = (u64 >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
-    blk = w.astype(np.uint32).view(np.int32).astype(np.int64).reshape(-1, 2, 32)  # (w[i], w[32+i])
-    x = blk[:, 0, :]
-    y = blk[:, 1, :]
+    xy = w.astype(np.uint32).view(np.int32).astype(np.int64).reshape(-1, 2)  # (w[2m], w[2m+1])
+    x = xy[:, 0]
+    y = xy[:, 1]
     hits = int(np.count_nonzero((x * x).astype(np.uint64) + (y * y).astype(np.uint64)
                                 < np.uint64(1 << 62)))
     out["conversions_seed42"] = {"f32_bits": [f"{v:08x}" for v in f32.view(np.uint32)],

@@ -157,7 +157,7 @@ def test_mc_pi_exact_vs_oracle(oracle, samples):
 
 
 def test_mc_pi_block_rule_and_continuation(oracle):
-    """Samples come in 64-word blocks (w[64j+i], w[64j+32+i]); a call must be
+    """Samples are consecutive word pairs (w[2m], w[2m+1]); a call must be
     a multiple of 32 samples; MC and fills interleave on the same streams."""
     e = xg.BlockEnsemble(GP32, 21, 3, 63)
     with pytest.raises(ValueError):

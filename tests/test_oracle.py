@@ -236,3 +236,48 @@ def test_golden_raw_streams(oracle, golden):
     for seed, words in golden["raw_streams"].items():
         e = oracle.ensemble(int(seed), 1)
         assert np.array_equal(e.fill_raw_u32(len(words))[0], u32(words)), seed
+
+
+def _xs(x, l, r):
+    t = (x ^ (x << np.uint32(l))) & np.uint32(0xFFFFFFFF)
+    return t ^ (t >> np.uint32(r))
+
+
+def _shfl(vals, src):
+    return vals[src]
+
+
+@pytest.mark.parametrize("s", [65, 67, 79, 93, 95])
+def test_pair_lane_schedule_equals_serial(oracle, s):
+    """The pair-lane kernel's schedule (paper_1108_0486_b200/csrc/xg_pairs.cuh),
+    simulated lane by lane with its exact shuffle sources and giver selects:
+    lane l holds pairs A = (W[2l], W[2l+1]) and B = (W[64+2l], W[65+2l]), and
+    a double step makes the 64 words N[2l], N[2l+1] from the pre-step window.
+    Must equal the serial linear recurrence (RawXorgens::next,
+    proj/include/xg/baselines.hpp:60-71) for every r = 128 set with
+    r - s < 64 (s = 65 is xorgensgp32: one shuffle, the other operand own)."""
+    p = oracle.params(128, s, 15, 14, 12, 17, 32) if s == 65 else oracle.params(128, s, 11, 7, 9, 19, 32)
+    assert oracle.check(p) == 0
+    q = 128 - s  # 33..63: the J = 1 sets (r - s = 32 + delta)
+    m = 16 + (q - 32 - 1) // 2  # make_pair_lane: q = 2m + 1
+    assert q == 2 * m + 1
+    e = oracle.ensemble(5, 1, p)
+    W = e.logical_buffer(0).astype(np.uint32)
+    want = e.fill_raw_u32(64 * 9)[0]
+    lane = np.arange(32)
+    A = np.stack([W[2 * lane], W[2 * lane + 1]], axis=1)
+    B = np.stack([W[64 + 2 * lane], W[65 + 2 * lane]], axis=1)
+    got = []
+    for _ in range(9):
+        if s == 65:  # GP32 specialisation: give = lane == 31 ? A.y : B.y from lane l-1
+            give = np.where(lane == 31, A[:, 1], B[:, 1])
+            ty = _shfl(give, (lane + 31) & 31)
+            tx = B[:, 0]
+        else:  # runtime sets: two shuffles
+            ty = _shfl(np.where(lane >= m, A[:, 1], B[:, 1]), (lane + m) & 31)
+            tx = _shfl(np.where(lane >= m + 1, A[:, 0], B[:, 0]), (lane + m + 1) & 31)
+        N = np.stack([_xs(A[:, 0], p.a, p.b) ^ _xs(ty, p.c, p.d),
+                      _xs(A[:, 1], p.a, p.b) ^ _xs(tx, p.c, p.d)], axis=1).astype(np.uint32)
+        got.append(N.reshape(-1))  # lane l's pair = words 2l, 2l+1 of the step
+        A, B = B, N
+    assert np.array_equal(np.concatenate(got), want)
