@@ -6,7 +6,7 @@ P = 2^14 streams x 2^16 words, base_seed 1, block-major, bit-exact with the
 reference.  A "step" is one BlockEnsemble::generate(2^16) pass over the
 persistent ensemble (streams continue across steps, exactly like repeated
 generate() calls in the reference, proj/src/parallel.cpp:97-135 and
-proj/src/bench.cpp:95-112) -- one fill_kernel launch.
+proj/src/bench.cpp:95-112) -- one pair_kernel launch (xg_pairs.cuh).
 
 Other workloads (--workload): fill_f32, fill_f64 (config 3), fill_2p34
 (config 4: 2^34 words over N GPUs, strong scaling), mc_pi (config 5: 2^40

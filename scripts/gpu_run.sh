@@ -19,9 +19,9 @@ timeout 900 python bench.py --workload fill_2p34 --steps 10 --warmup 3 --no-cpu 
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
   --log-file $OUT/launches.csv python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu > /dev/null 2>> $OUT/ncu.err
 for w in fill_u32 fill_f32 fill_f64; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:fill_kernel -s 3 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"pair_kernel|fill_kernel" -s 3 -c 1 \
     -o $OUT/prof_$w python bench.py --workload $w --steps 2 --warmup 3 --no-e2e --no-cpu > /dev/null 2>> $OUT/ncu.err
 done
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fill_kernel -s 3 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"pair_kernel|fill_kernel" -s 3 -c 1 \
   -o $OUT/prof_mc_pi python bench.py --workload mc_pi --steps 1 --warmup 3 --no-cpu > /dev/null 2>> $OUT/ncu.err
 echo done > $OUT/DONE
