@@ -272,6 +272,8 @@ def workload_geometry(wl: str, world: int, rank: int):
         P, per = 1 << 14, 1 << 16
         words = P * per * (2 if wl == "fill_f64" else 1)
         return rank * P, P, per, "weak", words * world
+    if wl == "stream1":  # config 1 on the GPU: ONE stream (seed 1 + rank), 10^8 words
+        return rank, 1, 10**8, "weak", 10**8 * world
     if wl == "fill_2p34":
         first, count = xg.partition(1 << 18, world, rank)
         return first, count, 1 << 16, "strong", 1 << 34
@@ -317,7 +319,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="fill_u32",
-                    choices=["fill_u32", "fill_f32", "fill_f64", "fill_2p34", "mc_pi", "skip"])
+                    choices=["fill_u32", "fill_f32", "fill_f64", "fill_2p34", "mc_pi", "skip", "stream1"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -346,9 +348,9 @@ def main():
 
     out = None
     bytes_per_val = {"fill_u32": 4, "fill_f32": 4, "fill_f64": 8, "fill_2p34": 4, "mc_pi": 0,
-                     "skip": 0}[wl]
+                     "skip": 0, "stream1": 4}[wl]
     words_per_val = 2 if wl in ("fill_f64", "mc_pi") else 1
-    if wl in ("fill_u32", "fill_2p34"):
+    if wl in ("fill_u32", "fill_2p34", "stream1"):
         out = torch.empty((count, per), dtype=torch.uint32, device="cuda")
         fn = lambda: ens.fill_u32(per, out=out)  # noqa: E731
     elif wl == "fill_f32":
@@ -389,7 +391,8 @@ def main():
             "fill_f64": "uniform float64 [0,1) fill of 2^30 values (2^31 words) per GPU, fused conversion",
             "fill_2p34": "disjoint-stream fill of 2^34 uint32 across N GPUs",
             "mc_pi": "fused in-register Monte Carlo pi, 2^40 samples across N GPUs",
-            "skip": "generator core only (advance 2^30 words, no stores)"}[wl],
+            "skip": "generator core only (advance 2^30 words, no stores)",
+            "stream1": "one stream per GPU (BASELINE config 1: seed 1, 10^8 uint32), one warp"}[wl],
             "params": "xorgensgp32 (128,65,15,14,12,17) w=32", "base_seed": 1,
             "streams_per_gpu": count, "values_per_stream": per,
             "layout": "block-major out[g*per_stream+k]",
@@ -399,7 +402,12 @@ def main():
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
-    if bytes_per_val:
+    if wl == "stream1":
+        # One warp: the dependency chain of the recurrence, not HBM, bounds it.
+        result["roofline"] = {"bound": "latency (one warp per stream)", "achieved": value / world,
+                              "peak": None, "unit": "RN/s per GPU", "frac": None, "traffic": None,
+                              "kernel_ms_mean": kern_ms}
+    elif bytes_per_val:
         achieved = alg_bytes / (kern_ms / 1e3) / 1e9
         result["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                               "frac": achieved / hbm_peak, "traffic": load_traffic(wl),
@@ -458,6 +466,17 @@ def main():
                          "api": "BlockEnsemble.generate -> xg_generate_host (pinned host buffer)",
                          "steps": e2e_steps}
         del host
+    if rank == 0 and world == 1 and not args.no_cpu and wl == "stream1":
+        try:
+            from oracle import Reference
+
+            result["cpu_baseline"] = {
+                "value": Reference().serial_rate(1, 10**8, 20), "unit": "RN/s", "cores": 1,
+                "kind": "reference",
+                "sample": "XorgensState(xorgensgp32, 1): 10^8 next_word in 20 chunks, best "
+                          "chunk rate (measure_throughput, proj/src/bench.cpp:67-93)"}
+        except Exception as e:  # noqa: BLE001
+            result["cpu_baseline"] = {"value": None, "unavailable": str(e)}
     if rank == 0 and world == 1 and not args.no_cpu and wl in ("fill_u32", "fill_f32", "fill_f64"):
         try:
             cb = reference_rate(1 << 14, 1 << 14, trials=100, budget_s=10.0)

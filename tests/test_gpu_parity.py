@@ -280,6 +280,24 @@ def test_config2_full_size_checksum(golden, oracle):
         assert np.array_equal(host[s * n:(s + 1) * n], oracle.stream(g["base_seed"] + s, n))
 
 
+def test_config1_single_stream(golden):
+    """BASELINE config 1 on the GPU: ONE stream, seed 1, 10^8 words (one warp,
+    pair-lane kernel) -- xor, sum_k w_k (k+1) mod 2^64 and the last word
+    against the reference-derived golden (tests/golden/ref_vectors.json)."""
+    g = golden["config1"]
+    e = xg.BlockEnsemble(GP32, g["seed"], 1, 63)
+    host = np_u32(e.fill_u32(g["n"]))[0]
+    assert f"{int(np.bitwise_xor.reduce(host)):08x}" == g["xor"]
+    ws = 0
+    chunk = 1 << 24
+    for start in range(0, host.size, chunk):
+        w = host[start:start + chunk].astype(np.uint64)
+        pos = np.arange(start + 1, start + w.size + 1, dtype=np.uint64)
+        ws = (ws + int(np.sum(w * pos, dtype=np.uint64))) % 2**64
+    assert f"{ws:016x}" == g["sum"]
+    assert f"{int(host[-1]):08x}" == g["last"]
+
+
 @pytest.mark.slow
 def test_full_size_float_properties(oracle):
     """2^30 f32 and f64 values: range, mean, and sampled streams bit-exact."""
