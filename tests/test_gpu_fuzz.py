@@ -1,0 +1,89 @@
+"""Randomised call sequences on the GPU against the oracle.
+
+Every call continues the streams, so a random mix of fills (u32, f32, f64,
+u64, raw, uint64 words), Monte Carlo, skips and host generates -- at ragged
+lengths, odd and even stream positions, into aligned and deliberately
+misaligned output views -- walks the kernel dispatch through every
+transition: the pair-lane kernel (xg_pairs.cuh), its word-per-lane fallback
+for rows the pair stores cannot address and for J = 2 sets (xg_kernels.cuh),
+and the tail bodies of both.  Bit-exact after every call.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1108_0486_b200 as xg  # noqa: E402
+
+SETS = {
+    "gp32": (128, 65, 15, 14, 12, 17, 32, 2654435769, 16),  # compile-time kernels
+    "rt_j1": (128, 95, 17, 12, 13, 15, 32, 2654435769, 16),  # q = 33: pair kernel, 2 shuffles
+    "rt_j2": (128, 33, 11, 7, 9, 19, 32, 0x6A09E667 | 1, 11),  # q = 95: word-per-lane only
+}
+
+
+def _view(n_rows, per, dtype, misalign):
+    """A contiguous (n_rows, per) CUDA tensor, optionally 1 element off the
+    allocation's alignment (4 or 8 bytes: the pair kernel must not be used)."""
+    base = torch.empty(n_rows * per + 1, dtype=dtype, device="cuda")
+    off = 1 if misalign else 0
+    return base[off:off + n_rows * per].view(n_rows, per)
+
+
+def _host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", list(SETS))
+@pytest.mark.parametrize("seed", [1, 2])
+def test_random_call_sequence(oracle, name, seed):
+    rng = np.random.default_rng(1000 * seed + len(name))
+    r, s, a, b, c, d, w, omega, gamma = SETS[name]
+    p = xg.GeneratorParams(r, s, a, b, c, d, w, omega, gamma)
+    streams = int(rng.choice([1, 3, 8, 13]))
+    base = int(rng.integers(0, 2**63))
+    e = xg.BlockEnsemble(p, base, streams, 32)
+    o = oracle.ensemble(base, streams, oracle.params(r, s, a, b, c, d, w, omega, gamma))
+    ops = ["u32", "f32", "f64", "u64", "raw", "words", "mc", "skip", "host"]
+    for step in range(40):
+        op = ops[int(rng.integers(len(ops)))]
+        n = int(rng.integers(1, 700))
+        mis = bool(rng.integers(2))
+        tag = f"{name} step {step}: {op}({n}, misaligned={mis})"
+        if op == "u32":
+            got = _host(e.fill_u32(n, out=_view(streams, n, torch.uint32, mis)))
+            assert np.array_equal(got, o.fill_u32(n)), tag
+        elif op == "f32":
+            got = _host(e.fill_f32(n, out=_view(streams, n, torch.float32, mis)))
+            assert np.array_equal(got.view(np.uint32), o.fill_f32(n).view(np.uint32)), tag
+        elif op == "f64":
+            got = _host(e.fill_f64(n, out=_view(streams, n, torch.float64, mis)))
+            assert np.array_equal(got.view(np.uint64), o.fill_f64(n).view(np.uint64)), tag
+        elif op == "u64":
+            got = _host(e.fill_u64(n, out=_view(streams, n, torch.uint64, mis)))
+            want = o.fill_u32(2 * n).astype(np.uint64)
+            assert np.array_equal(got, want[:, 0::2] | (want[:, 1::2] << np.uint64(32))), tag
+        elif op == "raw":
+            got = _host(e.fill_raw_u32(n, out=_view(streams, n, torch.uint32, mis)))
+            assert np.array_equal(got, o.fill_raw_u32(n)), tag
+        elif op == "words":
+            got = _host(e.fill_words(n, out=_view(streams, n, torch.uint64, mis)))
+            assert np.array_equal(got, o.fill_words(n)), tag
+        elif op == "mc":
+            k = 32 * (1 + n % 7)
+            assert int(_host(e.mc_pi(k))[0]) == int(o.mc_hits(k).sum()), tag
+        elif op == "skip":
+            e.skip(n)
+            o.fill_u32(n)
+        else:
+            assert np.array_equal(e.generate(n), o.fill_u32(n)), tag
+    # the states agree at the end too
+    for g in range(streams):
+        buf, wy = e.block_state(g)
+        assert np.array_equal(np.array(buf, dtype=np.uint32), o.logical_buffer(g).astype(np.uint32))
+        assert wy == o.weyl(g)
