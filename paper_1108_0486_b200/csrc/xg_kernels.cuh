@@ -1,4 +1,8 @@
-// xg_kernels.cuh -- sm_100a device code for the xorgensGP generation path.
+// xg_kernels.cuh -- sm_100a device code for the xorgensGP generation path:
+// the seeding kernel (K1), shared helpers, and the WORD-PER-LANE fill kernel.
+// The default fill kernel is the pair-lane kernel in xg_pairs.cuh; the one
+// here runs the J = 2 parameter sets, output rows the pair stores cannot
+// address, and the XG_VARIANT experiments.
 //
 // Design: ONE WARP PER STREAM, the r = 128 word window in
 // registers.  Lane l holds logical window words W[l], W[32+l], W[64+l],
