@@ -14,6 +14,7 @@
 #include <cstring>
 #include <new>
 #include <numeric>
+#include <type_traits>
 #include <vector>
 
 #include "xg_gpu.h"
@@ -56,6 +57,7 @@ struct xg_ensemble {
     uint32_t num_streams = 0;
     uint64_t base_seed = 0, first_stream = 0;
     unsigned lanes = 0;
+    int sms = 148;  // multiprocessors of `device` (CTA sizing of small ensembles)
     uint32_t* d_win = nullptr;   // [num_streams][128] logical window, oldest first
     uint32_t* d_weyl = nullptr;  // [num_streams] Weyl accumulator
     uint64_t* d_win64 = nullptr;   // generic path: [num_streams][r] words, oldest first
@@ -161,8 +163,23 @@ bool pair_aligned(const void* out, uint64_t words) {
 template <int MODE, class P>
 int launch_pair(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t words,
                 void* out, unsigned long long* hits, cudaStream_t s) {
-    pair_kernel<P, MODE><<<grid_for(g_count), kThreads, 0, s>>>(p, h->d_win, h->d_weyl, g_begin,
-                                                                g_count, words, out, hits);
+    // Streams (warps) per CTA.  Every stream is the same amount of work, so
+    // what matters is how evenly the warps land on the SMs.  Up to 32 streams
+    // per SM, launch one CTA per SM holding ceil(P / SMs) streams: the
+    // busiest SM carries at most one stream more than the average, and small
+    // ensembles use every SM (8-stream CTAs put 64 streams on 8 SMs: 1.32e11
+    // against 0.95e11 RN/s; 4096 streams: 1.57e12 against 1.44e12).  Larger
+    // ensembles: 8-stream CTAs (profiles/README.md, r1p).
+    static const bool force8 = getenv("XG_CTA8") != nullptr;  // experiment: always 8 streams/CTA
+    const uint64_t sms = static_cast<uint64_t>(std::max(1, h->sms));
+    uint32_t wpb = kWarpsPerBlock;
+    if (!force8 && g_count <= 32 * sms) {
+        wpb = static_cast<uint32_t>((g_count + sms - 1) / sms);  // 1..32
+        if (!std::is_same_v<P, GP32>) wpb = std::min<uint32_t>(wpb, kWarpsPerBlock);
+    }
+    const unsigned grid = static_cast<unsigned>((static_cast<uint64_t>(g_count) + wpb - 1) / wpb);
+    pair_kernel<P, MODE><<<grid, 32 * wpb, 0, s>>>(p, h->d_win, h->d_weyl, g_begin, g_count, words,
+                                                   out, hits);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cuda_rc(cudaGetLastError());
 }
@@ -467,6 +484,7 @@ int xg_ensemble_create(const xg_params_t* p, uint64_t base_seed, uint64_t first_
     h->base_seed = base_seed;
     h->first_stream = first_stream;
     h->lanes = lanes;
+    cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
     int rc = alloc_state(h);
     if (!rc) rc = launch_seed(h, base_seed + first_stream, reinterpret_cast<cudaStream_t>(stream));
     if (rc) {
@@ -498,6 +516,7 @@ int xg_ensemble_create_from_raw(const xg_params_t* p, uint32_t num_streams,
     h->device = device;
     h->num_streams = num_streams;
     h->lanes = lane_bound_impl(p);
+    cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
     int rc = alloc_state(h);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (!rc && kind == kGeneric) {

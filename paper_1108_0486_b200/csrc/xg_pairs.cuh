@@ -146,15 +146,17 @@ __device__ __forceinline__ void pair_body(uint2& A, uint2& B, const P& p, const 
 // Requirements checked by the host: u32/f32/raw rows 8-byte aligned (even
 // `words`), u64 rows 16-byte aligned, f64 `words` even, MC `words` a
 // multiple of 64.
-// GP32 fits 32 registers (full occupancy); the runtime-parameter sets keep
-// their extra shift registers rather than spill.
+// CTAs of 1..32 warps (one stream each).  GP32 fits 32 registers (64 warps
+// per SM); the runtime-parameter sets (CTAs of <= 8 warps) keep their extra
+// shift registers rather than spill.
 template <class P, int MODE>
-__global__ void __launch_bounds__(kThreads, std::is_same_v<P, GP32> ? 8 : 5)
+__global__ void __launch_bounds__(std::is_same_v<P, GP32> ? 1024 : 256, std::is_same_v<P, GP32> ? 2 : 5)
 pair_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32_t g_begin,
             uint32_t g_count, uint64_t words, void* __restrict__ out,
             unsigned long long* __restrict__ hits_out) {
     const unsigned lane = threadIdx.x & 31u;
-    const uint32_t gl = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    // CTAs hold 1..8 streams (the host spreads small ensembles over the SMs)
+    const uint32_t gl = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (gl >= g_count) return;
     const uint32_t g = g_begin + gl;
     const PairLane pl = make_pair_lane(p.delta);
