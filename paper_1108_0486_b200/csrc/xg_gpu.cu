@@ -57,7 +57,8 @@ struct xg_ensemble {
     uint32_t num_streams = 0;
     uint64_t base_seed = 0, first_stream = 0;
     unsigned lanes = 0;
-    int sms = 148;  // multiprocessors of `device` (CTA sizing of small ensembles)
+    int sms = 148;          // multiprocessors of `device` (CTA sizing)
+    int smem_per_sm = 0;    // shared memory per SM (occupancy cap of the fills)
     uint32_t* d_win = nullptr;   // [num_streams][128] logical window, oldest first
     uint32_t* d_weyl = nullptr;  // [num_streams] Weyl accumulator
     uint64_t* d_win64 = nullptr;   // generic path: [num_streams][r] words, oldest first
@@ -141,6 +142,7 @@ unsigned grid_for(uint32_t n) {
 // xg_kernels.cuh).  XG_VARIANT = 0, 1, 16, 48 or 144 forces a word-per-lane
 // variant for experiments (measurements in profiles/README.md).
 constexpr int kPairs = 512;
+constexpr int kFillCtasPerSm = 2;  // resident 8-stream fill CTAs per SM (launch_pair)
 
 int variant_for(int) {
     static int forced = [] {
@@ -170,16 +172,38 @@ int launch_pair(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count, 
     // ensembles use every SM (8-stream CTAs put 64 streams on 8 SMs: 1.32e11
     // against 0.95e11 RN/s; 4096 streams: 1.57e12 against 1.44e12).  Larger
     // ensembles: 8-stream CTAs (profiles/README.md, r1p).
-    static const bool force8 = getenv("XG_CTA8") != nullptr;  // experiment: always 8 streams/CTA
     const uint64_t sms = static_cast<uint64_t>(std::max(1, h->sms));
     uint32_t wpb = kWarpsPerBlock;
-    if (!force8 && g_count <= 32 * sms) {
+    if (g_count <= 32 * sms) {
         wpb = static_cast<uint32_t>((g_count + sms - 1) / sms);  // 1..32
         if (!std::is_same_v<P, GP32>) wpb = std::min<uint32_t>(wpb, kWarpsPerBlock);
     }
+    // u32 / raw fills of large ensembles: at most kFillCtasPerSm resident
+    // 8-stream CTAs per SM (16 write streams per SM instead of 64), enforced
+    // by reserving shared memory the kernel does not use.  The fill is
+    // HBM-bound far below full occupancy (~7 streams saturate an SM's ALU
+    // pipe), and fewer concurrent write streams, started in staggered CTA
+    // waves, write faster: 1.57e12 against 1.53e12 RN/s under the power cap,
+    // +1 % in bursts at 2^14 streams, +6 % at 2^16 (r1u, profiles/README.md).
+    // The conversions gain nothing from it (f32 -0.6 %, f64 -1.2 % in
+    // bursts, equal under the cap) and run at full occupancy.
+    // XG_CTAS_PER_SM overrides the cap for experiments (0 = none).
+    constexpr bool kStores = MODE == kU32 || MODE == kRaw;
+    static const int cap = [] {
+        const char* e = getenv("XG_CTAS_PER_SM");
+        return e ? atoi(e) : kFillCtasPerSm;
+    }();
+    size_t smem = 0;
+    if (kStores && cap > 0 && wpb == kWarpsPerBlock && h->smem_per_sm > 0) {
+        // cap CTAs fit, cap + 1 do not (each CTA also reserves 1 KB).
+        smem = static_cast<size_t>(h->smem_per_sm) / cap - 2048;
+        if (cudaFuncSetAttribute(pair_kernel<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)) != cudaSuccess)
+            smem = 0;
+    }
     const unsigned grid = static_cast<unsigned>((static_cast<uint64_t>(g_count) + wpb - 1) / wpb);
-    pair_kernel<P, MODE><<<grid, 32 * wpb, 0, s>>>(p, h->d_win, h->d_weyl, g_begin, g_count, words,
-                                                   out, hits);
+    pair_kernel<P, MODE><<<grid, 32 * wpb, smem, s>>>(p, h->d_win, h->d_weyl, g_begin, g_count,
+                                                      words, out, hits);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cuda_rc(cudaGetLastError());
 }
@@ -485,6 +509,7 @@ int xg_ensemble_create(const xg_params_t* p, uint64_t base_seed, uint64_t first_
     h->first_stream = first_stream;
     h->lanes = lanes;
     cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&h->smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
     int rc = alloc_state(h);
     if (!rc) rc = launch_seed(h, base_seed + first_stream, reinterpret_cast<cudaStream_t>(stream));
     if (rc) {
@@ -517,6 +542,7 @@ int xg_ensemble_create_from_raw(const xg_params_t* p, uint32_t num_streams,
     h->num_streams = num_streams;
     h->lanes = lane_bound_impl(p);
     cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&h->smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
     int rc = alloc_state(h);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (!rc && kind == kGeneric) {
