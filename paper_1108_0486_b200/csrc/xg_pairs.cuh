@@ -45,6 +45,7 @@ struct PairLane {
     unsigned m;         // q = 2m + 1
     unsigned src1, src2;  // shuffle sources of pair l+m (.y) and pair l+m+1 (.x)
     bool a1, a2;        // this lane gives A (else B) to shuffle 1 / 2
+    uint32_t is31;      // 1 on lane 31 (the GP32 giver of A.y), else 0
 };
 
 __device__ __forceinline__ PairLane make_pair_lane(unsigned delta) {
@@ -56,6 +57,7 @@ __device__ __forceinline__ PairLane make_pair_lane(unsigned delta) {
     // Giver lane L serves reader L - m (A) when L >= m, else reader L + 32 - m (B).
     pl.a1 = lane >= pl.m;
     pl.a2 = lane >= pl.m + 1u;
+    pl.is31 = lane == 31u ? 1u : 0u;
     return pl;
 }
 
@@ -67,7 +69,11 @@ __device__ __forceinline__ uint2 double_step(const uint2 A, const uint2 B, const
     uint32_t ty, tx;
     if constexpr (std::is_same_v<P, GP32>) {
         const unsigned lane = threadIdx.x & 31u;
-        const uint32_t give = lane == 31u ? A.y : B.y;
+        // give = lane 31 ? A.y : B.y, as B.y + is31 * (A.y - B.y) on the FMA
+        // pipe (IADD + IMAD) instead of a SEL on the busier ALU pipe.
+        uint32_t give;
+        asm("{\n\t.reg .u32 d;\n\tsub.u32 d, %1, %2;\n\tmad.lo.u32 %0, d, %3, %2;\n\t}"
+            : "=r"(give) : "r"(A.y), "r"(B.y), "r"(pl.is31));
         ty = __shfl_sync(kFull, give, (lane + 31u) & 31u);
         tx = B.x;
     } else {
