@@ -71,6 +71,7 @@ __device__ __forceinline__ uint2 double_step(const uint2 A, const uint2 B, const
         const unsigned lane = threadIdx.x & 31u;
         // give = lane 31 ? A.y : B.y, as B.y + is31 * (A.y - B.y) on the FMA
         // pipe (IADD + IMAD) instead of a SEL on the busier ALU pipe.
+        // (The SEL form is 3 % slower for f32, 2 % for MC: profiles/README.md, r1w.)
         uint32_t give;
         asm("{\n\t.reg .u32 d;\n\tsub.u32 d, %1, %2;\n\tmad.lo.u32 %0, d, %3, %2;\n\t}"
             : "=r"(give) : "r"(A.y), "r"(B.y), "r"(pl.is31));
