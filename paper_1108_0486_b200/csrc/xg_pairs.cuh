@@ -45,7 +45,7 @@ struct PairLane {
     unsigned m;         // q = 2m + 1
     unsigned src1, src2;  // shuffle sources of pair l+m (.y) and pair l+m+1 (.x)
     bool a1, a2;        // this lane gives A (else B) to shuffle 1 / 2
-    uint32_t is31;      // 1 on lane 31 (the GP32 giver of A.y), else 0
+    uint32_t is31, not31;  // 1 / 0 on lane 31 (the GP32 giver of A.y), 0 / 1 elsewhere
 };
 
 __device__ __forceinline__ PairLane make_pair_lane(unsigned delta) {
@@ -58,23 +58,31 @@ __device__ __forceinline__ PairLane make_pair_lane(unsigned delta) {
     pl.a1 = lane >= pl.m;
     pl.a2 = lane >= pl.m + 1u;
     pl.is31 = lane == 31u ? 1u : 0u;
+    pl.not31 = 1u - pl.is31;
     return pl;
 }
 
 // One double step: the next 64 words from the window (A, B); returns the
 // lane's new pair.
-template <class P>
+template <int GIVE, class P>
 __device__ __forceinline__ uint2 double_step(const uint2 A, const uint2 B, const P& p,
                                              const PairLane& pl) {
     uint32_t ty, tx;
     if constexpr (std::is_same_v<P, GP32>) {
         const unsigned lane = threadIdx.x & 31u;
-        // give = lane 31 ? A.y : B.y, as B.y + is31 * (A.y - B.y) on the FMA
-        // pipe (IADD + IMAD) instead of a SEL on the busier ALU pipe.
-        // (The SEL form is 3 % slower for f32, 2 % for MC: profiles/README.md, r1w.)
+        // give = lane 31 ? A.y : B.y on the FMA pipe instead of a SEL on the
+        // busier ALU pipe.  GIVE 0: B.y * (1 - is31) + A.y * is31 -- A.y * is31
+        // does not depend on the previous step, so one IMAD sits on the
+        // step-to-step chain (MC +3 %, one stream +16 %); GIVE 1:
+        // B.y + is31 * (A.y - B.y) (IADD + IMAD, both on the chain), 2 % faster
+        // for f32 (profiles/README.md, r1w/r1z).
         uint32_t give;
-        asm("{\n\t.reg .u32 d;\n\tsub.u32 d, %1, %2;\n\tmad.lo.u32 %0, d, %3, %2;\n\t}"
-            : "=r"(give) : "r"(A.y), "r"(B.y), "r"(pl.is31));
+        if constexpr (GIVE == 0)
+            asm("{\n\t.reg .u32 t;\n\tmul.lo.u32 t, %1, %3;\n\tmad.lo.u32 %0, %2, %4, t;\n\t}"
+                : "=r"(give) : "r"(A.y), "r"(B.y), "r"(pl.is31), "r"(pl.not31));
+        else
+            asm("{\n\t.reg .u32 d;\n\tsub.u32 d, %1, %2;\n\tmad.lo.u32 %0, d, %3, %2;\n\t}"
+                : "=r"(give) : "r"(A.y), "r"(B.y), "r"(pl.is31));
         ty = __shfl_sync(kFull, give, (lane + 31u) & 31u);
         tx = B.x;
     } else {
@@ -128,8 +136,9 @@ __device__ __forceinline__ void pair_body(uint2& A, uint2& B, const P& p, const 
                                           uint32_t& wl, uint32_t w64, void* o, uint32_t& hits,
                                           unsigned limit) {
     constexpr bool kW = MODE != kRaw;
-    const uint2 n0 = double_step(A, B, p, pl);
-    const uint2 n1 = double_step(B, n0, p, pl);
+    constexpr int kGive = MODE == kF32 ? 1 : 0;
+    const uint2 n0 = double_step<kGive>(A, B, p, pl);
+    const uint2 n1 = double_step<kGive>(B, n0, p, pl);
     if constexpr (MODE != kSkip) {
         uint2 o0 = n0, o1 = n1;
         if constexpr (kW) {

@@ -18,6 +18,7 @@ b() {  # variant workload steps
 import json,sys; d=json.loads(open('$OUT/b_$2_$1_$3.json').read().strip().splitlines()[-1]); r=d.get('roofline') or {}
 print('$2 $1 steps=$3', '%.4e'%d['value'], r.get('frac'), r.get('kernel_ms_mean'), r.get('kernel_ms_min'), d['clocks']['sm_mhz'], d['clocks']['reasons'])" >> $OUT/bench.txt
 }
-for rep in 1 2; do for v in "$@"; do b $v mc_pi 3; b $v fill_f32 50; b $v fill_u32 50; b $v fill_f64 50; done; done
-for rep in 1 2; do for v in "$@"; do b $v fill_u32 600; done; done
+WL=${WL:-"mc_pi:3 fill_f32:50 fill_u32:50 fill_f64:50 stream1:3"}
+for rep in 1 2; do for v in "$@"; do for wl in $WL; do b $v ${wl%%:*} ${wl##*:}; done; done; done
+[ "${LONG:-1}" = 1 ] && for rep in 1 2; do for v in "$@"; do b $v fill_u32 600; done; done
 use def
