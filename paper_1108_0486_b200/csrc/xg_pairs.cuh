@@ -16,9 +16,9 @@
 // after both operands are read).  For xorgensgp32 (q = 63):
 //   W[2l + 63] = .y of pair l + 31: lane l-1's B.y, or lane 31's A.y for l = 0
 //   W[2l + 64] = .x of pair l + 32: the lane's OWN B.x
-// so a double step needs ONE shuffle (and one select of the giver's register)
-// for 64 words, against one shared-memory load + store per 32 words in the
-// word-per-lane kernel (xg_kernels.cuh).  N then becomes B and B becomes A by
+// so a double step needs ONE shuffle (and the giver's register choice, done
+// with IMADs on the FMA pipe) for 64 words, against one shared-memory load +
+// store per 32 words in the word-per-lane kernel (xg_kernels.cuh).  N then becomes B and B becomes A by
 // register renaming (2-step unroll), so there are no moves.
 //
 // Outputs.  A lane holds two consecutive words of the stream, so every store
