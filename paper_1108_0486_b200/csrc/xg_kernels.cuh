@@ -186,7 +186,9 @@ __device__ __forceinline__ uint32_t weyl_out(uint32_t w, uint32_t v, const P& p,
 // Uniform float: (u >> 8) * 2^-24, exact.  The
 // conversion of a 24-bit integer is exact in every rounding mode; the _rd
 // form compiles to I2F.U32.RM (XU pipe) instead of I2FP (ALU pipe), which is
-// the busiest pipe of this kernel.
+// the busiest pipe of this kernel.  (Reading the half-word and the byte
+// straight out of the register with I2F.U16 R.H1 + I2F.U8 R.B1 and one FFMA
+// saves the shift but is 1 % slower: profiles/README.md, r1za.)
 __device__ __forceinline__ float u32_to_f32(uint32_t u) {
     return __uint2float_rd(u >> 8) * 0x1p-24f;
 }
