@@ -188,13 +188,13 @@ int launch_pair(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count, 
     // The conversions gain nothing from it (f32 -0.6 %, f64 -1.2 % in
     // bursts, equal under the cap) and run at full occupancy.
     // XG_CTAS_PER_SM overrides the cap for experiments (0 = none).
-    constexpr bool kStores = MODE == kU32 || MODE == kRaw;
-    static const int cap = [] {
-        const char* e = getenv("XG_CTAS_PER_SM");
-        return e ? atoi(e) : kFillCtasPerSm;
-    }();
+    // XG_CTAS_PER_SM (experiments) sets the cap for every output mode.
+    constexpr bool kCapped = MODE == kU32 || MODE == kRaw;
+    constexpr bool kStores = kCapped || MODE == kF32 || MODE == kF64 || MODE == kWide;
+    static const char* cap_env = getenv("XG_CTAS_PER_SM");
+    static const int cap = cap_env ? atoi(cap_env) : kFillCtasPerSm;
     size_t smem = 0;
-    if (kStores && cap > 0 && wpb == kWarpsPerBlock && h->smem_per_sm > 0) {
+    if ((cap_env ? kStores : kCapped) && cap > 0 && wpb == kWarpsPerBlock && h->smem_per_sm > 0) {
         // cap CTAs fit, cap + 1 do not (each CTA also reserves 1 KB).
         smem = static_cast<size_t>(h->smem_per_sm) / cap - 2048;
         if (cudaFuncSetAttribute(pair_kernel<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
