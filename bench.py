@@ -158,9 +158,17 @@ def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # XG_BENCH_BACKEND=gloo (testing only): exercise the N>1 flow with every
+    # rank on the visible GPUs round-robin, e.g. two ranks on one GPU.
+    backend = os.environ.get("XG_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     if world > 1 and not dist.is_initialized():
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     elif world == 1:
         torch.cuda.set_device(local)
     return world, rank, local
