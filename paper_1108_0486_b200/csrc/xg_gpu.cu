@@ -142,7 +142,8 @@ unsigned grid_for(uint32_t n) {
 // xg_kernels.cuh).  XG_VARIANT = 0, 1, 16, 48 or 144 forces a word-per-lane
 // variant for experiments (measurements in profiles/README.md).
 constexpr int kPairs = 512;
-constexpr int kFillCtasPerSm = 2;  // resident 8-stream fill CTAs per SM (launch_pair)
+constexpr int kFillWarpsPerCta = 4;  // u32/raw fills of large ensembles: streams per CTA
+constexpr int kFillCtasPerSm = 4;    // ... and resident CTAs per SM (launch_pair)
 
 int variant_for(int) {
     static int forced = [] {
@@ -170,31 +171,43 @@ int launch_pair(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count, 
     // per SM, launch one CTA per SM holding ceil(P / SMs) streams: the
     // busiest SM carries at most one stream more than the average, and small
     // ensembles use every SM (8-stream CTAs put 64 streams on 8 SMs: 1.32e11
-    // against 0.95e11 RN/s; 4096 streams: 1.57e12 against 1.44e12).  Larger
-    // ensembles: 8-stream CTAs (profiles/README.md, r1p).
+    // against 0.95e11 RN/s; 4096 streams: 1.57e12 against 1.44e12;
+    // profiles/README.md, r1p).  Larger ensembles: below.
     const uint64_t sms = static_cast<uint64_t>(std::max(1, h->sms));
+    // u32 / raw fills of large ensembles: 4-stream CTAs, at most
+    // kFillCtasPerSm = 4 of them resident per SM (16 write streams per SM
+    // instead of 64), enforced by reserving shared memory the kernel does not
+    // use.  The fill is HBM-bound far below full occupancy (~7 streams
+    // saturate an SM's ALU pipe), and fewer concurrent write streams, started
+    // in small staggered CTA waves, write faster: 1.596e12 against 1.53e12
+    // RN/s under the power cap, 1.737e12 against 1.72e12 in bursts (r1u,
+    // r1zg in profiles/README.md).  The conversions gain nothing from the cap
+    // and run full (8-stream CTAs, 64 streams per SM).
+    // XG_FILL_WPB / XG_CTAS_PER_SM override CTA size / cap for experiments
+    // (the cap then applies to every output mode; 0 = none).
+    constexpr bool kCapped = MODE == kU32 || MODE == kRaw;
+    constexpr bool kStores = kCapped || MODE == kF32 || MODE == kF64 || MODE == kWide;
+    static const char* wpb_env = getenv("XG_FILL_WPB");
+    static const char* cap_env = getenv("XG_CTAS_PER_SM");
+    static const uint32_t env_wpb = wpb_env ? static_cast<uint32_t>(std::clamp(atoi(wpb_env), 1, 32)) : 0;
+    static const int env_cap = cap_env ? atoi(cap_env) : 0;
+    const bool large = g_count > 32 * sms;
     uint32_t wpb = kWarpsPerBlock;
-    if (g_count <= 32 * sms) {
+    int cap = 0;
+    if (large) {
+        if (kCapped) {
+            wpb = kFillWarpsPerCta;
+            cap = kFillCtasPerSm;
+        }
+        if (env_wpb && std::is_same_v<P, GP32>) wpb = env_wpb;
+        if (cap_env && kStores) cap = env_cap;
+    } else {
+        // one CTA per SM holding ceil(P / SMs) streams (see above)
         wpb = static_cast<uint32_t>((g_count + sms - 1) / sms);  // 1..32
         if (!std::is_same_v<P, GP32>) wpb = std::min<uint32_t>(wpb, kWarpsPerBlock);
     }
-    // u32 / raw fills of large ensembles: at most kFillCtasPerSm resident
-    // 8-stream CTAs per SM (16 write streams per SM instead of 64), enforced
-    // by reserving shared memory the kernel does not use.  The fill is
-    // HBM-bound far below full occupancy (~7 streams saturate an SM's ALU
-    // pipe), and fewer concurrent write streams, started in staggered CTA
-    // waves, write faster: 1.57e12 against 1.53e12 RN/s under the power cap,
-    // +1 % in bursts at 2^14 streams, +6 % at 2^16 (r1u, profiles/README.md).
-    // The conversions gain nothing from it (f32 -0.6 %, f64 -1.2 % in
-    // bursts, equal under the cap) and run at full occupancy.
-    // XG_CTAS_PER_SM overrides the cap for experiments (0 = none).
-    // XG_CTAS_PER_SM (experiments) sets the cap for every output mode.
-    constexpr bool kCapped = MODE == kU32 || MODE == kRaw;
-    constexpr bool kStores = kCapped || MODE == kF32 || MODE == kF64 || MODE == kWide;
-    static const char* cap_env = getenv("XG_CTAS_PER_SM");
-    static const int cap = cap_env ? atoi(cap_env) : kFillCtasPerSm;
     size_t smem = 0;
-    if ((cap_env ? kStores : kCapped) && cap > 0 && wpb == kWarpsPerBlock && h->smem_per_sm > 0) {
+    if (cap > 0 && h->smem_per_sm > 0) {
         // cap CTAs fit, cap + 1 do not (each CTA also reserves 1 KB).
         smem = static_cast<size_t>(h->smem_per_sm) / cap - 2048;
         if (cudaFuncSetAttribute(pair_kernel<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
