@@ -280,6 +280,9 @@ def workload_geometry(wl: str, world: int, rank: int):
         P, per = 1 << 14, 1 << 16
         words = P * per * (2 if wl == "fill_f64" else 1)
         return rank * P, P, per, "weak", words * world
+    if wl == "rank":  # fused GF(2) matrix-rank test: 2^14 streams x 2^12 32x32 matrices per GPU
+        P = 1 << 14
+        return rank * P, P, 1 << 12, "weak", (P << 17) * world
     if wl == "stream1":  # config 1 on the GPU: ONE stream (seed 1 + rank), 10^8 words
         return rank, 1, 10**8, "weak", 10**8 * world
     if wl == "fill_2p34":
@@ -327,7 +330,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="fill_u32",
-                    choices=["fill_u32", "fill_f32", "fill_f64", "fill_2p34", "mc_pi", "skip", "stream1"])
+                    choices=["fill_u32", "fill_f32", "fill_f64", "fill_2p34", "mc_pi", "skip", "stream1",
+                             "rank"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -356,8 +360,8 @@ def main():
 
     out = None
     bytes_per_val = {"fill_u32": 4, "fill_f32": 4, "fill_f64": 8, "fill_2p34": 4, "mc_pi": 0,
-                     "skip": 0, "stream1": 4}[wl]
-    words_per_val = 2 if wl in ("fill_f64", "mc_pi") else 1
+                     "skip": 0, "stream1": 4, "rank": 0}[wl]
+    words_per_val = 2 if wl in ("fill_f64", "mc_pi") else (32 if wl == "rank" else 1)
     if wl in ("fill_u32", "fill_2p34", "stream1"):
         out = torch.empty((count, per), dtype=torch.uint32, device="cuda")
         fn = lambda: ens.fill_u32(per, out=out)  # noqa: E731
@@ -370,6 +374,9 @@ def main():
     elif wl == "skip":  # generator core only (no stores): the integer-issue ceiling
         hits = None
         fn = lambda: ens.skip(per)  # noqa: E731
+    elif wl == "rank":  # fused matrix-rank test: bins only, no HBM traffic
+        hits = torch.zeros(3, dtype=torch.int64, device="cuda")
+        fn = lambda: ens.rank_test(per, counts=hits)  # noqa: E731
     else:
         hits = torch.zeros(1, dtype=torch.int64, device="cuda")
         fn = lambda: ens.mc_pi(per, hits=hits)  # noqa: E731
@@ -400,7 +407,9 @@ def main():
             "fill_2p34": "disjoint-stream fill of 2^34 uint32 across N GPUs",
             "mc_pi": "fused in-register Monte Carlo pi, 2^40 samples across N GPUs",
             "skip": "generator core only (advance 2^30 words, no stores)",
-            "stream1": "one stream per GPU (BASELINE config 1: seed 1, 10^8 uint32), one warp"}[wl],
+            "stream1": "one stream per GPU (BASELINE config 1: seed 1, 10^8 uint32), one warp",
+            "rank": "fused GF(2) 32x32 matrix-rank test (reference matrix_rank_test), "
+                    "2^14 streams x 2^12 matrices per GPU"}[wl],
             "params": "xorgensgp32 (128,65,15,14,12,17) w=32", "base_seed": 1,
             "streams_per_gpu": count, "values_per_stream": per,
             "layout": "block-major out[g*per_stream+k]",
@@ -428,6 +437,24 @@ def main():
                 result["roofline"]["write_only_probe_gbs"] = write_probe_gbs(out, stream)
             except OSError:
                 pass
+    elif wl == "rank":
+        import paper_1108_0486_b200 as xg_
+
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(hits)
+        c = [int(v) for v in hits.tolist()]
+        chi2, pv = xg_.matrix_rank_statistic(c)
+        result["rank"] = {"counts_rank32_31_le30": c, "chi2": chi2, "p_value": pv,
+                          "matrices_per_s": value / 32, "kernel_ms_mean": kern_ms}
+        pipes = load_ncu(wl)
+        result["roofline"] = {
+            "bound": "int-issue", "achieved": value / world, "peak": None, "unit": "RN/s per GPU",
+            "frac": None, "traffic": load_traffic(wl),
+            "alu_pipe_pct": pipes.get("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+            "issue_active_pct": pipes.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "pipe_source": "profiles/ncu_summary.json (ncu --set full)"}
     elif wl == "skip":
         result["roofline"] = {"bound": "int-issue", "achieved": value / world, "peak": None,
                               "unit": "RN/s per GPU", "frac": None, "traffic": None,
@@ -474,6 +501,22 @@ def main():
                          "api": "BlockEnsemble.generate -> xg_generate_host (pinned host buffer)",
                          "steps": e2e_steps}
         del host
+    if rank == 0 and world == 1 and not args.no_cpu and wl == "rank":
+        try:
+            from oracle import Battery, Oracle
+
+            m = 200_000  # bounded sample: 6.4e6 words through the reference's own test
+            words = Oracle().ensemble(1, 1).fill_u32(32 * m)[0]
+            t0 = time.perf_counter()
+            Battery().matrix_rank(words, m)
+            dt = time.perf_counter() - t0
+            result["cpu_baseline"] = {
+                "value": 32 * m / dt, "unit": "RN/s", "cores": 1, "kind": "reference",
+                "sample": f"reference matrix_rank_test (proj/src/stattests/tests.cpp:81-126) over "
+                          f"{m} 32x32 matrices of one stream, 1 thread (the reference test is serial)",
+                "matrices_per_s": m / dt}
+        except Exception as e:  # noqa: BLE001
+            result["cpu_baseline"] = {"value": None, "unavailable": str(e)}
     if rank == 0 and world == 1 and not args.no_cpu and wl == "stream1":
         try:
             from oracle import Reference

@@ -130,6 +130,11 @@ public:
     void mc_pi(std::uint64_t samples, std::uint64_t* dev_hits, xg_stream_t s = nullptr) {
         check(xg_mc_pi(h_, samples, dev_hits, s));
     }
+    // Fused matrix_rank_test counting (proj/src/stattests/tests.cpp:93-109):
+    // adds the (rank 32, 31, <= 30) bins to dev_counts[0..2].
+    void rank_test(std::uint64_t matrices, std::uint64_t* dev_counts, xg_stream_t s = nullptr) {
+        check(xg_rank_test(h_, matrices, dev_counts, s));
+    }
 
     unsigned num_blocks() const noexcept { return n_; }
     unsigned lanes() const noexcept { return lanes_; }

@@ -149,6 +149,19 @@ int xg_fill_f64(xg_ensemble_t h, uint64_t per_stream, double* dev_out, xg_stream
  * *dev_hits (a device uint64).  No HBM traffic. */
 int xg_mc_pi(xg_ensemble_t h, uint64_t samples_per_stream, uint64_t* dev_hits,
              xg_stream_t stream);
+
+/* Fused GF(2) matrix-rank test -- the reference's matrix_rank_test
+ * (proj/src/stattests/tests.cpp:81-126, M = 32) run inside the generator:
+ * each stream supplies 32*matrices_per_stream words continuing its stream,
+ * every 32 consecutive words are one 32 x 32 matrix (row i = word i, bits MSB
+ * first as BitSource reads them, proj/include/xg/stream.hpp:95-112), and the
+ * ranks are binned (32, 31, <= 30) and ADDED to dev_counts[0..2] (device
+ * uint64[3]).  The chi-square statistic and p-value follow on the host from
+ * the counts.  No HBM traffic.  w = 32 sets with r - s < 64 (the pair-lane
+ * kernel); XG_EUNSUPPORTED otherwise.  Replaces tests.cpp:81-126 (the
+ * counting loop; rank: proj/src/stattests/gf2.cpp:8-33). */
+int xg_rank_test(xg_ensemble_t h, uint64_t matrices_per_stream, uint64_t* dev_counts,
+                 xg_stream_t stream);
 /* Advance every stream by `words` without storing (discard). */
 int xg_skip(xg_ensemble_t h, uint64_t words, xg_stream_t stream);
 

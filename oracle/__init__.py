@@ -63,6 +63,9 @@ class Oracle:
                   "xgo_ensemble_mc_pi", "xgo_ensemble_fill_raw_u32", "xgo_ensemble_fill_words"):
             getattr(L, n).argtypes = [_vp, _u32, _u64, _vp, _int]
         L.xgo_ensemble_checksums.argtypes = [_vp, _u32, _u64, _vp, _vp, _int]
+        L.xgo_ensemble_rank_counts.argtypes = [_vp, _u32, _u64, _vp, _int]
+        L.xgo_gf2_rank32.argtypes = [_vp]
+        L.xgo_gf2_rank32.restype = ctypes.c_uint
         L.xgo_batch_step.argtypes = [_vp, ctypes.c_uint, _vp]
         L.xgo_unsynchronized_batch.argtypes = [_vp, ctypes.c_uint, _vp]
         L.xgo_logical_buffer.argtypes = [_vp, _vp]
@@ -176,6 +179,13 @@ class OracleEnsemble:
             raise ValueError("samples per stream must be a multiple of 32")
         return out
 
+    def rank_counts(self, matrices: int) -> np.ndarray:
+        """(num_streams, 3) bins (rank 32, 31, <= 30) of the next `matrices`
+        32 x 32 matrices of every stream (tests.cpp:93-109)."""
+        out = np.empty((self.n, 3), dtype=np.uint64)
+        self.o.lib.xgo_ensemble_rank_counts(self.buf, self.n, matrices, _ptr(out), self.o.threads)
+        return out
+
     def checksums(self, n: int):
         x = np.empty(self.n, dtype=np.uint32)
         s = np.empty(self.n, dtype=np.uint64)
@@ -212,6 +222,27 @@ class Battery:
         self.lib = ctypes.CDLL(path)
         self.lib.xgref_battery_on_words.argtypes = [_vp, _u64, _int, ctypes.c_char_p,
                                                     ctypes.c_char_p, _u64]
+        self.lib.xgref_gf2_rank32.argtypes = [_vp]
+        self.lib.xgref_gf2_rank32.restype = ctypes.c_uint
+        self.lib.xgref_matrix_rank_on_words.argtypes = [_vp, _u64, _u64,
+                                                        ctypes.POINTER(ctypes.c_double),
+                                                        ctypes.POINTER(ctypes.c_double)]
+
+    def gf2_rank32(self, rows: np.ndarray) -> int:
+        """The reference's gf2_rank (proj/src/stattests/gf2.cpp) of 32 rows."""
+        r = np.ascontiguousarray(rows, dtype=np.uint32)
+        assert r.size == 32
+        return int(self.lib.xgref_gf2_rank32(_ptr(r)))
+
+    def matrix_rank(self, words: np.ndarray, num_matrices: int):
+        """The reference's matrix_rank_test (tests.cpp:81-126) over words:
+        (statistic, p_value)."""
+        w = np.ascontiguousarray(words, dtype=np.uint32).reshape(-1)
+        st, pv = ctypes.c_double(), ctypes.c_double()
+        if self.lib.xgref_matrix_rank_on_words(_ptr(w), w.size, num_matrices, ctypes.byref(st),
+                                               ctypes.byref(pv)):
+            raise ValueError("matrix_rank_test failed (buffer too short or < 38 matrices)")
+        return st.value, pv.value
 
     def run(self, words: np.ndarray, quick: bool = False, label: str = "gpu"):
         w = np.ascontiguousarray(words, dtype=np.uint32).reshape(-1)

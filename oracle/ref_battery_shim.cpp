@@ -8,9 +8,13 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "xg/stattests/battery.hpp"
+#include "xg/stattests/gf2.hpp"
+#include "xg/stattests/tests.hpp"
 #include "xg/stream.hpp"
 
 extern "C" {
@@ -40,6 +44,36 @@ int xgref_battery_on_words(const std::uint32_t* words, std::uint64_t n, int quic
             std::strncpy(json_out, e.what(), cap - 1);
             json_out[cap - 1] = 0;
         }
+        return -1;
+    }
+}
+
+// The reference's own rank (proj/src/stattests/gf2.cpp:37-45, single-word
+// rows) of one 32 x 32 matrix.
+unsigned xgref_gf2_rank32(const std::uint32_t* rows32) {
+    std::vector<std::uint64_t> rows(rows32, rows32 + 32);
+    return xg::stats::gf2_rank(rows, 32);
+}
+
+// The reference's matrix_rank_test (proj/src/stattests/tests.cpp:81-126)
+// over a word buffer through CallbackSource + BitSource; returns 0, or -1
+// when the buffer ran out / the test threw.
+int xgref_matrix_rank_on_words(const std::uint32_t* words, std::uint64_t n,
+                               std::uint64_t num_matrices, double* statistic, double* p_value) {
+    std::uint64_t pos = 0;
+    xg::CallbackSource src(
+        [&]() -> std::uint64_t {
+            if (pos >= n) throw std::runtime_error("word buffer exhausted");
+            return words[pos++];
+        },
+        32);
+    try {
+        xg::BitSource bits(src);
+        auto r = xg::stats::matrix_rank_test(bits, num_matrices, 32);
+        *statistic = r.statistic;
+        *p_value = r.p_value;
+        return 0;
+    } catch (const std::exception&) {
         return -1;
     }
 }

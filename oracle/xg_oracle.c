@@ -245,6 +245,31 @@ int xgo_mc_hit(uint32_t x, uint32_t y) {
     return q < (UINT64_C(1) << 62);
 }
 
+/* ---- GF(2) rank: proj/src/stattests/gf2.cpp:8-33 ------------------------- */
+
+/* Rank of a 32 x 32 GF(2) matrix given as 32 row words -- the reference's
+ * row-by-row elimination: each row is reduced by the established pivots
+ * (in the order they were found), then its lowest set column (bit index,
+ * gf2.cpp:24-29 scans col = 0 upwards) becomes a new pivot. */
+unsigned xgo_gf2_rank32(const uint32_t* rows_in) {
+    uint32_t rows[32];
+    unsigned pcol[32], prow[32], npiv = 0;
+    for (int i = 0; i < 32; ++i) rows[i] = rows_in[i];
+    for (unsigned i = 0; i < 32; ++i) {
+        for (unsigned k = 0; k < npiv; ++k)
+            if ((rows[i] >> pcol[k]) & 1u) rows[i] ^= rows[prow[k]];
+        for (unsigned col = 0; col < 32; ++col) {
+            if ((rows[i] >> col) & 1u) {
+                pcol[npiv] = col;
+                prow[npiv] = i;
+                ++npiv;
+                break;
+            }
+        }
+    }
+    return npiv;
+}
+
 /* ---- block ensemble: proj/src/parallel.cpp:84-135 ----------------------- */
 
 typedef struct {
@@ -260,7 +285,7 @@ typedef struct {
     uint32_t t, used;
 } job_t;
 
-enum { J_SEED, J_U32, J_F32, J_F64, J_MC, J_SUM, J_RAW, J_WORDS };
+enum { J_SEED, J_U32, J_F32, J_F64, J_MC, J_SUM, J_RAW, J_WORDS, J_RANK };
 
 static void run_one(job_t* j, uint32_t g) {
     xgo_state* st = &j->states[g];
@@ -311,6 +336,23 @@ static void run_one(job_t* j, uint32_t g) {
             hits += (uint64_t)xgo_mc_hit(x, y);
         }
         ((uint64_t*)j->out)[g] = hits;
+        break;
+    }
+    case J_RANK: {
+        /* matrix_rank_test's counting loop (proj/src/stattests/tests.cpp:93-109),
+         * M = 32: matrix k = the next 32 words, row i = word i (bits MSB first
+         * as BitSource reads them, proj/include/xg/stream.hpp:99-106, so the
+         * row value IS the word).  out = 3 bins per stream. */
+        uint64_t* o = (uint64_t*)j->out + (size_t)g * 3;
+        uint32_t rows[32];
+        o[0] = o[1] = o[2] = 0;
+        for (uint64_t k = 0; k < j->n; ++k) {
+            for (int i = 0; i < 32; ++i) rows[i] = (uint32_t)xgo_next_word(st);
+            unsigned r = xgo_gf2_rank32(rows);
+            if (r == 32) ++o[0];
+            else if (r == 31) ++o[1];
+            else ++o[2];
+        }
         break;
     }
     case J_SUM: {
@@ -419,6 +461,10 @@ int xgo_ensemble_mc_pi(xgo_state* states, uint32_t num_streams, uint64_t samples
                        uint64_t* hits_per_stream, int threads) {
     if (samples_per_stream % 32 != 0) return -1;
     return fill(J_MC, states, num_streams, samples_per_stream, hits_per_stream, NULL, threads);
+}
+int xgo_ensemble_rank_counts(xgo_state* states, uint32_t num_streams, uint64_t matrices_per_stream,
+                             uint64_t* counts3_per_stream, int threads) {
+    return fill(J_RANK, states, num_streams, matrices_per_stream, counts3_per_stream, NULL, threads);
 }
 int xgo_ensemble_checksums(xgo_state* states, uint32_t num_streams, uint64_t n,
                            uint32_t* xor_out, uint64_t* wsum_out, int threads) {

@@ -93,6 +93,11 @@ int xgo_ensemble_fill_f64(xgo_state* states, uint32_t num_streams, uint64_t per_
  * (a multiple of 32; sample m is the consecutive pair (w[2m], w[2m+1])). */
 int xgo_ensemble_mc_pi(xgo_state* states, uint32_t num_streams, uint64_t samples_per_stream,
                        uint64_t* hits_per_stream, int threads);
+/* Matrix-rank bins (rank 32, 31, <= 30) of the next matrices_per_stream
+ * 32 x 32 matrices of each stream (32 words each), 3 counts per stream. */
+int xgo_ensemble_rank_counts(xgo_state* states, uint32_t num_streams, uint64_t matrices_per_stream,
+                             uint64_t* counts3_per_stream, int threads);
+unsigned xgo_gf2_rank32(const uint32_t* rows);
 /* Per-stream checksums of the next n words (continuing): xor and
  * sum_k word_k*(k+1) mod 2^64. */
 int xgo_ensemble_checksums(xgo_state* states, uint32_t num_streams, uint64_t n,

@@ -64,6 +64,7 @@ SIGNATURES = {
     "xg_fill_raw_u32": (_int, [_vp, _u64, _vp, _vp]),
     "xg_fill_f64": (_int, [_vp, _u64, _vp, _vp]),
     "xg_mc_pi": (_int, [_vp, _u64, _vp, _vp]),
+    "xg_rank_test": (_int, [_vp, _u64, _vp, _vp]),
     "xg_skip": (_int, [_vp, _u64, _vp]),
     "xg_generate_host": (_int, [_vp, _u64, _vp, _vp]),
     "xg_generate_host_words": (_int, [_vp, _u64, _vp, _vp]),

@@ -289,7 +289,12 @@ int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t wor
         return XG_EUNSUPPORTED;
     }
     const int var = variant_for(MODE);
-    if (var == kPairs && h->kind != kRtJ2 && pair_aligned<MODE>(out, words)) {
+    if constexpr (MODE == kRank) {  // pair-lane kernel only (needs r - s < 64)
+        if (h->kind == kGP32) return launch_pair<MODE>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        if (h->kind == kRtJ1)
+            return launch_pair<MODE>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s);
+        return XG_EUNSUPPORTED;
+    } else if (var == kPairs && h->kind != kRtJ2 && pair_aligned<MODE>(out, words)) {
         if (h->kind == kGP32) return launch_pair<MODE>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         return launch_pair<MODE>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s);
     }
@@ -646,6 +651,29 @@ int xg_mc_pi(xg_ensemble_t h, uint64_t samples_per_stream, uint64_t* dev_hits,
         const uint64_t n = std::min(left, kChunk);
         rc = launch_fill<kMC>(h, 0, h->num_streams, 2 * n, nullptr,
                               reinterpret_cast<unsigned long long*>(dev_hits), s);
+        if (rc) return rc;
+        left -= n;
+    }
+    return XG_OK;
+}
+
+int xg_rank_test(xg_ensemble_t h, uint64_t matrices_per_stream, uint64_t* dev_counts,
+                 xg_stream_t stream) {
+    if (!h || !dev_counts || (reinterpret_cast<uintptr_t>(dev_counts) % 8) != 0) return XG_EINVAL;
+    if (h->kind == kGeneric || h->kind == kRtJ2) return XG_EUNSUPPORTED;
+    if (matrices_per_stream == 0) return XG_OK;
+    DeviceGuard dg(h->device);
+    if (!dg.ok) return XG_ECUDA;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = settle_next(h, s);
+    if (rc) return rc;
+    // Per-lane bin counters are 32-bit: bound matrices per stream and launch.
+    constexpr uint64_t kChunk = 1ull << 31;
+    uint64_t left = matrices_per_stream;
+    while (left) {
+        const uint64_t n = std::min(left, kChunk);
+        rc = launch_fill<kRank>(h, 0, h->num_streams, 32 * n, nullptr,
+                                reinterpret_cast<unsigned long long*>(dev_counts), s);
         if (rc) return rc;
         left -= n;
     }

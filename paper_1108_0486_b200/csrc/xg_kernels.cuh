@@ -80,7 +80,10 @@ struct HiMul {
 // and leaves the Weyl accumulator untouched.
 // kWide: each word zero-extended to uint64 -- the element type of the
 // reference's generate() result (proj/include/xg/parallel.hpp:46-47).
-enum Mode : int { kU32 = 0, kF32 = 1, kF64 = 2, kMC = 3, kSkip = 4, kRaw = 5, kWide = 6 };
+// kRank: fused GF(2) matrix-rank test (pair-lane kernel only): every 32
+// consecutive words are a 32 x 32 matrix, rows = words (bits MSB first, as the
+// reference's BitSource reads them), ranks binned {32, 31, <= 30}.
+enum Mode : int { kU32 = 0, kF32 = 1, kF64 = 2, kMC = 3, kSkip = 4, kRaw = 5, kWide = 6, kRank = 7 };
 
 template <bool HI>
 __device__ __forceinline__ uint32_t shr(uint32_t x, unsigned k, uint32_t mul) {

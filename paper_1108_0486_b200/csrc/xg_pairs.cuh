@@ -100,11 +100,71 @@ __device__ __forceinline__ uint32_t weyl_mix(uint32_t w, uint32_t v, const P& p)
     return (w ^ (w >> p.gamma)) + v;  // xorgens.hpp:58-62
 }
 
+// Ranks over GF(2) of the two 32 x 32 matrices of a double step (words
+// 0..31 and 32..63; row i = word i).  The 64 words are first transposed so
+// lane l holds row l of each matrix (four shuffles), then Gaussian
+// elimination runs column by column from the MSB, both matrices at once: a
+// ballot finds the rows with the column's bit set, the last of them is the
+// pivot and is broadcast, and every row with the bit set -- the pivot too,
+// which thereby becomes zero and drops out -- is reduced by it.  The rank is
+// the number of columns with a pivot.  Same rank as the row-by-row
+// elimination of proj/src/stattests/gf2.cpp:8-33.  (Getting the pivot value
+// with redux.sync.max instead of ballot + bfind + shuffle is 6 % slower;
+// profiles/README.md, r1zm.)
+__device__ __forceinline__ void rank_pair(uint2 v, unsigned& rank_a, unsigned& rank_b) {
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned half = lane >> 1;
+    const bool odd = lane & 1u;
+    const uint32_t ax = __shfl_sync(kFull, v.x, half), ay = __shfl_sync(kFull, v.y, half);
+    const uint32_t bx = __shfl_sync(kFull, v.x, 16u + half), by = __shfl_sync(kFull, v.y, 16u + half);
+    uint32_t ra = odd ? ay : ax;  // word l
+    uint32_t rb = odd ? by : bx;  // word 32 + l
+    unsigned za = 0, zb = 0;  // columns without a pivot
+#pragma unroll 8
+    for (int c = 31; c >= 0; --c) {
+        // One column of both matrices: the bit tests feed the ballots and
+        // predicate the row reductions (no selects); bfind picks the highest
+        // lane with the bit set as pivot (~0 if none, counted as no pivot).
+        asm("{\n\t"
+            ".reg .pred pa, pb;\n\t"
+            ".reg .u32 t, ma, mb, qa, qb, va, vb;\n\t"
+            "and.b32 t, %0, %4;\n\t"
+            "setp.ne.u32 pa, t, 0;\n\t"
+            "and.b32 t, %1, %4;\n\t"
+            "setp.ne.u32 pb, t, 0;\n\t"
+            "vote.sync.ballot.b32 ma, pa, 0xffffffff;\n\t"
+            "vote.sync.ballot.b32 mb, pb, 0xffffffff;\n\t"
+            "bfind.u32 qa, ma;\n\t"
+            "bfind.u32 qb, mb;\n\t"
+            "shfl.sync.idx.b32 va, %0, qa, 0x1f, 0xffffffff;\n\t"
+            "shfl.sync.idx.b32 vb, %1, qb, 0x1f, 0xffffffff;\n\t"
+            "@pa xor.b32 %0, %0, va;\n\t"
+            "@pb xor.b32 %1, %1, vb;\n\t"
+            "shr.u32 t, qa, 31;\n\t"
+            "add.u32 %2, %2, t;\n\t"
+            "shr.u32 t, qb, 31;\n\t"
+            "add.u32 %3, %3, t;\n\t"
+            "}"
+            : "+r"(ra), "+r"(rb), "+r"(za), "+r"(zb)
+            : "r"(1u << c));
+    }
+    const unsigned na = 32u - za, nb = 32u - zb;
+    rank_a = na;
+    rank_b = nb;
+}
+
+// Per-lane accumulators: MC hits, or the rank-test bins.
+struct RankAcc {
+    uint32_t full = 0, minus1 = 0, rest = 0;  // rank 32, 31, <= 30
+};
+template <int MODE>
+using AccT = std::conditional_t<MODE == kRank, RankAcc, uint32_t>;
+
 // Emit double step `j` (0 or 1) of a body (128 words).  o is the lane's output
 // cursor at the body start; `limit` (TAIL only) = values of this body wanted.
 template <int MODE, bool TAIL>
 __device__ __forceinline__ void pair_emit(uint2 v, void* o, int j, unsigned limit,
-                                          uint32_t& hits) {
+                                          AccT<MODE>& hits) {
     const unsigned lane = threadIdx.x & 31u;
     if constexpr (MODE == kU32 || MODE == kRaw) {
         if (!TAIL || 64u * j + 2u * lane < limit) __stcs(static_cast<uint2*>(o) + 32 * j, v);
@@ -118,6 +178,22 @@ __device__ __forceinline__ void pair_emit(uint2 v, void* o, int j, unsigned limi
         if (!TAIL || 32u * j + lane < limit) __stcs(static_cast<double*>(o) + 32 * j, raw_pair_to_f64(v.x, v.y));
     } else if constexpr (MODE == kMC) {
         if (!TAIL || 32u * j + lane < limit) hits += mc_hit(v.x, v.y);
+    } else if constexpr (MODE == kRank) {
+        // this double step holds matrices 2j and 2j+1 of the body
+        unsigned ra, rb;
+        rank_pair(v, ra, rb);
+        if (lane == 0u) {
+            if (!TAIL || 2u * j < limit) {
+                hits.full += ra == 32u;
+                hits.minus1 += ra == 31u;
+                hits.rest += ra < 31u;
+            }
+            if (!TAIL || 2u * j + 1u < limit) {
+                hits.full += rb == 32u;
+                hits.minus1 += rb == 31u;
+                hits.rest += rb < 31u;
+            }
+        }
     }
 }
 
@@ -133,7 +209,7 @@ __device__ __forceinline__ void* pair_advance(void* o) {  // one body
 // One body = two double steps = 128 words; (A, B) := (N0, N1).
 template <int MODE, bool TAIL, class P>
 __device__ __forceinline__ void pair_body(uint2& A, uint2& B, const P& p, const PairLane& pl,
-                                          uint32_t& wl, uint32_t w64, void* o, uint32_t& hits,
+                                          uint32_t& wl, uint32_t w64, void* o, AccT<MODE>& hits,
                                           unsigned limit) {
     constexpr bool kW = MODE != kRaw;
     constexpr int kGive = MODE == kF32 ? 1 : 0;
@@ -161,7 +237,7 @@ __device__ __forceinline__ void pair_body(uint2& A, uint2& B, const P& p, const 
 // stream's state (same contract as fill_kernel in xg_kernels.cuh).
 // Requirements checked by the host: u32/f32/raw rows 8-byte aligned (even
 // `words`), u64 rows 16-byte aligned, f64 `words` even, MC `words` a
-// multiple of 64.
+// multiple of 64, rank `words` a multiple of 32.
 // CTAs of 1..32 warps (one stream each).  GP32 fits 32 registers (64 warps
 // per SM); the runtime-parameter sets (CTAs of <= 8 warps) keep their extra
 // shift registers rather than spill.
@@ -191,7 +267,7 @@ pair_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32
         o = static_cast<unsigned long long*>(out) + static_cast<uint64_t>(gl) * words + 2u * lane;
     else if constexpr (MODE == kF64)
         o = static_cast<double*>(out) + static_cast<uint64_t>(gl) * (words >> 1) + lane;
-    uint32_t hits = 0;
+    AccT<MODE> hits{};
 
     uint64_t left = words >> 7;  // bodies of 128 words
     while (left != 0) {
@@ -220,7 +296,7 @@ pair_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32
         // saved window ends exactly at word `words`: positions tail..tail+127
         // of (old window, new 128 words).
         const uint2 OA = A, OB = B;
-        const unsigned lim = (MODE == kF64 || MODE == kMC) ? tail >> 1 : tail;
+        const unsigned lim = (MODE == kF64 || MODE == kMC) ? tail >> 1 : (MODE == kRank ? tail >> 5 : tail);
         pair_body<MODE, true>(A, B, p, pl, wl, w64, o, hits, lim);
         const uint32_t v[8] = {OA.x, OA.y, OB.x, OB.y, A.x, A.y, B.x, B.y};
 #pragma unroll
@@ -239,6 +315,14 @@ pair_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32
 #pragma unroll
         for (int s = 16; s > 0; s >>= 1) t += __shfl_xor_sync(kFull, t, s);
         if (lane == 0 && t != 0) atomicAdd(hits_out, t);
+    } else if constexpr (MODE == kRank) {
+        // lane 0 holds the counts; hits_out[0..2] = rank 32, 31, <= 30
+        const uint32_t f = hits.full, m = hits.minus1, r = hits.rest;
+        if (lane == 0) {
+            if (f) atomicAdd(hits_out, static_cast<unsigned long long>(f));
+            if (m) atomicAdd(hits_out + 1, static_cast<unsigned long long>(m));
+            if (r) atomicAdd(hits_out + 2, static_cast<unsigned long long>(r));
+        }
     }
 }
 

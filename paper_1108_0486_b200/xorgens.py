@@ -26,6 +26,7 @@ libxg_gpu.so kernels; there is no CPU path.
 from __future__ import annotations
 
 import ctypes
+import math
 import enum
 from dataclasses import dataclass
 from typing import List, Optional, Sequence, Tuple
@@ -41,7 +42,8 @@ __all__ = [
     "recommended_weyl_increment", "default_output_shift", "period_description",
     "PeriodDescription", "xorgensgp32_params", "tiny_r2w8_params", "tiny_r2w16_params",
     "tiny_r4w16_params", "gpu_supported", "fast_path", "XorgensState", "seed_state", "batch_step",
-    "BlockEnsemble", "XorgensSource", "partition", "kernel_launches",
+    "BlockEnsemble", "XorgensSource", "partition", "kernel_launches", "matrix_rank_statistic",
+    "RANK_P32",
 ]
 
 
@@ -235,6 +237,25 @@ class _Handle:
             self.ptr = ctypes.c_void_p()
 
 
+# Random 32 x 32 GF(2) matrix: P(rank 32), P(rank 31), P(rank <= 30)
+# (proj/src/stattests/tests.cpp:89-91).
+RANK_P32 = (0.288788095153841, 0.577576190173205, 0.133635714672954)
+
+
+def matrix_rank_statistic(counts) -> Tuple[float, float]:
+    """(chi-square statistic, p-value) of rank-test bins, computed as
+    proj/src/stattests/tests.cpp:111-123: chi2 over the three bins, p the
+    chi-square survival function with 2 degrees of freedom (= exp(-chi2/2))."""
+    c = [float(int(v)) for v in (counts.tolist() if hasattr(counts, "tolist") else counts)][:3]
+    nm = sum(c)
+    chi2 = 0.0
+    for i in range(3):
+        e = nm * RANK_P32[i]
+        d = c[i] - e
+        chi2 += d * d / e
+    return chi2, math.exp(-chi2 / 2.0)
+
+
 class BlockEnsemble:
     """``xg::BlockEnsemble`` on one GPU (proj/src/parallel.cpp:84-135).
 
@@ -387,6 +408,22 @@ class BlockEnsemble:
         _raise(lib.xg_mc_pi(self._h.ptr, samples_per_block, ctypes.c_void_p(hits.data_ptr()),
                             self._stream(stream)))
         return hits
+
+    def rank_test(self, matrices_per_block: int, counts=None, stream=None):
+        """Fused GF(2) matrix-rank test (the reference's matrix_rank_test,
+        proj/src/stattests/tests.cpp:81-126, M = 32) over the next
+        32*matrices_per_block words of every block: adds the (rank 32, 31,
+        <= 30) bins to ``counts`` (a 3-element int64 CUDA tensor, created
+        zeroed if None) and returns it.  ``matrix_rank_statistic(counts)``
+        gives the chi-square statistic and p-value."""
+        torch = _torch()
+        if counts is None:
+            counts = torch.zeros(3, dtype=torch.int64, device=f"cuda:{self._h.device}")
+        if counts.numel() < 3 or counts.element_size() != 8 or not counts.is_cuda:
+            raise ValueError("counts must be a CUDA tensor of at least 3 int64")
+        _raise(lib.xg_rank_test(self._h.ptr, matrices_per_block, ctypes.c_void_p(counts.data_ptr()),
+                                self._stream(stream)))
+        return counts
 
     def skip(self, words: int, stream=None) -> None:
         _raise(lib.xg_skip(self._h.ptr, words, self._stream(stream)))

@@ -538,3 +538,57 @@ def test_generic_params_vs_oracle_and_reference(oracle, reference, name, ps):
     assert np.array_equal(np.array(got, dtype=np.uint64), ref)
     with pytest.raises(xg.UnsupportedParamsError):
         e.mc_pi(32)
+
+
+@pytest.mark.parametrize("streams", [1, 5, 33])
+@pytest.mark.parametrize("matrices", [1, 2, 3, 5, 38, 101])
+def test_rank_test_counts_vs_oracle(oracle, streams, matrices):
+    """Fused matrix-rank bins (xg_rank_test) equal the oracle's counting loop
+    (tests.cpp:93-109) on the same streams, from ragged positions, and the
+    streams continue exactly afterwards."""
+    base = 9000 + streams * 100 + matrices
+    e = xg.BlockEnsemble(GP32, base, streams, 63)
+    o = oracle.ensemble(base, streams)
+    e.fill_u32(17)
+    o.fill_u32(17)
+    got = np_u32(e.rank_test(matrices)).astype(np.uint64)
+    assert np.array_equal(got, o.rank_counts(matrices).sum(axis=0))
+    assert np.array_equal(np_u32(e.fill_u32(40)), o.fill_u32(40))
+
+
+def test_rank_test_runtime_params_and_unsupported(oracle):
+    p1 = xg.GeneratorParams(128, 95, 17, 12, 13, 15, 32, 2654435769, 16)  # J = 1: pair kernel
+    e = xg.BlockEnsemble(p1, 3, 9, 32)
+    o = oracle.ensemble(3, 9, oracle.params(128, 95, 17, 12, 13, 15, 32, 2654435769, 16))
+    assert np.array_equal(np_u32(e.rank_test(77)).astype(np.uint64), o.rank_counts(77).sum(axis=0))
+    p2 = xg.GeneratorParams(128, 33, 11, 7, 9, 19, 32, 0x6A09E667 | 1, 11)  # J = 2
+    with pytest.raises(Exception):
+        xg.BlockEnsemble(p2, 3, 2, 32).rank_test(4)
+    with pytest.raises(Exception):
+        xg.BlockEnsemble(xg.tiny_r4w16_params(), 3, 2, 1).rank_test(4)
+
+
+def test_rank_test_statistic_equals_reference_on_gpu_words():
+    """The statistic from the GPU bins equals the reference's own
+    matrix_rank_test run over the same GPU-generated words."""
+    from oracle import Battery
+    try:
+        b = Battery()
+    except FileNotFoundError as ex:  # pragma: no cover
+        pytest.skip(str(ex))
+    m = 5000
+    words = np_u32(xg.BlockEnsemble(GP32, 77, 1, 63).fill_u32(32 * m))[0]
+    counts = xg.BlockEnsemble(GP32, 77, 1, 63).rank_test(m)
+    chi2, p = xg.matrix_rank_statistic(counts)
+    rchi2, rp = b.matrix_rank(words, m)
+    assert chi2 == rchi2 and abs(p - rp) <= 1e-12 * max(1.0, rp)
+
+
+def test_rank_test_large_ensemble():
+    """2^14 streams x 2^10 matrices (2^29 words): bins sum to the matrix count
+    and the reference statistic is unremarkable."""
+    P, m = 1 << 14, 1 << 10
+    c = np_u32(xg.BlockEnsemble(GP32, 1, P, 63).rank_test(m))
+    assert int(c.sum()) == P * m
+    chi2, p = xg.matrix_rank_statistic(c)
+    assert 1e-6 < p <= 1.0, (c, chi2, p)

@@ -281,3 +281,57 @@ def test_pair_lane_schedule_equals_serial(oracle, s):
         got.append(N.reshape(-1))  # lane l's pair = words 2l, 2l+1 of the step
         A, B = B, N
     assert np.array_equal(np.concatenate(got), want)
+
+
+def _battery_or_skip():
+    from oracle import Battery
+    try:
+        return Battery()
+    except FileNotFoundError as e:  # pragma: no cover - needs the reference tree
+        pytest.skip(str(e))
+
+
+def test_gf2_rank32_matches_reference():
+    """The oracle's 32 x 32 GF(2) rank against the reference's own gf2_rank
+    (proj/src/stattests/gf2.cpp, compiled into oracle/_ref) on random,
+    duplicated-row, low-rank and zero matrices."""
+    from oracle import Oracle
+    o, b = Oracle(), _battery_or_skip()
+    rng = np.random.default_rng(11)
+    for t in range(3000):
+        rows = rng.integers(0, 2**32, size=32, dtype=np.uint64).astype(np.uint32)
+        kind = t % 6
+        if kind == 1:
+            rows[rng.integers(0, 32)] = rows[rng.integers(0, 32)]
+        elif kind == 2:
+            rows &= np.uint32(0xFFFF0000)
+        elif kind == 3:
+            basis = rows[:int(rng.integers(1, 32))]
+            rows = np.array([np.bitwise_xor.reduce(basis[rng.integers(0, 2, size=basis.size) == 1])
+                             if basis.size else 0 for _ in range(32)], dtype=np.uint32)
+        elif kind == 4:
+            rows[:] = 0
+        elif kind == 5:
+            rows = (np.uint32(1) << np.arange(32, dtype=np.uint32)).astype(np.uint32)
+        want = b.gf2_rank32(rows)
+        assert int(o.lib.xgo_gf2_rank32(rows.ctypes.data)) == want, t
+    assert b.gf2_rank32(np.zeros(32, dtype=np.uint32)) == 0
+
+
+def test_rank_counts_give_the_reference_statistic():
+    """Bins from the oracle's counting loop, turned into the statistic by the
+    Python mirror's matrix_rank_statistic, equal the reference's
+    matrix_rank_test (proj/src/stattests/tests.cpp:81-126) on the same words:
+    chi-square bit for bit, p-value to 1e-12."""
+    import paper_1108_0486_b200 as xg
+    from oracle import Oracle
+    b = _battery_or_skip()
+    o = Oracle()
+    for seed, m in ((1, 38), (42, 1000), (7, 4321)):
+        words = o.ensemble(seed, 1).fill_u32(32 * m)[0]
+        counts = o.ensemble(seed, 1).rank_counts(m)[0]
+        assert int(counts.sum()) == m
+        chi2, p = xg.matrix_rank_statistic(counts)
+        rchi2, rp = b.matrix_rank(words, m)
+        assert chi2 == rchi2
+        assert abs(p - rp) <= 1e-12 * max(1.0, rp)
