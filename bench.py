@@ -283,6 +283,9 @@ def workload_geometry(wl: str, world: int, rank: int):
     if wl == "rank":  # fused GF(2) matrix-rank test: 2^14 streams x 2^12 32x32 matrices per GPU
         P = 1 << 14
         return rank * P, P, 1 << 12, "weak", (P << 17) * world
+    if wl == "lc":  # linear complexity test: 2^14 streams x 256 blocks of 1000 bits per GPU
+        P = 1 << 14
+        return rank * P, P, 256, "weak", P * 256 * 1000 // 32 * world
     if wl == "stream1":  # config 1 on the GPU: ONE stream (seed 1 + rank), 10^8 words
         return rank, 1, 10**8, "weak", 10**8 * world
     if wl == "fill_2p34":
@@ -295,9 +298,11 @@ def workload_geometry(wl: str, world: int, rank: int):
     raise ValueError(wl)
 
 
-def timed_loop(fn, stream, steps, warmup, world):
+def timed_loop(fn, stream, steps, warmup, world, counter=None):
     """W warm-ups, then K timed steps bracketed by barrier + synchronize;
-    per-step CUDA events on the launching stream.  Returns (total_ms, [step_ms])."""
+    per-step CUDA events on the launching stream.  Returns (total_ms,
+    [step_ms], launches): `counter()` (our kernel-launch count) read around
+    the timed steps only."""
     import torch
 
     for _ in range(warmup):
@@ -305,6 +310,7 @@ def timed_loop(fn, stream, steps, warmup, world):
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
+    c0 = counter() if counter else 0
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps)]
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
@@ -316,9 +322,10 @@ def timed_loop(fn, stream, steps, warmup, world):
     end.record(stream)
     torch.cuda.synchronize()
     barrier(world)
+    launches = (counter() - c0) if counter else 0
     step_ms = [evs[2 * i].elapsed_time(evs[2 * i + 1]) for i in range(steps)]
     total = start.elapsed_time(end)
-    return total, step_ms
+    return total, step_ms, launches
 
 
 def main():
@@ -331,7 +338,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="fill_u32",
                     choices=["fill_u32", "fill_f32", "fill_f64", "fill_2p34", "mc_pi", "skip", "stream1",
-                             "rank"])
+                             "rank", "lc"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -360,8 +367,8 @@ def main():
 
     out = None
     bytes_per_val = {"fill_u32": 4, "fill_f32": 4, "fill_f64": 8, "fill_2p34": 4, "mc_pi": 0,
-                     "skip": 0, "stream1": 4, "rank": 0}[wl]
-    words_per_val = 2 if wl in ("fill_f64", "mc_pi") else (32 if wl == "rank" else 1)
+                     "skip": 0, "stream1": 4, "rank": 0, "lc": 0}[wl]
+    words_per_val = {"fill_f64": 2, "mc_pi": 2, "rank": 32, "lc": 1000 / 32}.get(wl, 1)
     if wl in ("fill_u32", "fill_2p34", "stream1"):
         out = torch.empty((count, per), dtype=torch.uint32, device="cuda")
         fn = lambda: ens.fill_u32(per, out=out)  # noqa: E731
@@ -374,6 +381,9 @@ def main():
     elif wl == "skip":  # generator core only (no stores): the integer-issue ceiling
         hits = None
         fn = lambda: ens.skip(per)  # noqa: E731
+    elif wl == "lc":  # linear complexity test: words to a buffer, Berlekamp-Massey per block
+        hits = torch.zeros(1001, dtype=torch.int64, device="cuda")
+        fn = lambda: ens.linear_complexity_test(1000, per, hist=hits)  # noqa: E731
     elif wl == "rank":  # fused matrix-rank test: bins only, no HBM traffic
         hits = torch.zeros(3, dtype=torch.int64, device="cuda")
         fn = lambda: ens.rank_test(per, counts=hits)  # noqa: E731
@@ -383,10 +393,9 @@ def main():
 
     vals_per_step = count * per
     words_per_step = vals_per_step * words_per_val
-    launches0 = xg.kernel_launches()
     with ClockSampler(local) as clk:
-        total_ms, step_ms = timed_loop(fn, stream, args.steps, args.warmup, world)
-    launches = xg.kernel_launches() - launches0 - args.warmup * (1 if wl != "mc_pi" else 1)
+        total_ms, step_ms, launches = timed_loop(fn, stream, args.steps, args.warmup, world,
+                                                 counter=xg.kernel_launches)
     t_max = max_over_ranks(total_ms, world)
     value = job_words_per_step * args.steps / (t_max / 1e3)
     kern_ms = statistics.mean(step_ms)
@@ -409,7 +418,9 @@ def main():
             "skip": "generator core only (advance 2^30 words, no stores)",
             "stream1": "one stream per GPU (BASELINE config 1: seed 1, 10^8 uint32), one warp",
             "rank": "fused GF(2) 32x32 matrix-rank test (reference matrix_rank_test), "
-                    "2^14 streams x 2^12 matrices per GPU"}[wl],
+                    "2^14 streams x 2^12 matrices per GPU",
+            "lc": "linear complexity test (reference linear_complexity_test, K = 1000), "
+                  "2^14 streams x 256 blocks per GPU"}[wl],
             "params": "xorgensgp32 (128,65,15,14,12,17) w=32", "base_seed": 1,
             "streams_per_gpu": count, "values_per_stream": per,
             "layout": "block-major out[g*per_stream+k]",
@@ -437,6 +448,19 @@ def main():
                 result["roofline"]["write_only_probe_gbs"] = write_probe_gbs(out, stream)
             except OSError:
                 pass
+    elif wl == "lc":
+        import paper_1108_0486_b200 as xg_
+
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(hits)
+        chi2, pv = xg_.linear_complexity_statistic(hits, 1000)
+        result["lc"] = {"blocks": int(hits.sum().item()), "chi2": chi2, "p_value": pv,
+                        "blocks_per_s": value / (1000 / 32), "kernel_ms_mean": kern_ms}
+        result["roofline"] = {"bound": "int-issue (Berlekamp-Massey, one warp per block)",
+                              "achieved": value / world, "peak": None, "unit": "RN/s per GPU",
+                              "frac": None, "traffic": None}
     elif wl == "rank":
         import paper_1108_0486_b200 as xg_
 
@@ -501,6 +525,22 @@ def main():
                          "api": "BlockEnsemble.generate -> xg_generate_host (pinned host buffer)",
                          "steps": e2e_steps}
         del host
+    if rank == 0 and world == 1 and not args.no_cpu and wl == "lc":
+        try:
+            from oracle import Battery, Oracle
+
+            nb = 3000  # bounded sample: 3e6 bits through the reference's own test
+            words = Oracle().ensemble(1, 1).fill_u32(nb * 1000 // 32)[0]
+            t0 = time.perf_counter()
+            Battery().linear_complexity(words, 1000, nb)
+            dt = time.perf_counter() - t0
+            result["cpu_baseline"] = {
+                "value": nb * 1000 / 32 / dt, "unit": "RN/s", "cores": 1, "kind": "reference",
+                "sample": f"reference linear_complexity_test (proj/src/stattests/tests.cpp:128-178), "
+                          f"{nb} blocks of 1000 bits of one stream, 1 thread (serial in the reference)",
+                "blocks_per_s": nb / dt}
+        except Exception as e:  # noqa: BLE001
+            result["cpu_baseline"] = {"value": None, "unavailable": str(e)}
     if rank == 0 and world == 1 and not args.no_cpu and wl == "rank":
         try:
             from oracle import Battery, Oracle

@@ -162,6 +162,18 @@ int xg_mc_pi(xg_ensemble_t h, uint64_t samples_per_stream, uint64_t* dev_hits,
  * counting loop; rank: proj/src/stattests/gf2.cpp:8-33). */
 int xg_rank_test(xg_ensemble_t h, uint64_t matrices_per_stream, uint64_t* dev_counts,
                  xg_stream_t stream);
+
+/* Linear complexity test (the reference's linear_complexity_test,
+ * proj/src/stattests/tests.cpp:128-178): each stream supplies
+ * ceil(block_length * blocks_per_stream / 32) words continuing its stream,
+ * read as a BitSource reads them (MSB first), cut into blocks of block_length
+ * bits; the Berlekamp-Massey linear complexity L of every block
+ * (proj/src/stattests/gf2.cpp:62-110) is histogrammed: dev_hist[L] += 1
+ * (device uint64[block_length + 1]).  The reference's bins, chi-square and
+ * p-value follow on the host from the histogram.  1 <= block_length <= 1023
+ * (XG_EINVAL otherwise); w = 32 sets (XG_EUNSUPPORTED otherwise). */
+int xg_linear_complexity_test(xg_ensemble_t h, unsigned block_length, uint64_t blocks_per_stream,
+                              uint64_t* dev_hist, xg_stream_t stream);
 /* Advance every stream by `words` without storing (discard). */
 int xg_skip(xg_ensemble_t h, uint64_t words, xg_stream_t stream);
 

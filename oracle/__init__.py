@@ -224,9 +224,38 @@ class Battery:
                                                     ctypes.c_char_p, _u64]
         self.lib.xgref_gf2_rank32.argtypes = [_vp]
         self.lib.xgref_gf2_rank32.restype = ctypes.c_uint
+        self.lib.xgref_berlekamp_massey.argtypes = [_vp, _u64]
+        self.lib.xgref_berlekamp_massey.restype = _u64
+        self.lib.xgref_linear_complexity_on_words.argtypes = [
+            _vp, _u64, ctypes.c_uint, _u64, ctypes.POINTER(ctypes.c_double),
+            ctypes.POINTER(ctypes.c_double)]
         self.lib.xgref_matrix_rank_on_words.argtypes = [_vp, _u64, _u64,
                                                         ctypes.POINTER(ctypes.c_double),
                                                         ctypes.POINTER(ctypes.c_double)]
+
+    def berlekamp_massey(self, bits: np.ndarray) -> int:
+        """The reference's linear complexity of a bit sequence (gf2.cpp:62-110)."""
+        b = np.ascontiguousarray(bits, dtype=np.uint8)
+        return int(self.lib.xgref_berlekamp_massey(_ptr(b), b.size))
+
+    def lc_histogram(self, words: np.ndarray, block_length: int, num_blocks: int) -> np.ndarray:
+        """Histogram of the reference's per-block linear complexity over
+        words read MSB first (BitSource), block_length bits per block."""
+        w = np.ascontiguousarray(words, dtype=np.uint32).reshape(-1)
+        bits = np.unpackbits(w.byteswap().view(np.uint8))  # MSB first per word
+        hist = np.zeros(block_length + 1, dtype=np.uint64)
+        for k in range(num_blocks):
+            hist[self.berlekamp_massey(bits[k * block_length:(k + 1) * block_length])] += 1
+        return hist
+
+    def linear_complexity(self, words: np.ndarray, block_length: int, num_blocks: int):
+        """The reference's linear_complexity_test over words: (statistic, p)."""
+        w = np.ascontiguousarray(words, dtype=np.uint32).reshape(-1)
+        st, pv = ctypes.c_double(), ctypes.c_double()
+        if self.lib.xgref_linear_complexity_on_words(_ptr(w), w.size, block_length, num_blocks,
+                                                     ctypes.byref(st), ctypes.byref(pv)):
+            raise ValueError("linear_complexity_test failed (short buffer, K < 128 or < 38 blocks)")
+        return st.value, pv.value
 
     def gf2_rank32(self, rows: np.ndarray) -> int:
         """The reference's gf2_rank (proj/src/stattests/gf2.cpp) of 32 rows."""

@@ -78,4 +78,34 @@ int xgref_matrix_rank_on_words(const std::uint32_t* words, std::uint64_t n,
     }
 }
 
+// The reference's Berlekamp-Massey (proj/src/stattests/gf2.cpp:62-110) of n
+// bits (one byte per bit).
+std::uint64_t xgref_berlekamp_massey(const std::uint8_t* bits, std::uint64_t n) {
+    std::vector<std::uint8_t> v(bits, bits + n);
+    return xg::stats::berlekamp_massey(v);
+}
+
+// The reference's linear_complexity_test (proj/src/stattests/tests.cpp:128-178)
+// over a word buffer; returns 0, or -1 when the buffer ran out / it threw.
+int xgref_linear_complexity_on_words(const std::uint32_t* words, std::uint64_t n,
+                                     unsigned block_length, std::uint64_t num_blocks,
+                                     double* statistic, double* p_value) {
+    std::uint64_t pos = 0;
+    xg::CallbackSource src(
+        [&]() -> std::uint64_t {
+            if (pos >= n) throw std::runtime_error("word buffer exhausted");
+            return words[pos++];
+        },
+        32);
+    try {
+        xg::BitSource bits(src);
+        auto r = xg::stats::linear_complexity_test(bits, block_length, num_blocks);
+        *statistic = r.statistic;
+        *p_value = r.p_value;
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 }  // extern "C"

@@ -21,6 +21,7 @@
 #include "xg_generic.cuh"
 #include "xg_kernels.cuh"
 #include "xg_pairs.cuh"
+#include "xg_stattests.cuh"
 
 using namespace xgk;
 
@@ -71,6 +72,9 @@ struct xg_ensemble {
     // xg_generate_host staging
     void* d_stage = nullptr;
     size_t stage_words = 0;  // bytes
+    // xg_linear_complexity_test word buffer
+    uint32_t* d_lc = nullptr;
+    size_t lc_bytes = 0;
 };
 
 namespace {
@@ -371,6 +375,7 @@ void free_handle(xg_ensemble* h) {
         cudaFree(h->d_snap);
         cudaFree(h->d_scratch);
         cudaFree(h->d_stage);
+        cudaFree(h->d_lc);
     }
     delete h;
 }
@@ -676,6 +681,50 @@ int xg_rank_test(xg_ensemble_t h, uint64_t matrices_per_stream, uint64_t* dev_co
                                 reinterpret_cast<unsigned long long*>(dev_counts), s);
         if (rc) return rc;
         left -= n;
+    }
+    return XG_OK;
+}
+
+int xg_linear_complexity_test(xg_ensemble_t h, unsigned block_length, uint64_t blocks_per_stream,
+                              uint64_t* dev_hist, xg_stream_t stream) {
+    if (!h || !dev_hist || (reinterpret_cast<uintptr_t>(dev_hist) % 8) != 0) return XG_EINVAL;
+    if (block_length == 0 || block_length > kLcMaxK) return XG_EINVAL;
+    if (h->params.w != 32) return XG_EUNSUPPORTED;  // BitSource reads w bits per word
+    if (blocks_per_stream == 0) return XG_OK;
+    DeviceGuard dg(h->device);
+    if (!dg.ok) return XG_ECUDA;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = settle_next(h, s);
+    if (rc) return rc;
+    const uint64_t P = h->num_streams, K = block_length;
+    // Chunks of whole words: 32 blocks are exactly K words.  Aim at <= 2^26
+    // buffered words; only the last chunk may end inside a word, whose
+    // remaining bits are dropped as a fresh BitSource drops them.
+    const uint64_t per32 = std::max<uint64_t>(1, (1ull << 26) / std::max<uint64_t>(1, P * K));
+    const uint64_t bc = std::min<uint64_t>(32 * per32, 1ull << 31);
+    uint64_t left = blocks_per_stream;
+    while (left) {
+        const uint64_t nb = std::min(left, bc);
+        const uint64_t wc = (nb * K + 31) / 32;
+        const size_t need = static_cast<size_t>(P * wc) * sizeof(uint32_t);
+        if (h->lc_bytes < need) {
+            cudaFree(h->d_lc);
+            h->d_lc = nullptr;
+            h->lc_bytes = 0;
+            rc = cuda_rc(cudaMalloc(&h->d_lc, need));
+            if (rc) return rc;
+            h->lc_bytes = need;
+        }
+        rc = launch_fill<kU32>(h, 0, h->num_streams, wc, h->d_lc, nullptr, s);
+        if (rc) return rc;
+        const uint64_t warps = P * nb;
+        lc_kernel<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, s>>>(
+            h->d_lc, h->num_streams, wc, block_length, static_cast<uint32_t>(nb),
+            reinterpret_cast<unsigned long long*>(dev_hist));
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        rc = cuda_rc(cudaGetLastError());
+        if (rc) return rc;
+        left -= nb;
     }
     return XG_OK;
 }

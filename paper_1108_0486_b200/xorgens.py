@@ -43,7 +43,7 @@ __all__ = [
     "PeriodDescription", "xorgensgp32_params", "tiny_r2w8_params", "tiny_r2w16_params",
     "tiny_r4w16_params", "gpu_supported", "fast_path", "XorgensState", "seed_state", "batch_step",
     "BlockEnsemble", "XorgensSource", "partition", "kernel_launches", "matrix_rank_statistic",
-    "RANK_P32",
+    "RANK_P32", "linear_complexity_statistic", "LC_PI",
 ]
 
 
@@ -256,6 +256,56 @@ def matrix_rank_statistic(counts) -> Tuple[float, float]:
     return chi2, math.exp(-chi2 / 2.0)
 
 
+# Linear complexity test bins (proj/src/stattests/tests.cpp:140-141).
+LC_PI = (0.010417, 0.03125, 0.125, 0.5, 0.25, 0.0625, 0.020833)
+
+
+def _regularized_gamma_q_int(a: int, x: float) -> float:
+    """Q(a, x) for integer a: exp(-x) * sum_{k<a} x^k / k!."""
+    term, total = 1.0, 1.0
+    for k in range(1, a):
+        term *= x / k
+        total += term
+    return math.exp(-x) * total
+
+
+def linear_complexity_statistic(hist, block_length: int) -> Tuple[float, float]:
+    """(chi-square statistic, p-value) from a histogram of per-block linear
+    complexities, binned exactly as proj/src/stattests/tests.cpp:135-172
+    (mu, the sign, T = sign * (L - mu) + 2/9, seven bins; p = chi-square
+    survival with 6 degrees of freedom)."""
+    h = [int(v) for v in (hist.tolist() if hasattr(hist, "tolist") else hist)]
+    k = float(block_length)
+    sign = 1.0 if block_length % 2 == 0 else -1.0
+    mu = k / 2.0 + (9.0 - sign) / 36.0 - (k / 3.0 + 2.0 / 9.0) / math.pow(2.0, 1000.0 if k > 1000 else k)
+    counts = [0] * 7
+    for L, c in enumerate(h):
+        if not c:
+            continue
+        t = sign * (float(L) - mu) + 2.0 / 9.0
+        if t <= -2.5:
+            b = 0
+        elif t <= -1.5:
+            b = 1
+        elif t <= -0.5:
+            b = 2
+        elif t <= 0.5:
+            b = 3
+        elif t <= 1.5:
+            b = 4
+        elif t <= 2.5:
+            b = 5
+        else:
+            b = 6
+        counts[b] += c
+    nb = float(sum(counts))
+    chi2 = 0.0
+    for i in range(7):
+        diff = float(counts[i]) - nb * LC_PI[i]
+        chi2 += diff * diff / (nb * LC_PI[i])
+    return chi2, _regularized_gamma_q_int(3, chi2 / 2.0)
+
+
 class BlockEnsemble:
     """``xg::BlockEnsemble`` on one GPU (proj/src/parallel.cpp:84-135).
 
@@ -424,6 +474,27 @@ class BlockEnsemble:
         _raise(lib.xg_rank_test(self._h.ptr, matrices_per_block, ctypes.c_void_p(counts.data_ptr()),
                                 self._stream(stream)))
         return counts
+
+    def linear_complexity_test(self, block_length: int, blocks_per_block: int, hist=None,
+                               stream=None):
+        """Linear complexity test (the reference's linear_complexity_test,
+        proj/src/stattests/tests.cpp:128-178) on the GPU: the next
+        ceil(block_length * blocks_per_block / 32) words of every block, read
+        MSB first, in blocks of block_length bits; adds the histogram of the
+        Berlekamp-Massey complexities to ``hist`` (an int64 CUDA tensor of
+        block_length + 1 entries, created zeroed if None) and returns it.
+        ``linear_complexity_statistic(hist, block_length)`` gives the
+        reference's chi-square statistic and p-value."""
+        torch = _torch()
+        if hist is None:
+            hist = torch.zeros(block_length + 1, dtype=torch.int64,
+                               device=f"cuda:{self._h.device}")
+        if hist.numel() < block_length + 1 or hist.element_size() != 8 or not hist.is_cuda:
+            raise ValueError("hist must be a CUDA tensor of block_length + 1 int64")
+        _raise(lib.xg_linear_complexity_test(self._h.ptr, block_length, blocks_per_block,
+                                             ctypes.c_void_p(hist.data_ptr()),
+                                             self._stream(stream)))
+        return hist
 
     def skip(self, words: int, stream=None) -> None:
         _raise(lib.xg_skip(self._h.ptr, words, self._stream(stream)))

@@ -16,6 +16,7 @@ for w in fill_f32 fill_f64 skip; do
 done
 timeout 600 python bench.py --workload mc_pi --steps 5 --warmup 3 --no-cpu > $OUT/bench_mc_pi.json 2>> $OUT/bench.err
 timeout 600 python bench.py --workload rank --steps 10 --warmup 3 > $OUT/bench_rank.json 2>> $OUT/bench.err
+timeout 600 python bench.py --workload lc --steps 5 --warmup 3 > $OUT/bench_lc.json 2>> $OUT/bench.err
 timeout 600 python bench.py --workload stream1 --steps 5 --warmup 3 --no-e2e > $OUT/bench_stream1.json 2>> $OUT/bench.err
 timeout 900 python bench.py --workload fill_2p34 --steps 10 --warmup 3 --no-cpu --no-e2e > $OUT/bench_fill_2p34.json 2>> $OUT/bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \

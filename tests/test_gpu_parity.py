@@ -592,3 +592,57 @@ def test_rank_test_large_ensemble():
     assert int(c.sum()) == P * m
     chi2, p = xg.matrix_rank_statistic(c)
     assert 1e-6 < p <= 1.0, (c, chi2, p)
+
+
+@pytest.mark.parametrize("K,nb", [(1, 50), (7, 65), (31, 33), (32, 40), (33, 97), (100, 64),
+                                  (500, 70), (1000, 45), (1023, 38)])
+def test_linear_complexity_histogram_vs_reference(K, nb):
+    """GPU Berlekamp-Massey histogram (xg_linear_complexity_test) equals the
+    reference's own berlekamp_massey (gf2.cpp:62-110) block by block over the
+    same words (3 streams, blocks straddling words, ragged last word), and
+    the streams continue after exactly ceil(K * nb / 32) words."""
+    from oracle import Battery
+    try:
+        b = Battery()
+    except FileNotFoundError as ex:  # pragma: no cover
+        pytest.skip(str(ex))
+    P = 3
+    nwords = (K * nb + 31) // 32
+    words = np_u32(xg.BlockEnsemble(GP32, 555 + K, P, 63).fill_u32(nwords + 7))
+    e = xg.BlockEnsemble(GP32, 555 + K, P, 63)
+    got = np_u32(e.linear_complexity_test(K, nb)).astype(np.uint64)
+    want = sum(b.lc_histogram(words[g, :nwords], K, nb) for g in range(P))
+    assert np.array_equal(got, want)
+    assert np.array_equal(np_u32(e.fill_u32(7)), words[:, nwords:nwords + 7])
+
+
+def test_linear_complexity_statistic_on_gpu_equals_reference():
+    from oracle import Battery
+    try:
+        b = Battery()
+    except FileNotFoundError as ex:  # pragma: no cover
+        pytest.skip(str(ex))
+    K, nb = 1000, 2000
+    words = np_u32(xg.BlockEnsemble(GP32, 31, 1, 63).fill_u32((K * nb + 31) // 32))[0]
+    hist = xg.BlockEnsemble(GP32, 31, 1, 63).linear_complexity_test(K, nb)
+    chi2, p = xg.linear_complexity_statistic(hist, K)
+    rchi2, rp = b.linear_complexity(words, K, nb)
+    assert chi2 == rchi2 and abs(p - rp) <= 1e-12 * max(1.0, rp)
+
+
+def test_linear_complexity_chunked_and_errors():
+    """More blocks than one chunk holds (2^14 streams x 4100 blocks of 1000
+    bits: chunk boundaries at multiples of 32 blocks) -- all blocks counted,
+    the statistic unremarkable; argument errors."""
+    P, K, nb = 1 << 14, 1000, 4100
+    e = xg.BlockEnsemble(GP32, 1, P, 63)
+    h = np_u32(e.linear_complexity_test(K, nb))
+    assert int(h.sum()) == P * nb
+    chi2, p = xg.linear_complexity_statistic(h, K)
+    assert 1e-6 < p <= 1.0, (chi2, p)
+    with pytest.raises(Exception):
+        e.linear_complexity_test(1024, 1)
+    with pytest.raises(Exception):
+        e.linear_complexity_test(0, 1)
+    with pytest.raises(Exception):
+        xg.BlockEnsemble(xg.tiny_r4w16_params(), 3, 2, 1).linear_complexity_test(100, 4)

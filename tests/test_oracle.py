@@ -335,3 +335,37 @@ def test_rank_counts_give_the_reference_statistic():
         rchi2, rp = b.matrix_rank(words, m)
         assert chi2 == rchi2
         assert abs(p - rp) <= 1e-12 * max(1.0, rp)
+
+
+def test_linear_complexity_statistic_equals_reference():
+    """The reference's per-block Berlekamp-Massey (gf2.cpp:62-110) histogram,
+    binned by the Python mirror's linear_complexity_statistic, gives the
+    reference's linear_complexity_test (tests.cpp:128-178) statistic bit for
+    bit and its p-value to 1e-12, on oracle words, for even and odd K."""
+    import paper_1108_0486_b200 as xg
+    from oracle import Oracle
+    b = _battery_or_skip()
+    o = Oracle()
+    for seed, K, nb in ((1, 1000, 200), (5, 500, 300), (9, 129, 400), (3, 128, 1000)):
+        w = o.ensemble(seed, 1).fill_u32((K * nb + 31) // 32)[0]
+        hist = b.lc_histogram(w, K, nb)
+        assert int(hist.sum()) == nb
+        chi2, p = xg.linear_complexity_statistic(hist, K)
+        rchi2, rp = b.linear_complexity(w, K, nb)
+        assert chi2 == rchi2
+        assert abs(p - rp) <= 1e-12 * max(1.0, rp)
+
+
+def test_berlekamp_massey_known_sequences():
+    """The reference's own KATs (proj/tests/acceptance.cpp:369-382): the
+    v13 sequence has complexity 4, alternating 24 bits complexity 2."""
+    b = _battery_or_skip()
+    assert b.berlekamp_massey(np.array([1, 1, 0, 1, 0, 1, 1, 1, 1, 0, 0, 0, 1], dtype=np.uint8)) == 4
+    assert b.berlekamp_massey(np.array([0, 1] * 12, dtype=np.uint8)) == 2
+    lfsr = [1, 0, 0, 0, 0, 0, 0, 0]
+    while len(lfsr) < 24:
+        i = len(lfsr)
+        lfsr.append(lfsr[i - 8] ^ lfsr[i - 4] ^ lfsr[i - 3] ^ lfsr[i - 2])
+    assert b.berlekamp_massey(np.array(lfsr, dtype=np.uint8)) == 8
+    assert b.berlekamp_massey(np.zeros(64, dtype=np.uint8)) == 0
+    assert b.berlekamp_massey(np.array([0] * 63 + [1], dtype=np.uint8)) == 64
