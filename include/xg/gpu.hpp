@@ -135,6 +135,12 @@ public:
     void rank_test(std::uint64_t matrices, std::uint64_t* dev_counts, xg_stream_t s = nullptr) {
         check(xg_rank_test(h_, matrices, dev_counts, s));
     }
+    // linear_complexity_test's per-block Berlekamp-Massey (tests.cpp:128-178):
+    // adds the histogram of complexities to dev_hist[0..block_length].
+    void linear_complexity_test(unsigned block_length, std::uint64_t blocks, std::uint64_t* dev_hist,
+                                xg_stream_t s = nullptr) {
+        check(xg_linear_complexity_test(h_, block_length, blocks, dev_hist, s));
+    }
 
     unsigned num_blocks() const noexcept { return n_; }
     unsigned lanes() const noexcept { return lanes_; }
