@@ -174,6 +174,19 @@ int xg_rank_test(xg_ensemble_t h, uint64_t matrices_per_stream, uint64_t* dev_co
  * (XG_EINVAL otherwise); w = 32 sets (XG_EUNSUPPORTED otherwise). */
 int xg_linear_complexity_test(xg_ensemble_t h, unsigned block_length, uint64_t blocks_per_stream,
                               uint64_t* dev_hist, xg_stream_t stream);
+
+/* Counting loops of monobit and runs_test (proj/src/stattests/tests.cpp:33-79)
+ * over the first nbits bits of a device word buffer read MSB first (as
+ * BitSource reads 32-bit words): dev_out2[0] += ones, dev_out2[1] +=
+ * adjacent-bit transitions (runs = 1 + transitions). */
+int xg_bits_ones_runs(const uint32_t* dev_words, uint64_t nbits, uint64_t* dev_out2,
+                      xg_stream_t stream);
+/* Birthday spacings (tests.cpp:175-212) over `rounds` consecutive groups of
+ * n_draws device words: each round sorts the words' top t_bits bits and their
+ * n_draws - 1 spacings and counts equal neighbours; *dev_dup += the total.
+ * 2 <= n_draws <= 8192, 1 <= t_bits <= 32 (XG_EINVAL otherwise). */
+int xg_birthday_duplicates(const uint32_t* dev_words, uint32_t n_draws, uint32_t rounds,
+                           unsigned t_bits, uint64_t* dev_dup, xg_stream_t stream);
 /* Advance every stream by `words` without storing (discard). */
 int xg_skip(xg_ensemble_t h, uint64_t words, xg_stream_t stream);
 

@@ -5,3 +5,4 @@ Python host mirror of the reference ``xg`` API over it (see ``xorgens.py``).
 """
 from .xorgens import *  # noqa: F401,F403
 from .xorgens import __all__  # noqa: F401
+from . import battery  # noqa: F401,E402  (run_battery_gpu)

@@ -729,6 +729,33 @@ int xg_linear_complexity_test(xg_ensemble_t h, unsigned block_length, uint64_t b
     return XG_OK;
 }
 
+int xg_bits_ones_runs(const uint32_t* dev_words, uint64_t nbits, uint64_t* dev_out2,
+                      xg_stream_t stream) {
+    if (!dev_words || !dev_out2 || (reinterpret_cast<uintptr_t>(dev_out2) % 8) != 0) return XG_EINVAL;
+    if (nbits == 0) return XG_OK;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const uint64_t nwords = (nbits + 31) / 32;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((nwords + 255) / 256, 148 * 16));
+    ones_runs_kernel<<<grid, 256, 0, s>>>(dev_words, nbits,
+                                          reinterpret_cast<unsigned long long*>(dev_out2));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cuda_rc(cudaGetLastError());
+}
+
+int xg_birthday_duplicates(const uint32_t* dev_words, uint32_t n_draws, uint32_t rounds,
+                           unsigned t_bits, uint64_t* dev_dup, xg_stream_t stream) {
+    if (!dev_words || !dev_dup || (reinterpret_cast<uintptr_t>(dev_dup) % 8) != 0) return XG_EINVAL;
+    if (t_bits == 0 || t_bits > 32 || n_draws < 2 ||
+        n_draws > static_cast<uint32_t>(kBdThreads * kBdItems))
+        return XG_EINVAL;
+    if (rounds == 0) return XG_OK;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    birthday_kernel<<<rounds, kBdThreads, 0, s>>>(dev_words, n_draws, 32u - t_bits,
+                                                   reinterpret_cast<unsigned long long*>(dev_dup));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cuda_rc(cudaGetLastError());
+}
+
 int xg_skip(xg_ensemble_t h, uint64_t words, xg_stream_t stream) {
     if (!h) return XG_EINVAL;
     if (words == 0) return XG_OK;

@@ -84,3 +84,91 @@ lc_kernel(const uint32_t* __restrict__ words, uint32_t streams, uint64_t words_p
 }
 
 }  // namespace xgk
+
+// ---- monobit / runs / birthday spacings (tests.cpp:33-79, 175-212) --------
+#include <cub/block/block_radix_sort.cuh>
+
+namespace xgk {
+
+// Ones and adjacent-bit transitions among the first `nbits` bits of `words`
+// read MSB first: out[0] += ones, out[1] += transitions (runs = 1 +
+// transitions) -- the counting loops of monobit and runs_test
+// (proj/src/stattests/tests.cpp:33-79).  Grid-stride over words.
+__global__ void __launch_bounds__(256)
+ones_runs_kernel(const uint32_t* __restrict__ words, uint64_t nbits,
+                 unsigned long long* __restrict__ out) {
+    const uint64_t nwords = (nbits + 31) >> 5;
+    unsigned long long ones = 0, trans = 0;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nwords;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t w = words[i];
+        const uint64_t rem = nbits - 32 * i;
+        const unsigned valid = rem >= 32 ? 32u : static_cast<unsigned>(rem);  // 1..32
+        const unsigned low = 32u - valid;                                      // 0..31
+        ones += __popc(w & (~0u << low));
+        // pair (bit k+1, bit k), k = low..30: both bits among the valid ones
+        trans += __popc((w ^ (w >> 1)) & 0x7fffffffu & (~0u << low));
+        if (valid == 32u && i + 1 < nwords) trans += (w ^ (words[i + 1] >> 31)) & 1u;
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        ones += __shfl_xor_sync(kFull, ones, s);
+        trans += __shfl_xor_sync(kFull, trans, s);
+    }
+    if ((threadIdx.x & 31u) == 0) {
+        if (ones) atomicAdd(out, ones);
+        if (trans) atomicAdd(out + 1, trans);
+    }
+}
+
+constexpr int kBdThreads = 256, kBdItems = 32;  // up to 8192 draws per round
+
+// Birthday spacings, one CTA per round (tests.cpp:193-204): the round's
+// n_draws words >> drop are sorted, their n - 1 spacings sorted, and equal
+// neighbours counted; *dup += the count.  Sorting: cub::BlockRadixSort.
+__global__ void __launch_bounds__(kBdThreads)
+birthday_kernel(const uint32_t* __restrict__ words, uint32_t n, unsigned drop,
+                unsigned long long* __restrict__ dup) {
+    using Sort = cub::BlockRadixSort<uint32_t, kBdThreads, kBdItems>;
+    // The sort's scratch and the sorted values are never live at once.
+    __shared__ union {
+        typename Sort::TempStorage tmp;
+        uint32_t vals[kBdThreads * kBdItems];
+    } sm;
+    auto& tmp = sm.tmp;
+    uint32_t* vals = sm.vals;
+    const uint32_t* base = words + static_cast<uint64_t>(blockIdx.x) * n;
+    uint32_t k[kBdItems];
+#pragma unroll
+    for (int j = 0; j < kBdItems; ++j) {
+        const uint32_t idx = threadIdx.x * kBdItems + j;  // blocked arrangement
+        k[j] = idx < n ? (base[idx] >> drop) : 0xffffffffu;
+    }
+    Sort(tmp).Sort(k);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kBdItems; ++j) vals[threadIdx.x * kBdItems + j] = k[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kBdItems; ++j) {
+        const uint32_t idx = threadIdx.x * kBdItems + j;
+        k[j] = idx + 1 < n ? vals[idx + 1] - vals[idx] : 0xffffffffu;
+    }
+    __syncthreads();
+    Sort(tmp).Sort(k);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kBdItems; ++j) vals[threadIdx.x * kBdItems + j] = k[j];
+    __syncthreads();
+    unsigned c = 0;
+#pragma unroll
+    for (int j = 0; j < kBdItems; ++j) {
+        const uint32_t idx = threadIdx.x * kBdItems + j;
+        if (idx >= 1 && idx + 1 < n) c += vals[idx] == vals[idx - 1];
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) c += __shfl_xor_sync(kFull, c, s);
+    if ((threadIdx.x & 31u) == 0 && c) atomicAdd(dup, static_cast<unsigned long long>(c));
+}
+
+}  // namespace xgk

@@ -35,6 +35,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import lib, xg_params_t
+from .pvalues import chi_square_pvalue
 
 __all__ = [
     "GeneratorParams", "ParamError", "ParamValidationError", "OutOfRangeError", "XgCudaError",
@@ -245,7 +246,8 @@ RANK_P32 = (0.288788095153841, 0.577576190173205, 0.133635714672954)
 def matrix_rank_statistic(counts) -> Tuple[float, float]:
     """(chi-square statistic, p-value) of rank-test bins, computed as
     proj/src/stattests/tests.cpp:111-123: chi2 over the three bins, p the
-    chi-square survival function with 2 degrees of freedom (= exp(-chi2/2))."""
+    chi-square survival function with 2 degrees of freedom, computed by the
+    reference's own incomplete-gamma code (pvalues.py)."""
     c = [float(int(v)) for v in (counts.tolist() if hasattr(counts, "tolist") else counts)][:3]
     nm = sum(c)
     chi2 = 0.0
@@ -253,20 +255,11 @@ def matrix_rank_statistic(counts) -> Tuple[float, float]:
         e = nm * RANK_P32[i]
         d = c[i] - e
         chi2 += d * d / e
-    return chi2, math.exp(-chi2 / 2.0)
+    return chi2, chi_square_pvalue(chi2, 2)
 
 
 # Linear complexity test bins (proj/src/stattests/tests.cpp:140-141).
 LC_PI = (0.010417, 0.03125, 0.125, 0.5, 0.25, 0.0625, 0.020833)
-
-
-def _regularized_gamma_q_int(a: int, x: float) -> float:
-    """Q(a, x) for integer a: exp(-x) * sum_{k<a} x^k / k!."""
-    term, total = 1.0, 1.0
-    for k in range(1, a):
-        term *= x / k
-        total += term
-    return math.exp(-x) * total
 
 
 def linear_complexity_statistic(hist, block_length: int) -> Tuple[float, float]:
@@ -303,7 +296,7 @@ def linear_complexity_statistic(hist, block_length: int) -> Tuple[float, float]:
     for i in range(7):
         diff = float(counts[i]) - nb * LC_PI[i]
         chi2 += diff * diff / (nb * LC_PI[i])
-    return chi2, _regularized_gamma_q_int(3, chi2 / 2.0)
+    return chi2, chi_square_pvalue(chi2, 6)
 
 
 class BlockEnsemble:

@@ -1,0 +1,82 @@
+"""The reference's battery run on the GPU (paper_1108_0486_b200/battery.py)
+equals the reference's own run_battery (proj/src/stattests/battery.cpp:72-130,
+compiled into oracle/_ref/libxgref_battery.so) over the same stream: every
+test's statistic and p-value bit for bit, every verdict -- for the quick and
+the default configuration."""
+import json
+import time
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1108_0486_b200 as xg  # noqa: E402
+from paper_1108_0486_b200.battery import BatteryConfig, run_battery_gpu  # noqa: E402
+
+
+def _battery():
+    from oracle import Battery
+    try:
+        return Battery()
+    except FileNotFoundError as e:  # pragma: no cover
+        pytest.skip(str(e))
+
+
+def _words_consumed(cfg):
+    return ((cfg.monobit_bits + 31) // 32 + (cfg.runs_bits + 31) // 32 + 32 * cfg.rank_matrices +
+            (cfg.lc_block_length * cfg.lc_blocks + 31) // 32 +
+            cfg.birthday_draws * cfg.birthday_rounds)
+
+
+@pytest.mark.parametrize("quick,seed", [(True, 1), (True, 42), (False, 7)])
+def test_gpu_battery_equals_reference(quick, seed):
+    b = _battery()
+    cfg = BatteryConfig.quick() if quick else BatteryConfig.defaults()
+    p = xg.xorgensgp32_params()
+    t0 = time.perf_counter()
+    rep = run_battery_gpu(p, seed, cfg)
+    torch.cuda.synchronize()
+    t_gpu = time.perf_counter() - t0
+    words = xg.BlockEnsemble(p, seed, 1, 63).fill_u32(_words_consumed(cfg)).cpu().numpy()[0]
+    t0 = time.perf_counter()
+    verdict, js = b.run(words, quick=quick, label="xorgensgp32")
+    t_ref = time.perf_counter() - t0
+    ref = json.loads(js)
+    assert rep["overall"] == ref["overall"] == verdict
+    assert [t["name"] for t in rep["tests"]] == [t["name"] for t in ref["tests"]]
+    for mine, theirs in zip(rep["tests"], ref["tests"]):
+        assert mine["n"] == theirs["n"], mine["name"]
+        assert mine["statistic"] == theirs["statistic"], mine["name"]
+        assert mine["p"] == theirs["p"], mine["name"]
+        assert mine["verdict"] == theirs["verdict"], mine["name"]
+    print(f"battery {'quick' if quick else 'default'}: GPU {t_gpu:.3f} s, reference {t_ref:.3f} s")
+
+
+def test_ones_runs_and_birthday_kernels_direct():
+    """The counting kernels on buffers with ragged bit counts."""
+    rng = np.random.default_rng(3)
+    w = rng.integers(0, 2**32, size=1000, dtype=np.uint64).astype(np.uint32)
+    bits = np.unpackbits(w.byteswap().view(np.uint8)).astype(np.int64)
+    dev = torch.from_numpy(w.view(np.int32)).cuda()
+    for n in (1, 31, 32, 33, 100, 999, 31999, 32000):
+        out = torch.zeros(2, dtype=torch.int64, device="cuda")
+        xg._lib.lib.xg_bits_ones_runs(dev.data_ptr(), n, out.data_ptr(), None)
+        ones, trans = out.tolist()
+        assert ones == int(bits[:n].sum())
+        assert trans == int(np.count_nonzero(bits[1:n] != bits[:n - 1]))
+    for nd, t in ((2, 32), (100, 20), (4096, 32), (8192, 30), (5000, 31)):
+        rounds = 3
+        v = rng.integers(0, 2**32, size=nd * rounds, dtype=np.uint64)
+        dup = 0
+        for r in v.reshape(rounds, nd):
+            sp = np.sort(np.diff(np.sort(r >> np.uint64(32 - t))))
+            dup += int(np.count_nonzero(sp[1:] == sp[:-1]))
+        d = torch.from_numpy(v.astype(np.uint32).view(np.int32)).cuda()
+        out = torch.zeros(1, dtype=torch.int64, device="cuda")
+        assert xg._lib.lib.xg_birthday_duplicates(d.data_ptr(), nd, rounds, t, out.data_ptr(), None) == 0
+        assert int(out.item()) == dup, (nd, t)
