@@ -60,6 +60,8 @@ struct xg_ensemble {
     unsigned lanes = 0;
     int sms = 148;          // multiprocessors of `device` (CTA sizing)
     int smem_per_sm = 0;    // shared memory per SM (occupancy cap of the fills)
+    int smem_optin = 0;     // largest dynamic shared memory a CTA may request
+    bool pair_smem_ok = false;  // pair kernels accept that much (prepare_pair_kernels)
     uint32_t* d_win = nullptr;   // [num_streams][128] logical window, oldest first
     uint32_t* d_weyl = nullptr;  // [num_streams] Weyl accumulator
     uint64_t* d_win64 = nullptr;   // generic path: [num_streams][r] words, oldest first
@@ -211,12 +213,13 @@ int launch_pair(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count, 
         if (!std::is_same_v<P, GP32>) wpb = std::min<uint32_t>(wpb, kWarpsPerBlock);
     }
     size_t smem = 0;
-    if (cap > 0 && h->smem_per_sm > 0) {
-        // cap CTAs fit, cap + 1 do not (each CTA also reserves 1 KB).
-        smem = static_cast<size_t>(h->smem_per_sm) / cap - 2048;
-        if (cudaFuncSetAttribute(pair_kernel<P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)) != cudaSuccess)
-            smem = 0;
+    if (cap > 0 && h->smem_per_sm > 0 && h->pair_smem_ok) {
+        // cap CTAs fit, cap + 1 do not (each CTA also reserves 1 KB).  The
+        // kernels' dynamic shared memory limit was raised at ensemble
+        // creation (prepare_pair_kernels), so nothing here is a
+        // non-stream call -- fills capture into CUDA graphs.
+        smem = std::min<size_t>(static_cast<size_t>(h->smem_per_sm) / cap - 2048,
+                                static_cast<size_t>(h->smem_optin));
     }
     const unsigned grid = static_cast<unsigned>((static_cast<uint64_t>(g_count) + wpb - 1) / wpb);
     pair_kernel<P, MODE><<<grid, 32 * wpb, smem, s>>>(p, h->d_win, h->d_weyl, g_begin, g_count,
@@ -322,6 +325,30 @@ int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t wor
     default:
         return launch_fill_v<MODE, 16>(rt_params<2>(h->params), h, g_begin, g_count, words, out, hits, s);
     }
+}
+
+// Raise the dynamic shared-memory limit of the pair kernels once, at
+// ensemble creation (a function attribute, not a stream operation), so the
+// occupancy cap of launch_pair needs no driver call at launch time.
+template <class P>
+bool prepare_pair_kernels_for(int bytes) {
+    auto set = [bytes](auto kernel) {
+        return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
+               cudaSuccess;
+    };
+    bool ok = set(pair_kernel<P, kU32>) && set(pair_kernel<P, kRaw>) && set(pair_kernel<P, kF32>) &&
+              set(pair_kernel<P, kF64>) && set(pair_kernel<P, kWide>);
+    return ok;
+}
+
+void prepare_pair_kernels(xg_ensemble* h) {
+    cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->device);
+    cudaDeviceGetAttribute(&h->smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device);
+    cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
+    if (h->smem_optin <= 0) return;
+    if (h->kind == kGP32) h->pair_smem_ok = prepare_pair_kernels_for<GP32>(h->smem_optin);
+    else if (h->kind == kRtJ1) h->pair_smem_ok = prepare_pair_kernels_for<RtParams<1>>(h->smem_optin);
+    cudaGetLastError();  // a refused attribute only disables the cap
 }
 
 int launch_seed(xg_ensemble* h, uint64_t seed0, cudaStream_t s) {
@@ -531,8 +558,7 @@ int xg_ensemble_create(const xg_params_t* p, uint64_t base_seed, uint64_t first_
     h->base_seed = base_seed;
     h->first_stream = first_stream;
     h->lanes = lanes;
-    cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
-    cudaDeviceGetAttribute(&h->smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+    prepare_pair_kernels(h);
     int rc = alloc_state(h);
     if (!rc) rc = launch_seed(h, base_seed + first_stream, reinterpret_cast<cudaStream_t>(stream));
     if (rc) {
@@ -564,8 +590,7 @@ int xg_ensemble_create_from_raw(const xg_params_t* p, uint32_t num_streams,
     h->device = device;
     h->num_streams = num_streams;
     h->lanes = lane_bound_impl(p);
-    cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
-    cudaDeviceGetAttribute(&h->smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+    prepare_pair_kernels(h);
     int rc = alloc_state(h);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (!rc && kind == kGeneric) {

@@ -646,3 +646,22 @@ def test_linear_complexity_chunked_and_errors():
         e.linear_complexity_test(0, 1)
     with pytest.raises(Exception):
         xg.BlockEnsemble(xg.tiny_r4w16_params(), 3, 2, 1).linear_complexity_test(100, 4)
+
+
+def test_cuda_graph_capture_of_a_capped_fill(oracle):
+    """A large-ensemble u32 fill (the occupancy-capped launch: 4-stream CTAs,
+    reserved shared memory) captured into a CUDA graph on a fresh ensemble
+    with no warm-up launch: the launch path makes no non-stream driver call,
+    and every replay continues the streams."""
+    P, n = 8192, 256
+    e = xg.BlockEnsemble(GP32, 11, P, 63)
+    out = torch.empty((P, n), dtype=torch.uint32, device="cuda")
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        e.fill_u32(n, out=out)
+    o = oracle.ensemble(11, P)
+    for _ in range(2):
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(np_u32(out), o.fill_u32(n))
