@@ -49,35 +49,42 @@ lc_kernel(const uint32_t* __restrict__ words, uint32_t streams, uint64_t words_p
     uint32_t W = 0u;                     // window: coefficient i <-> s[n - i]
     unsigned L = 0, m = 1;
     const unsigned up = (lane + 31u) & 31u;
+    // 32 bits of the sequence per outer step: one broadcast of the chunk
+    // holding s[32j .. 32j + 31], then one iteration per bit.
 #pragma unroll 1
-    for (unsigned n = 0; n < K; ++n) {
-        // shift the window by one coefficient and insert s[n] at coefficient 0
-        const uint32_t carry = __shfl_sync(kFull, W, up) >> 31;
-        const uint32_t sw = __shfl_sync(kFull, chunk, n >> 5);
-        const uint32_t sn = (sw >> (31u - (n & 31u))) & 1u;
-        W = (W << 1) | (lane == 0u ? sn : carry);
-        // discrepancy
-        const unsigned par = __popc(C & W) & 1u;
-        const unsigned d = __popc(__ballot_sync(kFull, par != 0u)) & 1u;
-        if (d) {
-            // Bs = B x^m: coefficient i of Bs = coefficient i - m of B
-            const unsigned ws = m >> 5, bs = m & 31u;
-            const uint32_t x1 = __shfl_sync(kFull, B, (lane - ws) & 31u);
-            const uint32_t x2 = __shfl_sync(kFull, B, (lane - ws - 1u) & 31u);
-            const uint32_t v1 = lane >= ws ? x1 : 0u;
-            const uint32_t v2 = lane >= ws + 1u ? x2 : 0u;
-            const uint32_t Bs = m >= 1024u ? 0u : __funnelshift_l(v2, v1, bs);
-            if (2u * L <= n) {
-                B = C;
-                C ^= Bs;
-                L = n + 1u - L;
-                m = 1;
+    for (unsigned j = 0; 32u * j < K; ++j) {
+        const uint32_t cur = __shfl_sync(kFull, chunk, j);
+        const unsigned nend = K - 32u * j < 32u ? K - 32u * j : 32u;
+#pragma unroll 4
+        for (unsigned t = 0; t < nend; ++t) {
+            const unsigned n = 32u * j + t;
+            // shift the window by one coefficient and insert s[n] at coefficient 0
+            const uint32_t carry = __shfl_sync(kFull, W, up) >> 31;
+            const uint32_t sn = (cur >> (31u - t)) & 1u;
+            W = (W << 1) | (lane == 0u ? sn : carry);
+            // discrepancy
+            const unsigned par = __popc(C & W) & 1u;
+            const unsigned d = __popc(__ballot_sync(kFull, par != 0u)) & 1u;
+            if (d) {
+                // Bs = B x^m: coefficient i of Bs = coefficient i - m of B
+                const unsigned ws = m >> 5, bs = m & 31u;
+                const uint32_t x1 = __shfl_sync(kFull, B, (lane - ws) & 31u);
+                const uint32_t x2 = __shfl_sync(kFull, B, (lane - ws - 1u) & 31u);
+                const uint32_t v1 = lane >= ws ? x1 : 0u;
+                const uint32_t v2 = lane >= ws + 1u ? x2 : 0u;
+                const uint32_t Bs = m >= 1024u ? 0u : __funnelshift_l(v2, v1, bs);
+                if (2u * L <= n) {
+                    B = C;
+                    C ^= Bs;
+                    L = n + 1u - L;
+                    m = 1;
+                } else {
+                    C ^= Bs;
+                    ++m;
+                }
             } else {
-                C ^= Bs;
                 ++m;
             }
-        } else {
-            ++m;
         }
     }
     if (lane == 0) atomicAdd(hist + L, 1ull);
