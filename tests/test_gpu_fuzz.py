@@ -8,6 +8,8 @@ transition: the pair-lane kernel (xg_pairs.cuh), its word-per-lane fallback
 for rows the pair stores cannot address and for J = 2 sets (xg_kernels.cuh),
 and the tail bodies of both.  Bit-exact after every call.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -39,8 +41,12 @@ def _host(t):
     return t.cpu().numpy()
 
 
+# XG_FUZZ_SEEDS=N widens the sweep (default 2 seeds x 40 calls per set).
+_SEEDS = list(range(1, 1 + int(os.environ.get("XG_FUZZ_SEEDS", "2"))))
+
+
 @pytest.mark.parametrize("name", list(SETS))
-@pytest.mark.parametrize("seed", [1, 2])
+@pytest.mark.parametrize("seed", _SEEDS)
 def test_random_call_sequence(oracle, name, seed):
     rng = np.random.default_rng(1000 * seed + len(name))
     r, s, a, b, c, d, w, omega, gamma = SETS[name]
@@ -49,7 +55,7 @@ def test_random_call_sequence(oracle, name, seed):
     base = int(rng.integers(0, 2**63))
     e = xg.BlockEnsemble(p, base, streams, 32)
     o = oracle.ensemble(base, streams, oracle.params(r, s, a, b, c, d, w, omega, gamma))
-    ops = ["u32", "f32", "f64", "u64", "raw", "words", "mc", "skip", "host"]
+    ops = ["u32", "f32", "f64", "u64", "raw", "words", "mc", "skip", "host", "rank"]
     for step in range(40):
         op = ops[int(rng.integers(len(ops)))]
         n = int(rng.integers(1, 700))
@@ -80,6 +86,14 @@ def test_random_call_sequence(oracle, name, seed):
         elif op == "skip":
             e.skip(n)
             o.fill_u32(n)
+        elif op == "rank":
+            k = 1 + n % 9
+            try:
+                got = e.rank_test(k)
+            except Exception:  # J = 2 sets: XG_EUNSUPPORTED, the streams stay put
+                assert name == "rt_j2", tag
+                continue
+            assert np.array_equal(_host(got).astype(np.uint64), o.rank_counts(k).sum(axis=0)), tag
         else:
             assert np.array_equal(e.generate(n), o.fill_u32(n)), tag
     # the states agree at the end too
