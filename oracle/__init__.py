@@ -301,6 +301,7 @@ class Reference:
                                               ctypes.POINTER(ctypes.c_double),
                                               ctypes.POINTER(_u64)]
         L.xgref_raw_stream.argtypes = [arr, _u64, ctypes.c_uint, _u64, _u64, _vp]
+        L.xgref_low_bit_windows.argtypes = [arr, _u64, ctypes.c_uint, _u64, _int, _u64, _u64, _vp, _vp]
         L.xgref_serial_rate.restype = ctypes.c_double
         L.xgref_serial_rate.argtypes = [_u64, _u64, ctypes.c_uint, ctypes.POINTER(_u64)]
 
@@ -325,6 +326,16 @@ class Reference:
         if rc:
             raise ValueError("reference rejected the parameters")
         return out
+
+    def low_bit_windows(self, seed: int, words: int, window: int, p, raw: bool = True):
+        """(first, last) windows of the words' low bits (test_long_linearity.cpp:30-52)."""
+        first = np.zeros(window, dtype=np.uint8)
+        last = np.zeros(window, dtype=np.uint8)
+        rc = self.lib.xgref_low_bit_windows(self._arr(p), p.omega, p.gamma, seed & (2**64 - 1),
+                                            int(raw), words, window, _ptr(first), _ptr(last))
+        if rc:
+            raise ValueError("reference rejected the parameters")
+        return first, last
 
     def seeded_state(self, seed: int, p):
         buf = np.empty(p.r, dtype=np.uint64)

@@ -78,6 +78,32 @@ int xgref_raw_stream(const unsigned* rsabcdw, std::uint64_t omega, unsigned gamm
     }
 }
 
+// Low bit of every word of RawXorgens(params, seed) (raw = 1) or
+// XorgensState(params, seed) (raw = 0) over `words` words: the first `window`
+// bits and the last `window` bits, as collect_low_bits does
+// (proj/tests/test_long_linearity.cpp:30-52).
+int xgref_low_bit_windows(const unsigned* rsabcdw, std::uint64_t omega, unsigned gamma,
+                          std::uint64_t seed, int raw, std::uint64_t words, std::uint64_t window,
+                          std::uint8_t* first, std::uint8_t* last) {
+    try {
+        const auto p = to_params(rsabcdw, omega, gamma);
+        xg::RawXorgens rg(p, seed);
+        xg::XorgensState st(p, seed);
+        std::vector<std::uint8_t> ring(window, 0);
+        std::uint64_t pos = 0;
+        for (std::uint64_t i = 0; i < words; ++i) {
+            const auto bit = static_cast<std::uint8_t>((raw ? rg.next() : st.next_word()) & 1);
+            if (i < window) first[i] = bit;
+            ring[pos] = bit;
+            if (++pos == window) pos = 0;
+        }
+        for (std::uint64_t i = 0; i < window; ++i) last[i] = ring[(pos + i) % window];
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 // State right after seeding: logical buffer (oldest first) + weyl.
 int xgref_seeded_state(const unsigned* rsabcdw, std::uint64_t omega, unsigned gamma,
                        std::uint64_t seed, std::uint64_t* buffer, std::uint64_t* weyl) {

@@ -124,6 +124,23 @@ def main() -> None:
                       "per_stream_xor_sha": __import__("hashlib").sha256(per_stream_xor.tobytes()).hexdigest(),
                       "per_stream_xor_first16": hexs(per_stream_xor[:16])}
 
+    # 9. proj/tests/test_long_linearity.cpp:71-99: low-bit windows of 2^14 bits,
+    #    linear complexity by the reference's berlekamp_massey.  Raw xorgens
+    #    seed 1 over 2^30 words (first and last window), Weyl-combined seed 1
+    #    over its first 2^14 words.
+    from oracle import Battery
+    bat = Battery()
+    win = 1 << 14
+    rf, rl = ref.low_bit_windows(1, 1 << 30, win, gp32, raw=True)
+    wf, _ = ref.low_bit_windows(1, win, win, gp32, raw=False)
+    import hashlib
+    out["long_linearity"] = {"window": win, "raw_words": 1 << 30,
+                             "raw_seed1_first": bat.berlekamp_massey(rf),
+                             "raw_seed1_last": bat.berlekamp_massey(rl),
+                             "weyl_seed1_first": bat.berlekamp_massey(wf),
+                             "raw_seed1_last_bits_sha256": hashlib.sha256(rl.tobytes()).hexdigest(),
+                             "raw_seed1_first_bits_sha256": hashlib.sha256(rf.tobytes()).hexdigest()}
+
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ref_vectors.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1)

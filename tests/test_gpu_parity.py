@@ -665,3 +665,32 @@ def test_cuda_graph_capture_of_a_capped_fill(oracle):
         g.replay()
         torch.cuda.synchronize()
         assert np.array_equal(np_u32(out), o.fill_u32(n))
+
+
+def test_long_linearity_on_gpu(golden):
+    """proj/tests/test_long_linearity.cpp:71-99 (an opt-in long test in the
+    reference) on the GPU: the low bits of the Weyl-ablated stream, seed 1,
+    over 2^30 words -- the first and the last 2^14-bit windows, the stream
+    skipped 2^30 - 2^15 words in between on the device -- have linear
+    complexity exactly 4096 (the state size) and the last window's bits equal
+    the reference's bit for bit; the Weyl-combined stream's first window has
+    complexity 8192.  Complexities by the reference's berlekamp_massey."""
+    import hashlib
+
+    from oracle import Battery
+    try:
+        b = Battery()
+    except FileNotFoundError as ex:  # pragma: no cover
+        pytest.skip(str(ex))
+    g = golden["long_linearity"]
+    win, words = g["window"], g["raw_words"]
+    e = xg.BlockEnsemble(GP32, 1, 1, 63)
+    first = (np_u32(e.fill_raw_u32(win))[0] & 1).astype(np.uint8)
+    e.skip(words - 2 * win)
+    last = (np_u32(e.fill_raw_u32(win))[0] & 1).astype(np.uint8)
+    assert hashlib.sha256(first.tobytes()).hexdigest() == g["raw_seed1_first_bits_sha256"]
+    assert hashlib.sha256(last.tobytes()).hexdigest() == g["raw_seed1_last_bits_sha256"]
+    assert b.berlekamp_massey(first) == g["raw_seed1_first"] == 4096
+    assert b.berlekamp_massey(last) == g["raw_seed1_last"] == 4096
+    weyl = (np_u32(xg.BlockEnsemble(GP32, 1, 1, 63).fill_u32(win))[0] & 1).astype(np.uint8)
+    assert b.berlekamp_massey(weyl) == g["weyl_seed1_first"] == 8192
