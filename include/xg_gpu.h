@@ -170,11 +170,19 @@ int xg_rank_test(xg_ensemble_t h, uint64_t matrices_per_stream, uint64_t* dev_co
  * bits; the Berlekamp-Massey linear complexity L of every block
  * (proj/src/stattests/gf2.cpp:62-110) is histogrammed: dev_hist[L] += 1
  * (device uint64[block_length + 1]).  The reference's bins, chi-square and
- * p-value follow on the host from the histogram.  1 <= block_length <= 1023
- * (XG_EINVAL otherwise); w = 32 sets (XG_EUNSUPPORTED otherwise). */
+ * p-value follow on the host from the histogram.  1 <= block_length <= 2^18
+ * (XG_EINVAL otherwise; blocks up to 1023 bits keep the polynomials in
+ * registers, longer ones in shared memory); w = 32 sets (XG_EUNSUPPORTED
+ * otherwise). */
 int xg_linear_complexity_test(xg_ensemble_t h, unsigned block_length, uint64_t blocks_per_stream,
                               uint64_t* dev_hist, xg_stream_t stream);
 
+/* Berlekamp-Massey (proj/src/stattests/gf2.cpp:62-110) of `count` device
+ * bit sequences of nbits bits each (1 <= nbits <= 2^18), sequence q starting
+ * at word q * stride_words, bits MSB first (bit i = bit 31 - i % 32 of word
+ * i / 32): dev_L[q] = its linear complexity.  One warp per sequence. */
+int xg_berlekamp_massey(const uint32_t* dev_seqs, uint64_t nbits, uint32_t count,
+                        uint64_t stride_words, uint32_t* dev_L, xg_stream_t stream);
 /* Counting loops of monobit and runs_test (proj/src/stattests/tests.cpp:33-79)
  * over the first nbits bits of a device word buffer read MSB first (as
  * BitSource reads 32-bit words): dev_out2[0] += ones, dev_out2[1] +=

@@ -66,6 +66,7 @@ SIGNATURES = {
     "xg_mc_pi": (_int, [_vp, _u64, _vp, _vp]),
     "xg_rank_test": (_int, [_vp, _u64, _vp, _vp]),
     "xg_linear_complexity_test": (_int, [_vp, ctypes.c_uint, _u64, _vp, _vp]),
+    "xg_berlekamp_massey": (_int, [_vp, _u64, _u32, _u64, _vp, _vp]),
     "xg_bits_ones_runs": (_int, [_vp, _u64, _vp, _vp]),
     "xg_birthday_duplicates": (_int, [_vp, _u32, _u32, ctypes.c_uint, _vp, _vp]),
     "xg_skip": (_int, [_vp, _u64, _vp]),

@@ -471,6 +471,18 @@ int fill_common(xg_ensemble_t h, uint64_t per_stream, void* dev_out, size_t alig
     }
 }
 
+int launch_bm_long(const uint32_t* data, uint64_t data_words, uint64_t nbits, uint64_t stride_bits,
+                   uint32_t per_row, uint64_t row_bits, uint64_t count, unsigned long long* hist,
+                   uint32_t* L_out, cudaStream_t s) {
+    const size_t smem = 4ull * bm_words(nbits) * sizeof(uint32_t);
+    int rc = gen_smem_attr(bm_long_kernel, smem);
+    if (rc) return rc;
+    bm_long_kernel<<<static_cast<unsigned>(count), 32, smem, s>>>(data, data_words, nbits, stride_bits,
+                                                                 per_row, row_bits, hist, L_out);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cuda_rc(cudaGetLastError());
+}
+
 }  // namespace
 
 extern "C" {
@@ -713,7 +725,7 @@ int xg_rank_test(xg_ensemble_t h, uint64_t matrices_per_stream, uint64_t* dev_co
 int xg_linear_complexity_test(xg_ensemble_t h, unsigned block_length, uint64_t blocks_per_stream,
                               uint64_t* dev_hist, xg_stream_t stream) {
     if (!h || !dev_hist || (reinterpret_cast<uintptr_t>(dev_hist) % 8) != 0) return XG_EINVAL;
-    if (block_length == 0 || block_length > kLcMaxK) return XG_EINVAL;
+    if (block_length == 0 || block_length > kBmMaxBits) return XG_EINVAL;
     if (h->params.w != 32) return XG_EUNSUPPORTED;  // BitSource reads w bits per word
     if (blocks_per_stream == 0) return XG_OK;
     DeviceGuard dg(h->device);
@@ -743,15 +755,31 @@ int xg_linear_complexity_test(xg_ensemble_t h, unsigned block_length, uint64_t b
         rc = launch_fill<kU32>(h, 0, h->num_streams, wc, h->d_lc, nullptr, s);
         if (rc) return rc;
         const uint64_t warps = P * nb;
-        lc_kernel<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, s>>>(
-            h->d_lc, h->num_streams, wc, block_length, static_cast<uint32_t>(nb),
-            reinterpret_cast<unsigned long long*>(dev_hist));
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        rc = cuda_rc(cudaGetLastError());
+        if (K <= kLcMaxK) {  // register-resident polynomials (1024 bits per warp)
+            lc_kernel<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, s>>>(
+                h->d_lc, h->num_streams, wc, block_length, static_cast<uint32_t>(nb),
+                reinterpret_cast<unsigned long long*>(dev_hist));
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            rc = cuda_rc(cudaGetLastError());
+        } else {  // longer blocks: polynomials in shared memory
+            rc = launch_bm_long(h->d_lc, P * wc, K, K, static_cast<uint32_t>(nb), wc * 32, warps,
+                                reinterpret_cast<unsigned long long*>(dev_hist), nullptr, s);
+        }
         if (rc) return rc;
         left -= nb;
     }
     return XG_OK;
+}
+
+int xg_berlekamp_massey(const uint32_t* dev_seqs, uint64_t nbits, uint32_t count,
+                        uint64_t stride_words, uint32_t* dev_L, xg_stream_t stream) {
+    if (!dev_seqs || !dev_L || nbits == 0 || nbits > kBmMaxBits) return XG_EINVAL;
+    if (count == 0) return XG_OK;
+    if (count > 1 && stride_words * 32 < nbits) return XG_EINVAL;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const uint64_t data_words = static_cast<uint64_t>(count - 1) * stride_words + (nbits + 31) / 32;
+    return launch_bm_long(dev_seqs, data_words, nbits, stride_words * 32, count, 0, count, nullptr,
+                          dev_L, s);
 }
 
 int xg_bits_ones_runs(const uint32_t* dev_words, uint64_t nbits, uint64_t* dev_out2,

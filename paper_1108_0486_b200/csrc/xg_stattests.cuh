@@ -179,3 +179,130 @@ birthday_kernel(const uint32_t* __restrict__ words, uint32_t n, unsigned drop,
 }
 
 }  // namespace xgk
+
+// ---- Berlekamp-Massey for long sequences (up to 2^18 bits) ----------------
+namespace xgk {
+
+constexpr uint64_t kBmMaxBits = 1ull << 18;
+
+// Words needed per polynomial / reversed-sequence buffer for n bits.
+__host__ __device__ constexpr uint32_t bm_words(uint64_t nbits) {
+    return static_cast<uint32_t>((nbits + 31) / 32 + 2);
+}
+
+// One warp per sequence, the reference's formulation (gf2.cpp:62-110) in
+// shared memory: the sequence reversed into `rev` (bit j of the buffer =
+// s[n_bits - 1 - j]) so the taps of step n are the contiguous slice starting
+// at n_bits - 1 - n; C, B and a scratch polynomial rotate between three
+// buffers that always hold exact polynomials.  Lane l works on words l,
+// l + 32, ...; the discrepancy is one ballot of the lanes' partial parities.
+// Bits are read MSB first (bit i of the data = bit 31 - i % 32 of word
+// i / 32, as BitSource reads words).  Sequence q = data bits
+// [bit0(q), bit0(q) + nbits) with bit0(q) = (q / per_row) * row_bits +
+// (q % per_row) * stride_bits.  Its linear complexity goes to L_out[q]
+// and/or hist[L].
+__global__ void __launch_bounds__(32)
+bm_long_kernel(const uint32_t* __restrict__ data, uint64_t data_words, uint64_t nbits,
+               uint64_t stride_bits, uint32_t per_row, uint64_t row_bits,
+               unsigned long long* __restrict__ hist, uint32_t* __restrict__ L_out) {
+    extern __shared__ uint32_t bm_smem[];
+    const unsigned lane = threadIdx.x;
+    const uint32_t nw = bm_words(nbits);
+    uint32_t* rev = bm_smem;
+    uint32_t* P0 = rev + nw;
+    uint32_t* P1 = P0 + nw;
+    uint32_t* P2 = P1 + nw;
+    const uint64_t q = blockIdx.x;
+    const uint64_t bit0 = (q / per_row) * row_bits + (q % per_row) * stride_bits;
+    // 32 data bits from sequence bit 32t on (MSB first); 0 outside the sequence
+    auto sword = [&](int64_t t) -> uint32_t {
+        if (t < 0 || 32 * t >= static_cast<int64_t>(nbits)) return 0u;
+        const uint64_t g = bit0 + 32 * static_cast<uint64_t>(t);
+        const uint64_t w = g >> 5;
+        const unsigned sh = static_cast<unsigned>(g & 31u);
+        const uint32_t hi = w < data_words ? data[w] : 0u;
+        const uint32_t lo = (sh && w + 1 < data_words) ? data[w + 1] : 0u;
+        uint32_t v = sh ? __funnelshift_l(lo, hi, sh) : hi;
+        const int64_t valid = static_cast<int64_t>(nbits) - 32 * t;
+        if (valid < 32) v &= ~0u << (32 - valid);
+        return v;
+    };
+    // rev word k = the 32 sequence bits ending at e = nbits - 1 - 32k, bit b = s[e - b]
+    for (uint32_t k = lane; k < nw; k += 32) {
+        const int64_t e = static_cast<int64_t>(nbits) - 1 - 32 * static_cast<int64_t>(k);
+        uint32_t v = 0;
+        if (e >= 0) {
+            const int64_t st = e - 31;  // first bit of the window (may be negative)
+            const int64_t t0 = st >= 0 ? st / 32 : -((31 - st) / 32);
+            const unsigned sh = static_cast<unsigned>(st - 32 * t0);
+            const uint32_t a = sword(t0), b2 = sword(t0 + 1);
+            v = sh ? __funnelshift_l(b2, a, sh) : a;
+        }
+        rev[k] = v;
+        P0[k] = k == 0 ? 1u : 0u;  // C = 1
+        P1[k] = k == 0 ? 1u : 0u;  // B = 1
+        P2[k] = 0u;
+    }
+    __syncwarp();
+    uint32_t* C = P0;
+    uint32_t* B = P1;
+    uint32_t* T = P2;
+    uint64_t L = 0, m = 1;
+    for (uint64_t n = 0; n < nbits; ++n) {
+        const uint64_t off = nbits - 1 - n;
+        const uint32_t ow = static_cast<uint32_t>(off >> 5), ob = static_cast<uint32_t>(off & 31u);
+        const uint64_t taps = L + 1;
+        const uint32_t tw = static_cast<uint32_t>((taps + 31) / 32);
+        unsigned par = 0;
+        for (uint32_t k = lane; k < tw; k += 32) {
+            uint32_t chunk = rev[ow + k] >> ob;
+            if (ob) chunk |= rev[ow + k + 1] << (32u - ob);
+            const uint64_t rem = taps - 32ull * k;
+            if (rem < 32) chunk &= (1u << rem) - 1u;
+            par ^= __popc(C[k] & chunk);
+        }
+        const unsigned d = __popc(__ballot_sync(kFull, (par & 1u) != 0u)) & 1u;
+        if (d) {
+            // T = C ^ B x^m, every word (the buffers always hold exact
+            // polynomials, zero above their degree: deg <= n + 1 < 32 nw)
+            const uint32_t ws = static_cast<uint32_t>(m >> 5), bs = static_cast<uint32_t>(m & 31u);
+            const uint32_t top = static_cast<uint32_t>(
+                (n + 2) / 32 + 2 < nw ? (n + 2) / 32 + 2 : nw);  // words above are zero in C and B x^m
+            for (uint32_t k = lane; k < nw; k += 32) {
+                if (k >= top) {
+                    T[k] = 0u;
+                    continue;
+                }
+                uint32_t sh = 0;
+                if (k >= ws) {
+                    sh = B[k - ws] << bs;
+                    if (bs && k >= ws + 1) sh |= B[k - ws - 1] >> (32u - bs);
+                }
+                T[k] = C[k] ^ sh;
+            }
+            __syncwarp();
+            if (2 * L <= n) {
+                uint32_t* oldB = B;
+                B = C;
+                C = T;
+                T = oldB;
+                L = n + 1 - L;
+                m = 1;
+            } else {
+                uint32_t* oldC = C;
+                C = T;
+                T = oldC;
+                ++m;
+            }
+            __syncwarp();
+        } else {
+            ++m;
+        }
+    }
+    if (lane == 0) {
+        if (L_out) L_out[blockIdx.x] = static_cast<uint32_t>(L);
+        if (hist) atomicAdd(hist + L, 1ull);
+    }
+}
+
+}  // namespace xgk

@@ -44,7 +44,7 @@ __all__ = [
     "PeriodDescription", "xorgensgp32_params", "tiny_r2w8_params", "tiny_r2w16_params",
     "tiny_r4w16_params", "gpu_supported", "fast_path", "XorgensState", "seed_state", "batch_step",
     "BlockEnsemble", "XorgensSource", "partition", "kernel_launches", "matrix_rank_statistic",
-    "RANK_P32", "linear_complexity_statistic", "LC_PI",
+    "RANK_P32", "linear_complexity_statistic", "LC_PI", "berlekamp_massey",
 ]
 
 
@@ -260,6 +260,23 @@ def matrix_rank_statistic(counts) -> Tuple[float, float]:
 
 # Linear complexity test bins (proj/src/stattests/tests.cpp:140-141).
 LC_PI = (0.010417, 0.03125, 0.125, 0.5, 0.25, 0.0625, 0.020833)
+
+
+def berlekamp_massey(seqs, nbits: int):
+    """Linear complexity (proj/src/stattests/gf2.cpp:62-110) of every row of
+    ``seqs`` -- a 2-D CUDA tensor of 32-bit words, each row one sequence of
+    ``nbits`` bits packed MSB first -- on the GPU, one warp per row.  Returns
+    an int32 CUDA tensor of the complexities."""
+    torch = _torch()
+    if seqs.dim() != 2 or seqs.element_size() != 4 or not seqs.is_cuda or not seqs.is_contiguous():
+        raise ValueError("seqs must be a contiguous 2-D CUDA tensor of 32-bit words")
+    if nbits > 32 * seqs.shape[1]:
+        raise ValueError("rows hold fewer than nbits bits")
+    out = torch.empty(seqs.shape[0], dtype=torch.int32, device=seqs.device)
+    _raise(lib.xg_berlekamp_massey(ctypes.c_void_p(seqs.data_ptr()), nbits, seqs.shape[0],
+                                   seqs.shape[1], ctypes.c_void_p(out.data_ptr()),
+                                   _stream_ptr(seqs.device.index or 0)))
+    return out
 
 
 def linear_complexity_statistic(hist, block_length: int) -> Tuple[float, float]:

@@ -595,7 +595,8 @@ def test_rank_test_large_ensemble():
 
 
 @pytest.mark.parametrize("K,nb", [(1, 50), (7, 65), (31, 33), (32, 40), (33, 97), (100, 64),
-                                  (500, 70), (1000, 45), (1023, 38)])
+                                  (500, 70), (1000, 45), (1023, 38), (1024, 40), (2000, 39),
+                                  (4099, 40)])
 def test_linear_complexity_histogram_vs_reference(K, nb):
     """GPU Berlekamp-Massey histogram (xg_linear_complexity_test) equals the
     reference's own berlekamp_massey (gf2.cpp:62-110) block by block over the
@@ -641,7 +642,7 @@ def test_linear_complexity_chunked_and_errors():
     chi2, p = xg.linear_complexity_statistic(h, K)
     assert 1e-6 < p <= 1.0, (chi2, p)
     with pytest.raises(Exception):
-        e.linear_complexity_test(1024, 1)
+        e.linear_complexity_test((1 << 18) + 1, 1)
     with pytest.raises(Exception):
         e.linear_complexity_test(0, 1)
     with pytest.raises(Exception):
@@ -694,3 +695,36 @@ def test_long_linearity_on_gpu(golden):
     assert b.berlekamp_massey(last) == g["raw_seed1_last"] == 4096
     weyl = (np_u32(xg.BlockEnsemble(GP32, 1, 1, 63).fill_u32(win))[0] & 1).astype(np.uint8)
     assert b.berlekamp_massey(weyl) == g["weyl_seed1_first"] == 8192
+    # the same three complexities by the GPU's own Berlekamp-Massey
+    packed = np.stack([np.packbits(x).view(">u4").astype(np.uint32) for x in (first, last, weyl)])
+    dev = torch.from_numpy(packed.view(np.int32)).cuda()
+    assert np_u32(xg.berlekamp_massey(dev, win)).tolist() == [4096, 4096, 8192]
+
+
+@pytest.mark.parametrize("nbits", [1, 2, 31, 32, 33, 64, 999, 1000, 4096, 16384, 40001])
+def test_gpu_berlekamp_massey_vs_reference(nbits):
+    """xg_berlekamp_massey (shared-memory polynomials, one warp per sequence)
+    equals the reference's berlekamp_massey (gf2.cpp:62-110) on random,
+    LFSR-generated (low complexity) and zero sequences."""
+    from oracle import Battery
+    try:
+        b = Battery()
+    except FileNotFoundError as ex:  # pragma: no cover
+        pytest.skip(str(ex))
+    rng = np.random.default_rng(nbits)
+    seqs = [rng.integers(0, 2, size=nbits, dtype=np.uint8) for _ in range(3)]
+    lfsr = list(rng.integers(0, 2, size=min(nbits, 40), dtype=np.uint8))
+    taps = [int(t) for t in rng.choice(np.arange(1, 41), size=4, replace=False)]
+    while len(lfsr) < nbits:
+        i = len(lfsr)
+        lfsr.append(np.uint8(np.bitwise_xor.reduce([lfsr[i - t] for t in taps if i - t >= 0])))
+    seqs.append(np.array(lfsr[:nbits], dtype=np.uint8))
+    seqs.append(np.zeros(nbits, dtype=np.uint8))
+    words = (nbits + 31) // 32 + 1
+    packed = np.zeros((len(seqs), words), dtype=np.uint32)
+    for i, sq in enumerate(seqs):
+        pb = np.packbits(np.concatenate([sq, np.zeros(32 * words - nbits, dtype=np.uint8)]))
+        packed[i] = pb.view(">u4").astype(np.uint32)
+    dev = torch.from_numpy(packed.view(np.int32)).cuda()
+    got = np_u32(xg.berlekamp_massey(dev, nbits)).tolist()
+    assert got == [b.berlekamp_massey(sq) for sq in seqs]
