@@ -30,3 +30,18 @@ for var_params in (p, xg.GeneratorParams(128, 95, 17, 12, 13, 15, 32, 2654435769
     e.generate(300)
 torch.cuda.synchronize()
 print("sanitize smoke ok")
+
+# statistical-test kernels (fused rank, Berlekamp-Massey both ways, counting kernels)
+e = xg.BlockEnsemble(p, 5, 9, 63)
+oe = o.ensemble(5, 9)
+assert np.array_equal(e.rank_test(5).cpu().numpy().astype(np.uint64), oe.rank_counts(5).sum(axis=0))
+h1 = e.linear_complexity_test(100, 40)
+h2 = e.linear_complexity_test(2000, 38)
+assert int(h1.sum()) == 9 * 40 and int(h2.sum()) == 9 * 38
+seqs = torch.randint(-2**31, 2**31 - 1, (3, 160), dtype=torch.int32, device="cuda")
+L = xg.berlekamp_massey(seqs, 5000)
+assert all(2000 < int(v) < 3000 for v in L.tolist())
+from paper_1108_0486_b200.battery import BatteryConfig, run_battery_gpu  # noqa: E402
+rep = run_battery_gpu(p, 3, BatteryConfig.quick())
+assert rep["num_tests"] == 5
+print("sanitize stattests ok")
