@@ -1,5 +1,5 @@
 #!/usr/bin/env python3
-"""xorgensGP throughput on B200: RN/s (32-bit, device-timed), % of HBM roofline.
+"""xorgensGP throughput on B200: RN/s (32-bit, device-timed), % of HBM write BW.
 
 Default workload (BASELINE.json configs[1]): fill of 2^30 uint32 per GPU,
 P = 2^14 streams x 2^16 words, base_seed 1, block-major, bit-exact with the
@@ -8,19 +8,28 @@ persistent ensemble (streams continue across steps, exactly like repeated
 generate() calls in the reference, proj/src/parallel.cpp:97-135 and
 proj/src/bench.cpp:95-112) -- one pair_kernel launch (xg_pairs.cuh).
 
-Other workloads (--workload): fill_f32, fill_f64 (config 3), fill_2p34
-(config 4: 2^34 words over N GPUs, strong scaling), mc_pi (config 5: 2^40
-samples over N GPUs, one NCCL all-reduce of the uint64 hit count).
+The default line also carries, each under the same clock and with its own
+roofline, parity check and CPU baseline, the other BASELINE configs as
+``extra_workloads``: fill_f32 / fill_f64 (config 3, weak), fill_2p34 (config
+4: 2^34 words over N GPUs, strong) and mc_pi (config 5: 2^40 samples over N
+GPUs, the uint64 hit count all-reduced over NCCL inside every step).
+
+After the timed loop every workload re-runs on a FRESH ensemble and its
+output is digested on the device (xg_digest_u32) and compared stream by
+stream with tests/golden/full_size.json (the reference's own words):
+``parity.ok``.
 
   python bench.py [--gpus N --steps K --warmup W] [--workload W] [--impl reference]
-Multi-GPU: launched by torchrun, one rank per GPU; each rank owns a disjoint
-stream range; timing = max over ranks of CUDA-event time.
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run
+(one rank per GPU, NCCL); each rank owns a disjoint stream range; timing =
+max over ranks of CUDA-event time.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -29,6 +38,13 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+
+METRIC = "RN/s (32-bit, device-timed) at 1/2/4/8 B200; % of HBM write BW"
+FULL_SIZE = os.path.join(ROOT, "tests", "golden", "full_size.json")
+CHUNK = 1 << 14  # streams per golden chunk
+WORKLOADS = ["fill_u32", "fill_f32", "fill_f64", "fill_2p34", "mc_pi", "skip", "stream1", "rank", "lc"]
+EXTRA = ("fill_f32", "fill_f64", "fill_2p34", "mc_pi")
+
 
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -48,15 +64,15 @@ def load_ncu(workload: str) -> dict:
         return {}
 
 
-def load_traffic(workload: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+def cpu_model() -> str:
     try:
-        with open(path) as f:
-            d = json.load(f)
-        return d.get(workload, {}).get("dram_bytes_per_launch")
-    except Exception:
-        return None
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -128,30 +144,32 @@ class ClockSampler:
                 "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
-def write_probe_gbs(out, stream, reps: int = 5):
-    """Write-only HBM ceiling on the same buffer (libxg_probe.so, bench-only)."""
-    import ctypes
+# --------------------------------------------------------------------------
+# process group
+# --------------------------------------------------------------------------
 
-    import torch
-
-    lib = ctypes.CDLL(os.path.join(ROOT, "paper_1108_0486_b200", "lib", "libxg_probe.so"))
-    lib.xg_probe_write.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
-    nbytes = out.numel() * out.element_size()
-    ptr, sp = ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(stream.cuda_stream)
-    for _ in range(3):
-        lib.xg_probe_write(ptr, nbytes, sp)
-    best = float("inf")
-    for _ in range(reps):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        lib.xg_probe_write(ptr, nbytes, sp)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        best = min(best, e0.elapsed_time(e1))
-    return nbytes / (best / 1e3) / 1e9
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
 
 
-def dist_setup():
+def self_launch(args) -> int:
+    """--gpus N > 1 outside torchrun: re-run this script under
+    torch.distributed.run with N ranks on this node (the driver's own
+    launch line), so `python bench.py --gpus N` is an N-GPU job."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def dist_setup(dry: bool = False):
     import torch
     import torch.distributed as dist
 
@@ -160,17 +178,17 @@ def dist_setup():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # XG_BENCH_BACKEND=gloo (testing only): exercise the N>1 flow with every
     # rank on the visible GPUs round-robin, e.g. two ranks on one GPU.
-    backend = os.environ.get("XG_BENCH_BACKEND", "nccl")
-    if backend != "nccl":
+    backend = "gloo" if dry else os.environ.get("XG_BENCH_BACKEND", "nccl")
+    if not dry and backend != "nccl":
         local = local % max(1, torch.cuda.device_count())
-    if world > 1 and not dist.is_initialized():
+    if not dry:
         torch.cuda.set_device(local)
+    if world > 1 and not dist.is_initialized():
         if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         else:
             dist.init_process_group(backend)
-    elif world == 1:
-        torch.cuda.set_device(local)
     return world, rank, local
 
 
@@ -181,110 +199,63 @@ def barrier(world):
         dist.barrier()
 
 
+def _coll_device():
+    import torch.distributed as dist
+
+    return "cuda" if dist.get_backend() == "nccl" else "cpu"
+
+
 def max_over_ranks(x: float, world: int) -> float:
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
 
-    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
 
-# --------------------------------------------------------------------------
-# CPU baseline / reference arm: the reference's own code (oracle/_ref),
-# BlockEnsemble(p, 1, P, 63).generate(per_block) on all host threads,
-# wall-clocked around generate() as measure_ensemble_throughput does.
-# --------------------------------------------------------------------------
+def all_ok(ok: bool, world: int) -> bool:
+    if world == 1:
+        return ok
+    import torch
+    import torch.distributed as dist
 
-def reference_rate(streams: int, per_block: int, trials: int, warmup: int = 1, budget_s: float = 30.0,
-                   min_trials: int = 3):
-    from oracle import REF_SO, Oracle, Reference
-
-    threads = os.cpu_count() or 1
-    if os.path.exists(REF_SO):
-        ref = Reference()
-        p = Oracle().gp32()
-        h = ref.ensemble(p, 1, streams, 63)
-        rates = []
-        t0 = time.perf_counter()
-        for i in range(warmup + trials):
-            secs, _ = ref.generate_timed(h, per_block, threads)
-            if i >= warmup:
-                rates.append(streams * per_block / secs)
-            if time.perf_counter() - t0 > budget_s and len(rates) >= min_trials:
-                break
-        ref.destroy(h)
-        kind = "reference"
-    else:  # the C restatement, when the reference could not be compiled
-        import numpy as np  # noqa: F401
-
-        o = Oracle()
-        e = o.ensemble(1, streams)
-        rates = []
-        for i in range(warmup + trials):
-            t = time.perf_counter()
-            e.fill_u32(per_block)
-            dt = time.perf_counter() - t
-            if i >= warmup:
-                rates.append(streams * per_block / dt)
-        kind = "port"
-    return {"value": statistics.mean(rates), "unit": "RN/s", "cores": threads, "kind": kind,
-            "sample": f"BlockEnsemble(xorgensgp32, base_seed=1, blocks={streams}, lanes=63)"
-                      f".generate({per_block}) = {streams * per_block} words per trial, "
-                      f"{len(rates)} trials after {warmup} warm-up, workers={threads}, "
-                      f"wall clock around generate() (proj/src/bench.cpp:95-112)",
-            "trials": len(rates), "min": min(rates), "max": max(rates)}
+    t = torch.tensor([1 if ok else 0], dtype=torch.int64, device=_coll_device())
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
 
 
-def run_reference_arm(args):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return 0
-    streams = 1 << 14
-    per_block = 1 << 13  # 2^27 words per step (8 B/word in the reference: 1 GiB of vectors)
-    base = reference_rate(streams, per_block, trials=max(1, args.steps), warmup=args.warmup,
-                          budget_s=120.0)
-    v = base["value"]
-    line = {
-        "impl": "reference", "metric": "RN/s (32-bit, device-timed) at 1/2/4/8 B200; % of HBM write BW",
-        "value": v, "unit": "RN/s", "n_gpus": world, "steps": base["trials"], "warmup": args.warmup,
-        "ms_per_step": streams * per_block / v * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": "xorgensGP fill, xorgensgp32, base_seed 1, 2^14 streams "
-                               f"(reference BlockEnsemble::generate, {per_block} words/stream/step "
-                               "bounded sample of the 2^30-word config)",
-                   "streams": streams, "per_stream": per_block},
-        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
-        "e2e": {"value": v, "unit": "RN/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-    return 0
+def comm_info(world: int) -> dict:
+    if world == 1:
+        return {"backend": None, "nranks": 1}
+    import torch.distributed as dist
+
+    return {"backend": dist.get_backend(), "nranks": dist.get_world_size(),
+            "nccl_debug": os.environ.get("NCCL_DEBUG")}
 
 
 # --------------------------------------------------------------------------
-# our arm
+# workloads
 # --------------------------------------------------------------------------
 
 def workload_geometry(wl: str, world: int, rank: int):
-    """Per-rank stream slice and per-stream length of each workload, and the
-    words the whole job consumes per step.  Weak scaling: every rank owns
-    2^14 streams of its own (global ids rank*2^14 ...), 2^30 values per GPU.
-    Strong scaling: one global ensemble split by xg_partition."""
+    """(first stream, streams, values per stream, scaling, job words per step)
+    of a rank.  Weak scaling: every rank owns 2^14 streams of its own (global
+    ids rank*2^14 ...), 2^30 values per GPU.  Strong scaling: one global
+    ensemble split by xg_partition."""
     import paper_1108_0486_b200 as xg
 
     if wl in ("fill_u32", "fill_f32", "fill_f64", "skip"):
-        P, per = 1 << 14, 1 << 16
+        P, per = CHUNK, 1 << 16
         words = P * per * (2 if wl == "fill_f64" else 1)
         return rank * P, P, per, "weak", words * world
     if wl == "rank":  # fused GF(2) matrix-rank test: 2^14 streams x 2^12 32x32 matrices per GPU
-        P = 1 << 14
+        P = CHUNK
         return rank * P, P, 1 << 12, "weak", (P << 17) * world
     if wl == "lc":  # linear complexity test: 2^14 streams x 256 blocks of 1000 bits per GPU
-        P = 1 << 14
+        P = CHUNK
         return rank * P, P, 256, "weak", P * 256 * 1000 // 32 * world
     if wl == "stream1":  # config 1 on the GPU: ONE stream (seed 1 + rank), 10^8 words
         return rank, 1, 10**8, "weak", 10**8 * world
@@ -296,6 +267,36 @@ def workload_geometry(wl: str, world: int, rank: int):
         first, count = xg.partition(total_streams, world, rank)
         return first, count, (1 << 40) // total_streams, "strong", 1 << 41
     raise ValueError(wl)
+
+
+WORKLOAD_TEXT = {
+    "fill_u32": "xorgensGP fill of 2^30 uint32 per GPU, bit-exact vs CPU per stream",
+    "fill_f32": "uniform float32 [0,1) fill of 2^30 values per GPU, fused conversion",
+    "fill_f64": "uniform float64 [0,1) fill of 2^30 values (2^31 words) per GPU, fused conversion",
+    "fill_2p34": "disjoint-stream fill of 2^34 uint32 across N GPUs",
+    "mc_pi": "fused in-register Monte Carlo pi, 2^40 samples across N GPUs, NCCL scalar reduce",
+    "skip": "generator core only (advance 2^30 words, no stores)",
+    "stream1": "one stream per GPU (BASELINE config 1: seed 1, 10^8 uint32), one warp",
+    "rank": "fused GF(2) 32x32 matrix-rank test (reference matrix_rank_test), "
+            "2^14 streams x 2^12 matrices per GPU",
+    "lc": "linear complexity test (reference linear_complexity_test, K = 1000), "
+          "2^14 streams x 256 blocks per GPU",
+}
+BYTES_PER_VAL = {"fill_u32": 4, "fill_f32": 4, "fill_f64": 8, "fill_2p34": 4, "stream1": 4}
+WORDS_PER_VAL = {"fill_f64": 2, "mc_pi": 2, "rank": 32, "lc": 1000 / 32}
+
+
+def config_for(wl: str, world: int) -> dict:
+    """The workload's config object -- shared verbatim by the reference arm."""
+    _, count, per, scaling, _ = workload_geometry(wl, world, 0)
+    return {"workload": WORKLOAD_TEXT[wl], "params": "xorgensgp32 (128,65,15,14,12,17) w=32",
+            "base_seed": 1, "streams_per_gpu": count, "values_per_stream": per,
+            "layout": "block-major out[g*per_stream+k]",
+            "l2": "output per step >> 126 MB L2 (no flush needed)" if wl in BYTES_PER_VAL else
+                  "no HBM traffic (in-register consumer)",
+            "parallelism": f"dp{world} (disjoint stream ranges"
+                           + (", one uint64 all-reduce per step)" if wl == "mc_pi" else
+                              ", no data-path collective)")}
 
 
 def timed_loop(fn, stream, steps, warmup, world, counter=None):
@@ -328,262 +329,560 @@ def timed_loop(fn, stream, steps, warmup, world, counter=None):
     return total, step_ms, launches
 
 
+def _load_full_size():
+    with open(FULL_SIZE) as f:
+        return json.load(f)
+
+
+def parity_check(wl: str, world: int, rank: int, local: int, out=None) -> dict:
+    """Re-run the workload on a FRESH ensemble of this rank's streams and
+    compare it with the reference-derived goldens (tests/golden/full_size.json,
+    per chunk of 2^14 streams): device digests of every stream for the fills,
+    the exact hit count of 2^15 samples per stream for MC.  The verdict is
+    the AND over ranks."""
+    import torch
+
+    import paper_1108_0486_b200 as xg
+    from paper_1108_0486_b200.digest import chunk_record, row_digests
+
+    fs = _load_full_size()
+    first, count, per, _, _ = workload_geometry(wl, world, rank)
+    p = xg.xorgensgp32_params()
+    res = {"checked": False}
+    if first % CHUNK or count % CHUNK:
+        res["why"] = "rank slice is not whole golden chunks"
+    elif wl in ("fill_u32", "fill_2p34", "fill_f32", "fill_f64"):
+        key = {"fill_u32": "u32", "fill_2p34": "u32"}.get(wl, wl[5:])
+        chunks = fs[key]["chunks"]
+        c0, nc = first // CHUNK, count // CHUNK
+        if c0 + nc > len(chunks):
+            res["why"] = f"golden covers {len(chunks)} chunks; rank needs {c0 + nc}"
+        else:
+            e = xg.BlockEnsemble(p, 1, count, 63, first_stream=first, device=local)
+            fill = {"u32": e.fill_u32, "f32": e.fill_f32, "f64": e.fill_f64}[key]
+            buf = fill(per, out=out)
+            x, s, ws = row_digests(buf)
+            elems = per * (2 if key == "f64" else 1)
+            ok = all(chunk_record(x[i * CHUNK:(i + 1) * CHUNK], s[i * CHUNK:(i + 1) * CHUNK],
+                                  ws[i * CHUNK:(i + 1) * CHUNK], elems) == chunks[c0 + i]
+                     for i in range(nc))
+            res = {"checked": True, "ok_rank0": ok, "streams": count, "values_per_stream": per,
+                   "golden": f"tests/golden/full_size.json {key} chunks [{c0}, {c0 + nc})",
+                   "method": "fresh ensemble, xg_digest_u32 per stream (xor, sum, weighted sum) "
+                             "vs digests of the reference's own words"}
+            del buf
+    elif wl == "mc_pi":
+        hits_g = fs["mc"]["chunk_hits"]
+        c0, nc = first // CHUNK, count // CHUNK
+        spp = fs["mc"]["samples_per_stream"]
+        e = xg.BlockEnsemble(p, 1, count, 63, first_stream=first, device=local)
+        h = e.mc_pi(spp)
+        mine = int(h.item())
+        ok = mine == sum(hits_g[c0:c0 + nc])
+        if world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([mine], dtype=torch.int64, device=_coll_device())
+            dist.all_reduce(t)
+            ok = ok and int(t.item()) == fs["mc"]["total_hits_2p32"]
+        res = {"checked": True, "ok_rank0": ok, "samples_per_stream": spp,
+               "total_samples": spp * (1 << 17),
+               "golden": "tests/golden/full_size.json mc (exact hits, 2^32 samples over the "
+                         "2^17 streams)",
+               "method": "fresh ensemble, exact hit count per rank slice + all-reduced total"}
+    else:
+        res["why"] = "no full-size golden for this workload (see tests/)"
+    if res["checked"]:
+        res["ok"] = all_ok(res["ok_rank0"], world)
+        del res["ok_rank0"]
+    else:
+        all_ok(True, world)  # keep the collective sequence aligned across ranks
+    return res
+
+
+def write_ceiling(out, stream, reps: int = 5) -> dict:
+    """Write-only HBM ceilings on the same buffer, same run (libxg_probe.so):
+    memset, the fill's store shape (one warp per row, 8- or 16-byte stores,
+    4 rows per CTA, <= 4 resident CTAs per SM) and a grid-stride stream."""
+    import ctypes
+
+    import torch
+
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_1108_0486_b200", "lib", "libxg_probe.so"))
+    vp = ctypes.c_void_p
+    lib.xg_probe_memset.argtypes = [vp, ctypes.c_size_t, vp]
+    lib.xg_probe_rows.argtypes = [vp, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+                                  ctypes.c_int, vp]
+    lib.xg_probe_gridstride.argtypes = [vp, ctypes.c_size_t, vp]
+    nbytes = out.numel() * out.element_size()
+    row = out.shape[1] * out.element_size()
+    ptr, sp = vp(out.data_ptr()), vp(stream.cuda_stream)
+    shapes = {
+        "memset": lambda: lib.xg_probe_memset(ptr, nbytes, sp),
+        "rows_stg64_4w_cap4": lambda: lib.xg_probe_rows(ptr, nbytes, row, 8, 4, 4, sp),
+        "rows_stg128_4w_cap4": lambda: lib.xg_probe_rows(ptr, nbytes, row, 16, 4, 4, sp),
+        "rows_stg128_8w_nocap": lambda: lib.xg_probe_rows(ptr, nbytes, row, 16, 8, 0, sp),
+        "gridstride_stg128": lambda: lib.xg_probe_gridstride(ptr, nbytes, sp),
+    }
+    res = {}
+    for name, fn in shapes.items():
+        for _ in range(3):
+            fn()
+        best = float("inf")
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rc = fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if rc:
+                break
+            best = min(best, e0.elapsed_time(e1))
+        if best < float("inf"):
+            res[name] = nbytes / (best / 1e3) / 1e9
+    return res
+
+
+def make_step(wl, ens, count, per, world, local):
+    """The step function and its buffers."""
+    import torch
+
+    dev = f"cuda:{local}"
+    ctx = {"out": None, "hits": None}
+    if wl in ("fill_u32", "fill_2p34", "stream1"):
+        out = ctx["out"] = torch.empty((count, per), dtype=torch.uint32, device=dev)
+        fn = lambda: ens.fill_u32(per, out=out)  # noqa: E731
+    elif wl == "fill_f32":
+        out = ctx["out"] = torch.empty((count, per), dtype=torch.float32, device=dev)
+        fn = lambda: ens.fill_f32(per, out=out)  # noqa: E731
+    elif wl == "fill_f64":
+        out = ctx["out"] = torch.empty((count, per), dtype=torch.float64, device=dev)
+        fn = lambda: ens.fill_f64(per, out=out)  # noqa: E731
+    elif wl == "skip":  # generator core only (no stores): the integer-issue ceiling
+        fn = lambda: ens.skip(per)  # noqa: E731
+    elif wl == "lc":
+        hits = ctx["hits"] = torch.zeros(1001, dtype=torch.int64, device=dev)
+        fn = lambda: ens.linear_complexity_test(1000, per, hist=hits)  # noqa: E731
+    elif wl == "rank":
+        hits = ctx["hits"] = torch.zeros(3, dtype=torch.int64, device=dev)
+        fn = lambda: ens.rank_test(per, counts=hits)  # noqa: E731
+    else:  # mc_pi: per-rank hits, then the job's one collective, inside the step
+        hits = ctx["hits"] = torch.zeros(1, dtype=torch.int64, device=dev)
+        total = ctx["total"] = torch.zeros(1, dtype=torch.int64, device=dev)
+        if world > 1:
+            import torch.distributed as dist
+
+            def fn():
+                hits.zero_()
+                ens.mc_pi(per, hits=hits)
+                total.copy_(hits)
+                dist.all_reduce(total)  # NCCL uint64 sum over the job, every step
+        else:
+            def fn():
+                hits.zero_()
+                ens.mc_pi(per, hits=hits)
+                total.copy_(hits)
+    return fn, ctx
+
+
+def alu_ceiling(wl: str, sm_mhz, sms: int):
+    """Integer-pipe ceiling of an in-register workload: ALU warp-instructions
+    per word from the committed ncu capture (sm__inst_executed_pipe_alu.sum /
+    words of that launch) at the measured 2 ALU warp-instructions per SM per
+    clock (profiles/README.md, micro-benchmark) and the live SM clock."""
+    n = load_ncu(wl)
+    per_word = n.get("alu_warp_inst_per_word")
+    if not per_word or not sm_mhz:
+        return None, n
+    return 2.0 * sms * sm_mhz * 1e6 / per_word, n
+
+
+def run_workload(wl, steps, warmup, world, rank, local, hbm_peak, peak_src):
+    """Time one workload; returns (entry dict, step fn, ctx, ensemble)."""
+    import torch
+
+    import paper_1108_0486_b200 as xg
+
+    stream = torch.cuda.current_stream()
+    p = xg.xorgensgp32_params()
+    first, count, per, scaling, job_words = workload_geometry(wl, world, rank)
+    ens = xg.BlockEnsemble(p, 1, count, 63, first_stream=first, device=local)
+    fn, ctx = make_step(wl, ens, count, per, world, local)
+    with ClockSampler(local) as clk:
+        total_ms, step_ms, launches = timed_loop(fn, stream, steps, warmup, world,
+                                                 counter=xg.kernel_launches)
+    t_max = max_over_ranks(total_ms, world)
+    value = job_words * steps / (t_max / 1e3)
+    kern_ms = statistics.mean(step_ms)
+    clocks = clk.summary()
+    entry = {"metric": METRIC, "value": value, "unit": "RN/s", "n_gpus": world, "steps": steps,
+             "warmup": warmup, "ms_per_step": t_max / steps, "scaling": scaling,
+             "dtype": {"fill_f32": "u32->f32", "fill_f64": "u32->f64"}.get(wl, "u32"),
+             "config": config_for(wl, world), "gpu_launches": launches, "clocks": clocks,
+             "step_ms_median": statistics.median(step_ms), "step_ms_min": min(step_ms),
+             "step_ms_cv": (statistics.pstdev(step_ms) / kern_ms) if len(step_ms) > 1 else 0.0}
+    vals = count * per
+    if wl in BYTES_PER_VAL and wl != "stream1":
+        # algorithmic bytes of the launch: output + the 129-word state read and
+        # written back per stream
+        alg = vals * BYTES_PER_VAL[wl] + 2 * count * 129 * 4
+        achieved = alg / (kern_ms / 1e3) / 1e9
+        entry["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                             "frac": achieved / hbm_peak,
+                             "traffic": load_ncu(wl).get("dram_bytes_per_launch"),
+                             "peak_source": peak_src, "alg_bytes_per_launch": alg,
+                             "kernel_ms_mean": kern_ms, "kernel_ms_min": min(step_ms),
+                             "kernel": "pair_kernel<GP32, %s>" % {"fill_f32": "kF32",
+                                                                 "fill_f64": "kF64"}.get(wl, "kU32")}
+    elif wl == "stream1":
+        entry["roofline"] = {"bound": "latency (one warp per stream)", "achieved": value / world,
+                             "peak": None, "unit": "RN/s per GPU", "frac": None, "traffic": None,
+                             "kernel_ms_mean": kern_ms}
+    else:
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        ceil, n = alu_ceiling(wl, clocks.get("sm_mhz"), sms)
+        words_per_gpu_s = vals * WORDS_PER_VAL.get(wl, 1) / (kern_ms / 1e3)
+        entry["roofline"] = {
+            "bound": "alu-pipe (integer, in-register)", "achieved": words_per_gpu_s,
+            "peak": ceil, "unit": "RN/s per GPU", "frac": (words_per_gpu_s / ceil) if ceil else None,
+            "traffic": n.get("dram_bytes_per_launch"),
+            "peak_model": "2 ALU warp-instr/SM/clk x SMs x live SM clock / ALU warp-instr per word "
+                          f"({n.get('alu_warp_inst_per_word')}, ncu)",
+            "alu_pipe_pct_ncu": n.get("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+            "issue_active_pct_ncu": n.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "kernel_ms_mean": kern_ms}
+    if wl == "mc_pi":
+        total = int(ctx["total"].item())
+        samples_last = (1 << 40)
+        entry["mc"] = {"hits_last_step": total, "samples_per_step": samples_last,
+                       "pi_estimate": 4.0 * total / samples_last,
+                       "abs_err_over_sigma": abs(4.0 * total / samples_last - 3.141592653589793)
+                       / (4.0 * (0.7853981633974483 * 0.2146018366025517 / samples_last) ** 0.5),
+                       "allreduce_in_step": world > 1}
+    return entry, fn, ctx, ens
+
+
+# --------------------------------------------------------------------------
+# CPU baselines (rank 0, N = 1) and the reference arm: the reference's own
+# code (oracle/_ref) on the host cores.
+# --------------------------------------------------------------------------
+
+def _host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def reference_generate_rate(streams: int, per_block: int, trials: int, warmup: int = 1,
+                            budget_s: float = 60.0, min_trials: int = 3):
+    """BlockEnsemble(p, 1, streams, 63).generate(per_block) on all host
+    threads, wall clock around generate() as measure_ensemble_throughput
+    (proj/src/bench.cpp:95-112)."""
+    from oracle import REF_SO, Oracle, Reference
+
+    threads = _host_threads()
+    if os.path.exists(REF_SO):
+        ref = Reference()
+        p = Oracle().gp32()
+        h = ref.ensemble(p, 1, streams, 63)
+        rates = []
+        t0 = time.perf_counter()
+        for i in range(warmup + trials):
+            secs, _ = ref.generate_timed(h, per_block, threads)
+            if i >= warmup:
+                rates.append(streams * per_block / secs)
+            if time.perf_counter() - t0 > budget_s and len(rates) >= min_trials:
+                break
+        ref.destroy(h)
+        kind = "reference"
+    else:  # the C restatement, when the reference could not be compiled
+        o = Oracle()
+        e = o.ensemble(1, streams)
+        rates = []
+        for i in range(warmup + trials):
+            t = time.perf_counter()
+            e.fill_u32(per_block)
+            dt = time.perf_counter() - t
+            if i >= warmup:
+                rates.append(streams * per_block / dt)
+        kind = "port"
+    med = statistics.median(rates)
+    return {"value": med, "unit": "RN/s", "cores": threads, "kind": kind,
+            "sample": f"BlockEnsemble(xorgensgp32, base_seed=1, blocks={streams}, lanes=63)"
+                      f".generate({per_block}) = {streams * per_block} words per trial (the full "
+                      f"config), {len(rates)} trials after {warmup} warm-up, workers={threads}, "
+                      f"wall clock around generate() (proj/src/bench.cpp:95-112); value = median",
+            "cpu_model": cpu_model(), "trials": len(rates), "mean": statistics.mean(rates),
+            "median": med, "min": min(rates), "max": max(rates),
+            "cv": statistics.pstdev(rates) / statistics.mean(rates) if len(rates) > 1 else 0.0}
+
+
+def _threaded(fn, first: int, count: int, piece: int):
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=_host_threads()) as ex:
+        return list(ex.map(lambda f: fn(f, min(piece, first + count - f)),
+                           range(first, first + count, piece)))
+
+
+def cpu_baseline_for(wl: str) -> dict:
+    """Bounded CPU samples of each workload on all host threads."""
+    from oracle import Oracle, Reference
+
+    threads = _host_threads()
+    o = Oracle()
+    p = o.gp32()
+    if wl == "fill_u32":
+        cb = reference_generate_rate(CHUNK, 1 << 16, trials=10, warmup=1, budget_s=25.0)
+        try:
+            cb["serial_1core_rn_per_s"] = Reference().serial_rate(1, 10**8, 20)
+            cb["serial_sample"] = ("XorgensState(xorgensgp32, 1): 10^8 next_word, best chunk of 20 "
+                                   "(measure_throughput, proj/src/bench.cpp:67-93): config 1")
+        except Exception:  # noqa: BLE001
+            pass
+        return cb
+    if wl in ("fill_f32", "fill_f64"):
+        # The reference has no conversions: the C restatement's words + the
+        # same conversion, all threads (kind "port").
+        streams, per = 4096, 1 << 16
+        o.threads = threads
+        e = o.ensemble(1, streams)
+        f = e.fill_f32 if wl == "fill_f32" else e.fill_f64
+        f(1024)
+        t = time.perf_counter()
+        f(per)
+        dt = time.perf_counter() - t
+        words = streams * per * (2 if wl == "fill_f64" else 1)
+        return {"value": words / dt, "unit": "RN/s", "cores": threads, "kind": "port",
+                "values_per_s": streams * per / dt, "cpu_model": cpu_model(),
+                "sample": f"oracle/xg_oracle.c ensemble {streams} streams x {per} values "
+                          f"({wl[5:]} conversion of DESIGN.md section 3; the reference has none), "
+                          f"{threads} threads"}
+    ref = Reference()
+    if wl == "fill_2p34":
+        streams, per = 2048, 1 << 16
+        t = time.perf_counter()
+        _threaded(lambda f, c: ref.streams_xor(p, 1, f, c, per), 0, streams, 64)
+        dt = time.perf_counter() - t
+        return {"value": streams * per / dt, "unit": "RN/s", "cores": threads, "kind": "reference",
+                "cpu_model": cpu_model(),
+                "sample": f"{streams} per-stream XorgensState loops (proj/src/xorgens.cpp) of the "
+                          f"2^34 config's streams x {per} words, {threads} threads "
+                          "(BASELINE.md: generate() would need 128 GiB)"}
+    if wl == "mc_pi":
+        streams, spp = 2048, 1 << 15
+        t = time.perf_counter()
+        parts = _threaded(lambda f, c: ref.stream_digests(p, 1, f, c, 0, 0, spp)["mc"], 0, streams, 64)
+        dt = time.perf_counter() - t
+        hits = int(sum(int(x.sum()) for x in parts))
+        return {"value": 2 * streams * spp / dt, "unit": "RN/s", "cores": threads,
+                "kind": "reference", "cpu_model": cpu_model(),
+                "samples_per_s": streams * spp / dt, "hits": hits,
+                "sample": f"reference XorgensState words of {streams} streams x {spp} samples + "
+                          f"the exact integer predicate, {threads} threads (reduced N)"}
+    if wl == "stream1":
+        return {"value": Reference().serial_rate(1, 10**8, 20), "unit": "RN/s", "cores": 1,
+                "kind": "reference", "cpu_model": cpu_model(),
+                "sample": "XorgensState(xorgensgp32, 1): 10^8 next_word in 20 chunks, best "
+                          "chunk rate (measure_throughput, proj/src/bench.cpp:67-93)"}
+    return {"value": None, "unavailable": f"no CPU baseline for {wl}"}
+
+
+def run_reference_arm(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    # The exact per-GPU config of our arm: 2^14 streams x 2^16 words per
+    # generate() (8 GiB of vector<uint64_t>).
+    base = reference_generate_rate(CHUNK, 1 << 16, trials=max(1, args.steps), warmup=args.warmup,
+                                   budget_s=150.0)
+    v = base["value"]
+    line = {
+        "impl": "reference", "metric": METRIC,
+        "value": v, "unit": "RN/s", "n_gpus": world, "steps": base["trials"], "warmup": args.warmup,
+        "ms_per_step": CHUNK * (1 << 16) / v * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded generator state; no input data)",
+        "config": config_for("fill_u32", world),
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
+                                              "median", "mean", "cv", "min", "max", "trials")},
+        "e2e": {"value": v, "unit": "RN/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+
+def sustained(fn, stream, seconds: float, world: int, local: int, words_per_step: int) -> dict:
+    """The same step back to back for ~`seconds` (power-capped steady state),
+    timed with CUDA events; clocks sampled throughout."""
+    import torch
+
+    t0 = time.perf_counter()
+    steps = 0
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        while True:
+            for _ in range(100):
+                fn()
+            steps += 100
+            if time.perf_counter() - t0 > seconds:
+                break
+            if steps % 1000 == 0:
+                torch.cuda.synchronize()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    ms = max_over_ranks(e0.elapsed_time(e1), world)
+    return {"value": words_per_step * steps / (ms / 1e3), "steps": steps, "ms_per_step": ms / steps,
+            "clocks": clk.summary()}
+
+
+def dry_run(args) -> int:
+    """CPU-only check of the N-rank plumbing (gloo): world, ranks, slices."""
+    world, rank, _ = dist_setup(dry=True)
+    geo = {wl: workload_geometry(wl, world, rank) for wl in ("fill_u32", "fill_2p34", "mc_pi")}
+    t = max_over_ranks(float(rank + 1), world)
+    if world > 1:
+        import torch.distributed as dist
+
+        g = [None] * world
+        dist.all_gather_object(g, geo)
+    else:
+        g = [geo]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "gpus_requested": args.gpus,
+                          "max_over_ranks": t, "comm": comm_info(world), "slices": g}), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0 if world == args.gpus else 1
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1,
-                    help="GPUs in the job; N>1 runs under torchrun (one rank per GPU)")
+                    help="GPUs in the job; N > 1 runs one rank per GPU (self-launched under "
+                         "torch.distributed.run when WORLD_SIZE is unset)")
     ap.add_argument("--steps", type=int, default=None,
                     help="timed steps (default: 200 for fills, 5 for mc_pi)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="fill_u32",
-                    choices=["fill_u32", "fill_f32", "fill_f64", "fill_2p34", "mc_pi", "skip", "stream1",
-                             "rank", "lc"])
+    ap.add_argument("--workload", default="fill_u32", choices=WORKLOADS)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the extra_workloads block")
+    ap.add_argument("--sustained-s", type=float, default=3.0,
+                    help="seconds of back-to-back steps for the sustained rate (0 = skip)")
+    ap.add_argument("--dry-run", action="store_true", help="CPU-only check of the N-rank plumbing")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.steps is None:
-        args.steps = 5 if args.workload == "mc_pi" else (10 if args.impl == "reference" else 500)
+        args.steps = 5 if args.workload == "mc_pi" else (10 if args.impl == "reference" else 200)
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
+    if args.dry_run:
+        return dry_run(args)
 
     import torch
 
     import paper_1108_0486_b200 as xg
 
     world, rank, local = dist_setup()
-    if args.gpus != world and rank == 0:
-        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with torchrun",
-              file=sys.stderr)
+    if args.gpus != world:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     stream = torch.cuda.current_stream()
-    p = xg.xorgensgp32_params()
     wl = args.workload
     hbm_peak, peak_src = load_peaks()
 
-    first, count, per, scaling, job_words_per_step = workload_geometry(wl, world, rank)
-    ens = xg.BlockEnsemble(p, 1, count, 63, first_stream=first, device=local)
-
-    out = None
-    bytes_per_val = {"fill_u32": 4, "fill_f32": 4, "fill_f64": 8, "fill_2p34": 4, "mc_pi": 0,
-                     "skip": 0, "stream1": 4, "rank": 0, "lc": 0}[wl]
-    words_per_val = {"fill_f64": 2, "mc_pi": 2, "rank": 32, "lc": 1000 / 32}.get(wl, 1)
-    if wl in ("fill_u32", "fill_2p34", "stream1"):
-        out = torch.empty((count, per), dtype=torch.uint32, device="cuda")
-        fn = lambda: ens.fill_u32(per, out=out)  # noqa: E731
-    elif wl == "fill_f32":
-        out = torch.empty((count, per), dtype=torch.float32, device="cuda")
-        fn = lambda: ens.fill_f32(per, out=out)  # noqa: E731
-    elif wl == "fill_f64":
-        out = torch.empty((count, per), dtype=torch.float64, device="cuda")
-        fn = lambda: ens.fill_f64(per, out=out)  # noqa: E731
-    elif wl == "skip":  # generator core only (no stores): the integer-issue ceiling
-        hits = None
-        fn = lambda: ens.skip(per)  # noqa: E731
-    elif wl == "lc":  # linear complexity test: words to a buffer, Berlekamp-Massey per block
-        hits = torch.zeros(1001, dtype=torch.int64, device="cuda")
-        fn = lambda: ens.linear_complexity_test(1000, per, hist=hits)  # noqa: E731
-    elif wl == "rank":  # fused matrix-rank test: bins only, no HBM traffic
-        hits = torch.zeros(3, dtype=torch.int64, device="cuda")
-        fn = lambda: ens.rank_test(per, counts=hits)  # noqa: E731
-    else:
-        hits = torch.zeros(1, dtype=torch.int64, device="cuda")
-        fn = lambda: ens.mc_pi(per, hits=hits)  # noqa: E731
-
-    vals_per_step = count * per
-    words_per_step = vals_per_step * words_per_val
-    with ClockSampler(local) as clk:
-        total_ms, step_ms, launches = timed_loop(fn, stream, args.steps, args.warmup, world,
-                                                 counter=xg.kernel_launches)
-    t_max = max_over_ranks(total_ms, world)
-    value = job_words_per_step * args.steps / (t_max / 1e3)
-    kern_ms = statistics.mean(step_ms)
-    state_bytes = 2 * count * 129 * 4                     # window + weyl read and written back
-    alg_bytes = vals_per_step * bytes_per_val + state_bytes
-
-    result = {
-        "metric": "RN/s (32-bit, device-timed) at 1/2/4/8 B200; % of HBM write BW",
-        "value": value, "unit": "RN/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-        "scaling": scaling, "vs_baseline": None,
-        "dtype": {"fill_f32": "u32->f32", "fill_f64": "u32->f64"}.get(wl, "u32"),
-        "data": "synthetic (seeded generator state; no input data)",
-        "config": {"workload": {
-            "fill_u32": "xorgensGP fill of 2^30 uint32 per GPU, bit-exact vs CPU per stream",
-            "fill_f32": "uniform float32 [0,1) fill of 2^30 values per GPU, fused conversion",
-            "fill_f64": "uniform float64 [0,1) fill of 2^30 values (2^31 words) per GPU, fused conversion",
-            "fill_2p34": "disjoint-stream fill of 2^34 uint32 across N GPUs",
-            "mc_pi": "fused in-register Monte Carlo pi, 2^40 samples across N GPUs",
-            "skip": "generator core only (advance 2^30 words, no stores)",
-            "stream1": "one stream per GPU (BASELINE config 1: seed 1, 10^8 uint32), one warp",
-            "rank": "fused GF(2) 32x32 matrix-rank test (reference matrix_rank_test), "
-                    "2^14 streams x 2^12 matrices per GPU",
-            "lc": "linear complexity test (reference linear_complexity_test, K = 1000), "
-                  "2^14 streams x 256 blocks per GPU"}[wl],
-            "params": "xorgensgp32 (128,65,15,14,12,17) w=32", "base_seed": 1,
-            "streams_per_gpu": count, "values_per_stream": per,
-            "layout": "block-major out[g*per_stream+k]",
-            "l2": "output per step >> 126 MB L2 (no flush needed)" if bytes_per_val else
-                  "no HBM traffic (in-register consumer)",
-            "parallelism": f"dp{world} (disjoint stream ranges, no data-path collective)"},
-        "gpu_launches": launches,
-        "clocks": clk.summary(),
-    }
-    if wl == "stream1":
-        # One warp: the dependency chain of the recurrence, not HBM, bounds it.
-        result["roofline"] = {"bound": "latency (one warp per stream)", "achieved": value / world,
-                              "peak": None, "unit": "RN/s per GPU", "frac": None, "traffic": None,
-                              "kernel_ms_mean": kern_ms}
-    elif bytes_per_val:
-        achieved = alg_bytes / (kern_ms / 1e3) / 1e9
-        result["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                              "frac": achieved / hbm_peak, "traffic": load_traffic(wl),
-                              "peak_source": peak_src,
-                              "alg_bytes_per_launch": alg_bytes,
-                              "kernel_ms_mean": kern_ms, "kernel_ms_min": min(step_ms)}
-        # write-only ceiling on the same buffer, same run (context for frac)
-        if out is not None:
-            try:
-                result["roofline"]["write_only_probe_gbs"] = write_probe_gbs(out, stream)
-            except OSError:
-                pass
-    elif wl == "lc":
-        import paper_1108_0486_b200 as xg_
-
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.all_reduce(hits)
-        chi2, pv = xg_.linear_complexity_statistic(hits, 1000)
-        result["lc"] = {"blocks": int(hits.sum().item()), "chi2": chi2, "p_value": pv,
-                        "blocks_per_s": value / (1000 / 32), "kernel_ms_mean": kern_ms}
-        result["roofline"] = {"bound": "int-issue (Berlekamp-Massey, one warp per block)",
-                              "achieved": value / world, "peak": None, "unit": "RN/s per GPU",
-                              "frac": None, "traffic": None}
-    elif wl == "rank":
-        import paper_1108_0486_b200 as xg_
-
-        if world > 1:
-            import torch.distributed as dist
-
-            dist.all_reduce(hits)
-        c = [int(v) for v in hits.tolist()]
-        chi2, pv = xg_.matrix_rank_statistic(c)
-        result["rank"] = {"counts_rank32_31_le30": c, "chi2": chi2, "p_value": pv,
-                          "matrices_per_s": value / 32, "kernel_ms_mean": kern_ms}
-        pipes = load_ncu(wl)
-        result["roofline"] = {
-            "bound": "int-issue", "achieved": value / world, "peak": None, "unit": "RN/s per GPU",
-            "frac": None, "traffic": load_traffic(wl),
-            "alu_pipe_pct": pipes.get("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
-            "issue_active_pct": pipes.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-            "pipe_source": "profiles/ncu_summary.json (ncu --set full)"}
-    elif wl == "skip":
-        result["roofline"] = {"bound": "int-issue", "achieved": value / world, "peak": None,
-                              "unit": "RN/s per GPU", "frac": None, "traffic": None,
-                              "kernel_ms_mean": kern_ms}
-    else:
-        # in-register consumer: report integer-issue context
-        hits_v = int(hits.item())
-        if world > 1:
-            import torch.distributed as dist
-            t0 = torch.cuda.Event(enable_timing=True)
-            t1 = torch.cuda.Event(enable_timing=True)
-            t0.record(stream)
-            dist.all_reduce(hits)  # the one NCCL collective of the workload (uint64 sum)
-            t1.record(stream)
-            torch.cuda.synchronize()
-            hits_v = int(hits.item())
-            result["allreduce_ms"] = t0.elapsed_time(t1)
-        samples = (args.steps + args.warmup) * (1 << 40)
-        result["mc"] = {"hits": hits_v, "samples": samples, "pi_estimate": 4.0 * hits_v / samples,
-                        "kernel_ms_mean": kern_ms}
-        # In-register consumer: no HBM roofline.  The ceiling is the integer
-        # pipes; report their ncu utilisation (profiles/ncu_summary.json).
-        pipes = load_ncu(wl)
-        result["roofline"] = {
-            "bound": "int-issue", "achieved": value / world, "peak": None, "unit": "RN/s per GPU",
-            "frac": None, "traffic": load_traffic(wl),
-            "alu_pipe_pct": pipes.get("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
-            "issue_active_pct": pipes.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-            "pipe_source": "profiles/ncu_summary.json (ncu --set full)"}
-
+    entry, fn, ctx, ens = run_workload(wl, args.steps, args.warmup, world, rank, local, hbm_peak,
+                                       peak_src)
+    first, count, per, _, job_words = workload_geometry(wl, world, rank)
+    result = {"metric": METRIC, "value": entry.pop("value"), "unit": "RN/s", "n_gpus": world,
+              "steps": args.steps, "warmup": args.warmup, "ms_per_step": entry.pop("ms_per_step"),
+              "higher_is_better": True, "scaling": entry.pop("scaling"), "vs_baseline": None,
+              "dtype": entry.pop("dtype"), "data": "synthetic (seeded generator state; no input data)",
+              "config": entry.pop("config"), "gpu_launches": entry.pop("gpu_launches"),
+              "clocks": entry.pop("clocks"), "roofline": entry.pop("roofline"),
+              "comm": comm_info(world), "host_cpu": cpu_model()}
+    for k in ("step_ms_median", "step_ms_min", "step_ms_cv", "mc"):
+        if k in entry:
+            result[k] = entry[k]
+    out = ctx.get("out")
+    if out is not None and wl in ("fill_u32", "fill_f32", "fill_f64", "fill_2p34"):
+        try:
+            wc = write_ceiling(out, stream)
+            best = max(wc.values())
+            ach = result["roofline"]["achieved"]
+            result["roofline"].update({"write_ceiling_gbs": best, "frac_vs_write_ceiling": ach / best,
+                                       "write_probes_gbs": wc})
+        except OSError:
+            pass
+    if wl == "fill_u32" and args.sustained_s > 0:
+        result["sustained"] = sustained(fn, stream, args.sustained_s, world, local, job_words)
     # e2e through the public host API (generate into pinned host memory)
     if not args.no_e2e and wl == "fill_u32":
         host = torch.empty((count, per), dtype=torch.uint32, pin_memory=True)
         e2e_steps = max(3, min(args.steps, 5))
-        for _ in range(1):
-            ens.generate_into_host(per, host)
+        ens.generate_into_host(per, host)
         barrier(world)
         t = time.perf_counter()
         for _ in range(e2e_steps):
             ens.generate_into_host(per, host)
         dt = max_over_ranks(time.perf_counter() - t, world)
-        result["e2e"] = {"value": words_per_step * world * e2e_steps / dt, "unit": "RN/s",
-                         "h2d_bytes_per_step": 0, "d2h_bytes_per_step": words_per_step * 4,
+        result["e2e"] = {"value": count * per * world * e2e_steps / dt, "unit": "RN/s",
+                         "h2d_bytes_per_step": 0, "d2h_bytes_per_step": count * per * 4,
                          "api": "BlockEnsemble.generate -> xg_generate_host (pinned host buffer)",
                          "steps": e2e_steps}
         del host
-    if rank == 0 and world == 1 and not args.no_cpu and wl == "lc":
+    result["parity"] = parity_check(wl, world, rank, local, out=out)
+    del ens, ctx, fn, out
+    torch.cuda.empty_cache()
+    if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            from oracle import Battery, Oracle
-
-            nb = 3000  # bounded sample: 3e6 bits through the reference's own test
-            words = Oracle().ensemble(1, 1).fill_u32(nb * 1000 // 32)[0]
-            t0 = time.perf_counter()
-            Battery().linear_complexity(words, 1000, nb)
-            dt = time.perf_counter() - t0
-            result["cpu_baseline"] = {
-                "value": nb * 1000 / 32 / dt, "unit": "RN/s", "cores": 1, "kind": "reference",
-                "sample": f"reference linear_complexity_test (proj/src/stattests/tests.cpp:128-178), "
-                          f"{nb} blocks of 1000 bits of one stream, 1 thread (serial in the reference)",
-                "blocks_per_s": nb / dt}
+            result["cpu_baseline"] = cpu_baseline_for(wl)
         except Exception as e:  # noqa: BLE001
             result["cpu_baseline"] = {"value": None, "unavailable": str(e)}
-    if rank == 0 and world == 1 and not args.no_cpu and wl == "rank":
-        try:
-            from oracle import Battery, Oracle
 
-            m = 200_000  # bounded sample: 6.4e6 words through the reference's own test
-            words = Oracle().ensemble(1, 1).fill_u32(32 * m)[0]
-            t0 = time.perf_counter()
-            Battery().matrix_rank(words, m)
-            dt = time.perf_counter() - t0
-            result["cpu_baseline"] = {
-                "value": 32 * m / dt, "unit": "RN/s", "cores": 1, "kind": "reference",
-                "sample": f"reference matrix_rank_test (proj/src/stattests/tests.cpp:81-126) over "
-                          f"{m} 32x32 matrices of one stream, 1 thread (the reference test is serial)",
-                "matrices_per_s": m / dt}
-        except Exception as e:  # noqa: BLE001
-            result["cpu_baseline"] = {"value": None, "unavailable": str(e)}
-    if rank == 0 and world == 1 and not args.no_cpu and wl == "stream1":
-        try:
-            from oracle import Reference
-
-            result["cpu_baseline"] = {
-                "value": Reference().serial_rate(1, 10**8, 20), "unit": "RN/s", "cores": 1,
-                "kind": "reference",
-                "sample": "XorgensState(xorgensgp32, 1): 10^8 next_word in 20 chunks, best "
-                          "chunk rate (measure_throughput, proj/src/bench.cpp:67-93)"}
-        except Exception as e:  # noqa: BLE001
-            result["cpu_baseline"] = {"value": None, "unavailable": str(e)}
-    if rank == 0 and world == 1 and not args.no_cpu and wl in ("fill_u32", "fill_f32", "fill_f64"):
-        try:
-            cb = reference_rate(1 << 14, 1 << 14, trials=100, budget_s=10.0)
-            for k in ("trials", "min", "max"):
-                cb.pop(k, None)
-            # BASELINE config 1: one serial stream on one core, the reference's
-            # measure_throughput method (proj/src/bench.cpp:67-93), seed 1, 10^8 words.
-            try:
-                from oracle import Reference
-
-                cb["serial_1core_rn_per_s"] = Reference().serial_rate(1, 10**8, 20)
-            except Exception:  # noqa: BLE001
-                pass
-            result["cpu_baseline"] = cb
-        except Exception as e:  # noqa: BLE001
-            result["cpu_baseline"] = {"value": None, "unavailable": str(e)}
+    if wl == "fill_u32" and not args.no_extra:
+        extras = {}
+        for xw in EXTRA:
+            steps = min(args.steps, 5) if xw == "mc_pi" else args.steps
+            e, _, xctx, xens = run_workload(xw, steps, args.warmup, world, rank, local, hbm_peak,
+                                            peak_src)
+            xout = xctx.get("out")
+            if xout is not None:
+                try:
+                    wc = write_ceiling(xout, stream)
+                    e["roofline"]["write_ceiling_gbs"] = max(wc.values())
+                    e["roofline"]["frac_vs_write_ceiling"] = (e["roofline"]["achieved"] /
+                                                              max(wc.values()))
+                except OSError:
+                    pass
+            e["parity"] = parity_check(xw, world, rank, local, out=xout)
+            del xctx, xens, xout
+            torch.cuda.empty_cache()
+            if rank == 0 and world == 1 and not args.no_cpu:
+                try:
+                    e["cpu_baseline"] = cpu_baseline_for(xw)
+                except Exception as ex:  # noqa: BLE001
+                    e["cpu_baseline"] = {"value": None, "unavailable": str(ex)}
+            e.pop("metric", None)
+            extras[xw] = e
+        result["extra_workloads"] = extras
+        result["gpu_launches_all"] = result["gpu_launches"] + sum(
+            e["gpu_launches"] for e in extras.values())
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:

@@ -195,6 +195,18 @@ int xg_bits_ones_runs(const uint32_t* dev_words, uint64_t nbits, uint64_t* dev_o
  * 2 <= n_draws <= 8192, 1 <= t_bits <= 32 (XG_EINVAL otherwise). */
 int xg_birthday_duplicates(const uint32_t* dev_words, uint32_t n_draws, uint32_t rounds,
                            unsigned t_bits, uint64_t* dev_dup, xg_stream_t stream);
+/* The handle-less calls above (Berlekamp-Massey, ones/runs, birthday) and
+ * xg_digest_u32 run on the device that owns their input pointer, whatever
+ * device is current (XG_EINVAL for a host or unregistered pointer). */
+
+/* Row digests for parity checks: for each row r of a (rows x per_row)
+ * row-major buffer of 32-bit elements e_k, dev_xor[r] = xor of e_k,
+ * dev_sum[r] = sum e_k, dev_wsum[r] = sum e_k * (k + 1) (mod 2^64).  Floats
+ * are digested through their bit patterns (f64 rows as 2 * per_row u32
+ * halves).  Golden digests of the reference's streams in the same form:
+ * tests/golden/full_size.json. */
+int xg_digest_u32(const uint32_t* dev_words, uint64_t rows, uint64_t per_row, uint32_t* dev_xor,
+                  uint64_t* dev_sum, uint64_t* dev_wsum, xg_stream_t stream);
 /* Advance every stream by `words` without storing (discard). */
 int xg_skip(xg_ensemble_t h, uint64_t words, xg_stream_t stream);
 

@@ -302,6 +302,9 @@ class Reference:
                                               ctypes.POINTER(_u64)]
         L.xgref_raw_stream.argtypes = [arr, _u64, ctypes.c_uint, _u64, _u64, _vp]
         L.xgref_low_bit_windows.argtypes = [arr, _u64, ctypes.c_uint, _u64, _int, _u64, _u64, _vp, _vp]
+        L.xgref_stream_digests.argtypes = [arr, _u64, ctypes.c_uint, _u64, _u64, _u64, _u64, _u64,
+                                           _u64] + [_vp] * 10
+        L.xgref_streams_xor.argtypes = [arr, _u64, ctypes.c_uint, _u64, _u64, _u64, _u64, _vp]
         L.xgref_serial_rate.restype = ctypes.c_double
         L.xgref_serial_rate.argtypes = [_u64, _u64, ctypes.c_uint, ctypes.POINTER(_u64)]
 
@@ -383,6 +386,42 @@ class Reference:
 
     def destroy(self, h) -> None:
         self.lib.xgref_ensemble_destroy(h)
+
+    def stream_digests(self, p, base_seed: int, first: int, count: int, n_u32: int, n_f64: int = 0,
+                       n_mc: int = 0) -> dict:
+        """Per-stream digests of streams [first, first + count) (see
+        xgref_stream_digests in oracle/ref_shim.cpp): {"u32"|"f32"|"f64":
+        (xor u32[count], sum u64[count], wsum u64[count]), "mc": hits u32[count]}."""
+        out = {}
+        ptrs = []
+        for key, n in (("u32", n_u32), ("f32", n_u32), ("f64", n_f64)):
+            if n:
+                t = (np.zeros(count, np.uint32), np.zeros(count, np.uint64), np.zeros(count, np.uint64))
+                out[key] = t
+                ptrs += [_ptr(a) for a in t]
+            else:
+                ptrs += [None] * 3
+        if n_mc:
+            out["mc"] = np.zeros(count, np.uint32)
+            ptrs.append(_ptr(out["mc"]))
+        else:
+            ptrs.append(None)
+        rc = self.lib.xgref_stream_digests(self._arr(p), p.omega, p.gamma, base_seed & (2**64 - 1),
+                                           first, count, n_u32, n_f64, n_mc, *ptrs)
+        if rc:
+            raise ValueError("reference rejected the parameters")
+        return out
+
+    def streams_xor(self, p, base_seed: int, first: int, count: int, n: int) -> np.ndarray:
+        """Per-stream xor of n words of streams [first, first + count), each an
+        XorgensState loop (xgref_streams_xor); releases the GIL, so threads
+        run it on all cores."""
+        out = np.zeros(count, dtype=np.uint32)
+        rc = self.lib.xgref_streams_xor(self._arr(p), p.omega, p.gamma, base_seed & (2**64 - 1),
+                                        first, count, n, _ptr(out))
+        if rc:
+            raise ValueError("reference rejected the parameters")
+        return out
 
     def serial_rate(self, seed: int, count: int, chunks: int = 20) -> float:
         sink = ctypes.c_uint64()

@@ -174,6 +174,105 @@ int xgref_ensemble_generate(void* h, std::uint64_t per_block, unsigned workers,
     }
 }
 
+// Digests of streams [first, first + count) of BlockEnsemble(params,
+// base_seed, ...) -- stream g is XorgensState(params, base_seed + g)
+// (proj/src/parallel.cpp:84-95) -- for the full-size parity goldens.  Per
+// stream and per output, three numbers over the row's elements e_k (k = 0..):
+// xor (u32), sum e_k and sum e_k * (k + 1) (uint64 wrap).  Outputs (each
+// [count]-long, nullptr = skip):
+//   u32: the first n_u32 words;  f32: the bit patterns of (w >> 8) * 2^-24 of
+//   the same words;  f64: the n_f64 doubles (u64 >> 11) * 2^-53 with u64 = the
+//   word pair (w[2m], w[2m+1]) lo first, digested as 2 * n_f64 u32 elements
+//   (the little-endian halves);  mc: hits of the first n_mc samples (pair m,
+//   signed coordinates, hit iff x^2 + y^2 < 2^62).  The conversions are the
+//   DESIGN.md section 3 conventions applied to reference words (the reference
+//   has none of its own); every generated word comes from next_word().
+struct Digest3 {
+    std::uint32_t x = 0;
+    std::uint64_t s = 0, ws = 0, k = 0;
+    void add(std::uint32_t v) {
+        x ^= v;
+        s += v;
+        ws += static_cast<std::uint64_t>(v) * ++k;
+    }
+};
+
+int xgref_stream_digests(const unsigned* rsabcdw, std::uint64_t omega, unsigned gamma,
+                         std::uint64_t base_seed, std::uint64_t first, std::uint64_t count,
+                         std::uint64_t n_u32, std::uint64_t n_f64, std::uint64_t n_mc,
+                         std::uint32_t* u32_x, std::uint64_t* u32_s, std::uint64_t* u32_ws,
+                         std::uint32_t* f32_x, std::uint64_t* f32_s, std::uint64_t* f32_ws,
+                         std::uint32_t* f64_x, std::uint64_t* f64_s, std::uint64_t* f64_ws,
+                         std::uint32_t* mc_hits) {
+    try {
+        const auto p = to_params(rsabcdw, omega, gamma);
+        std::uint64_t n = n_u32;
+        if (2 * n_f64 > n) n = 2 * n_f64;
+        if (2 * n_mc > n) n = 2 * n_mc;
+        for (std::uint64_t i = 0; i < count; ++i) {
+            xg::XorgensState st(p, base_seed + first + i);
+            Digest3 du, df, dd;
+            std::uint32_t hits = 0, lo = 0;
+            for (std::uint64_t k = 0; k < n; ++k) {
+                const auto w = static_cast<std::uint32_t>(st.next_word());
+                if (k < n_u32) {
+                    du.add(w);
+                    const float f = static_cast<float>(w >> 8) * 0x1p-24f;
+                    std::uint32_t fb;
+                    std::memcpy(&fb, &f, 4);
+                    df.add(fb);
+                }
+                if ((k & 1) == 0) {
+                    lo = w;
+                    continue;
+                }
+                const std::uint64_t m = k >> 1;
+                if (m < n_f64) {
+                    const std::uint64_t u = lo | (static_cast<std::uint64_t>(w) << 32);
+                    const double d = static_cast<double>(u >> 11) * 0x1p-53;
+                    std::uint64_t db;
+                    std::memcpy(&db, &d, 8);
+                    dd.add(static_cast<std::uint32_t>(db));
+                    dd.add(static_cast<std::uint32_t>(db >> 32));
+                }
+                if (m < n_mc) {
+                    const std::int64_t x = static_cast<std::int32_t>(lo), y = static_cast<std::int32_t>(w);
+                    hits += static_cast<std::uint64_t>(x * x) + static_cast<std::uint64_t>(y * y) <
+                            (1ull << 62);
+                }
+            }
+            if (u32_x) { u32_x[i] = du.x; u32_s[i] = du.s; u32_ws[i] = du.ws; }
+            if (f32_x) { f32_x[i] = df.x; f32_s[i] = df.s; f32_ws[i] = df.ws; }
+            if (f64_x) { f64_x[i] = dd.x; f64_s[i] = dd.s; f64_ws[i] = dd.ws; }
+            if (mc_hits) mc_hits[i] = hits;
+        }
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// Streams [first, first + count) of BlockEnsemble(params, base_seed, ...) as
+// independent XorgensState loops, n words each, every word folded into a
+// per-stream xor (the CPU baseline of the 2^34-word disjoint-stream fill:
+// per-stream states on all cores; generate() would need 128 GiB).
+int xgref_streams_xor(const unsigned* rsabcdw, std::uint64_t omega, unsigned gamma,
+                      std::uint64_t base_seed, std::uint64_t first, std::uint64_t count,
+                      std::uint64_t n, std::uint32_t* xor_out) {
+    try {
+        const auto p = to_params(rsabcdw, omega, gamma);
+        for (std::uint64_t i = 0; i < count; ++i) {
+            xg::XorgensState st(p, base_seed + first + i);
+            std::uint64_t x = 0;
+            for (std::uint64_t k = 0; k < n; ++k) x ^= st.next_word();
+            xor_out[i] = static_cast<std::uint32_t>(x);
+        }
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 // Serial next_word throughput, the measure_throughput method
 // (proj/src/bench.cpp:67-93): best chunk rate on thread CPU time.
 double xgref_serial_rate(std::uint64_t seed, std::uint64_t count, unsigned chunks,

@@ -69,6 +69,7 @@ SIGNATURES = {
     "xg_berlekamp_massey": (_int, [_vp, _u64, _u32, _u64, _vp, _vp]),
     "xg_bits_ones_runs": (_int, [_vp, _u64, _vp, _vp]),
     "xg_birthday_duplicates": (_int, [_vp, _u32, _u32, ctypes.c_uint, _vp, _vp]),
+    "xg_digest_u32": (_int, [_vp, _u64, _u64, _vp, _vp, _vp, _vp]),
     "xg_skip": (_int, [_vp, _u64, _vp]),
     "xg_generate_host": (_int, [_vp, _u64, _vp, _vp]),
     "xg_generate_host_words": (_int, [_vp, _u64, _vp, _vp]),

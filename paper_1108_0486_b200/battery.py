@@ -22,8 +22,8 @@ from typing import Dict, List
 
 from ._lib import lib
 from .pvalues import poisson_upper_tail, regularized_gamma_p, regularized_gamma_q  # noqa: F401
-from .xorgens import (BlockEnsemble, GeneratorParams, _raise, _torch, lane_bound,
-                      linear_complexity_statistic, matrix_rank_statistic)
+from .xorgens import (BlockEnsemble, GeneratorParams, UnsupportedParamsError, _raise, _torch,
+                      fast_path, lane_bound, linear_complexity_statistic, matrix_rank_statistic)
 
 __all__ = ["BatteryConfig", "run_battery_gpu", "regularized_gamma_p", "regularized_gamma_q"]
 
@@ -79,6 +79,17 @@ def run_battery_gpu(params: GeneratorParams, seed: int, config: BatteryConfig = 
     cfg = config or BatteryConfig.defaults()
     if params.w != 32:
         raise ValueError("the GPU battery reads 32-bit words")
+    if cfg.run_matrix_rank and not (fast_path(params) and params.r - params.s < 64):
+        # The fused rank test runs in the pair-lane kernel only (xg_rank_test:
+        # r = 128, r - s < 64); refuse before any test consumes the stream.
+        raise UnsupportedParamsError(
+            "the GPU matrix-rank test needs r = 128 and r - s < 64 (set run_matrix_rank=False)")
+    with torch.cuda.device(device):
+        return _run_battery(params, seed, cfg, device)
+
+
+def _run_battery(params: GeneratorParams, seed: int, cfg: BatteryConfig, device: int) -> Dict:
+    torch = _torch()
     dev = f"cuda:{device}"
     e = BlockEnsemble(params, seed, 1, lane_bound(params), device=device)
     tests: List[Dict] = []

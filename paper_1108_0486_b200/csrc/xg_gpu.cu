@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "xg_gpu.h"
+#include "xg_digest.cuh"
 #include "xg_generic.cuh"
 #include "xg_kernels.cuh"
 #include "xg_pairs.cuh"
@@ -48,6 +49,20 @@ struct DeviceGuard {
         if (prev >= 0) cudaSetDevice(prev);
     }
 };
+
+// The device that owns a device pointer (entry points without a handle run on
+// it, whatever device is current for the calling thread).  Host or
+// unregistered pointers are XG_EINVAL.
+int ptr_device(const void* p, int* dev) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return XG_EINVAL;
+    }
+    if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) return XG_EINVAL;
+    *dev = a.device;
+    return XG_OK;
+}
 
 }  // namespace
 
@@ -142,22 +157,11 @@ unsigned grid_for(uint32_t n) {
     return static_cast<unsigned>((static_cast<uint64_t>(n) + kWarpsPerBlock - 1) / kWarpsPerBlock);
 }
 
-// Kernel choice for the register-window sets: 512 (default) = the pair-lane
-// kernel (xg_pairs.cuh) wherever it applies (r - s < 64 and aligned output
-// rows), else the word-per-lane kernel with the shared-memory s-tap (VAR 16,
-// xg_kernels.cuh).  XG_VARIANT = 0, 1, 16, 48 or 144 forces a word-per-lane
-// variant for experiments (measurements in profiles/README.md).
-constexpr int kPairs = 512;
+// Kernel choice for the register-window sets: the pair-lane kernel
+// (xg_pairs.cuh) wherever it applies (r - s < 64 and aligned output rows),
+// else the word-per-lane kernel with the shared-memory s-tap (xg_kernels.cuh).
 constexpr int kFillWarpsPerCta = 4;  // u32/raw fills of large ensembles: streams per CTA
 constexpr int kFillCtasPerSm = 4;    // ... and resident CTAs per SM (launch_pair)
-
-int variant_for(int) {
-    static int forced = [] {
-        const char* e = getenv("XG_VARIANT");
-        return e ? atoi(e) : -1;
-    }();
-    return forced >= 0 ? forced : kPairs;
-}
 
 // The pair-lane kernel stores 8-byte word pairs (16 for the zero-extended
 // u64 words): every output row must start on that boundary.
@@ -189,14 +193,7 @@ int launch_pair(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count, 
     // RN/s under the power cap, 1.737e12 against 1.72e12 in bursts (r1u,
     // r1zg in profiles/README.md).  The conversions gain nothing from the cap
     // and run full (8-stream CTAs, 64 streams per SM).
-    // XG_FILL_WPB / XG_CTAS_PER_SM override CTA size / cap for experiments
-    // (the cap then applies to every output mode; 0 = none).
     constexpr bool kCapped = MODE == kU32 || MODE == kRaw;
-    constexpr bool kStores = kCapped || MODE == kF32 || MODE == kF64 || MODE == kWide;
-    static const char* wpb_env = getenv("XG_FILL_WPB");
-    static const char* cap_env = getenv("XG_CTAS_PER_SM");
-    static const uint32_t env_wpb = wpb_env ? static_cast<uint32_t>(std::clamp(atoi(wpb_env), 1, 32)) : 0;
-    static const int env_cap = cap_env ? atoi(cap_env) : 0;
     const bool large = g_count > 32 * sms;
     uint32_t wpb = kWarpsPerBlock;
     int cap = 0;
@@ -205,8 +202,6 @@ int launch_pair(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count, 
             wpb = kFillWarpsPerCta;
             cap = kFillCtasPerSm;
         }
-        if (env_wpb && std::is_same_v<P, GP32>) wpb = env_wpb;
-        if (cap_env && kStores) cap = env_cap;
     } else {
         // one CTA per SM holding ceil(P / SMs) streams (see above)
         wpb = static_cast<uint32_t>((g_count + sms - 1) / sms);  // 1..32
@@ -228,19 +223,11 @@ int launch_pair(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count, 
     return cuda_rc(cudaGetLastError());
 }
 
-HiMul himul(const xg_params_t& p) {
-    HiMul m;
-    m.gamma = 1u << (32 - p.gamma);
-    m.b = 1u << (32 - p.b);
-    m.d = 1u << (32 - p.d);
-    return m;
-}
-
-template <int MODE, int VAR, class P>
-int launch_fill_v(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count,
-                  uint64_t words, void* out, unsigned long long* hits, cudaStream_t s) {
-    fill_kernel<P, MODE, VAR><<<grid_for(g_count), kThreads, 0, s>>>(
-        p, himul(h->params), h->d_win, h->d_weyl, g_begin, g_count, words, out, hits);
+template <int MODE, class P>
+int launch_word_lane(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count,
+                     uint64_t words, void* out, unsigned long long* hits, cudaStream_t s) {
+    fill_kernel<P, MODE><<<grid_for(g_count), kThreads, 0, s>>>(p, h->d_win, h->d_weyl, g_begin,
+                                                                g_count, words, out, hits);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cuda_rc(cudaGetLastError());
 }
@@ -257,18 +244,45 @@ GenParams gen_params(const xg_params_t& p) {
 
 size_t gen_smem(const xg_params_t& p) { return static_cast<size_t>(p.r) * sizeof(uint64_t); }
 
+// Dynamic shared-memory limit of `kernel` raised once per device, always to
+// the same value (the device's opt-in maximum, or a kernel's fixed maximum), so
+// launches make no non-stream driver call and concurrent host threads can
+// never lower the limit under one another's launch.
 template <class K>
-int gen_smem_attr(K kernel, size_t smem) {
+int raise_smem_once(K kernel, size_t bytes, std::atomic<uint64_t>& done) {
+    if (bytes <= 48 * 1024) return XG_OK;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return XG_ECUDA;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return XG_OK;
+    int rc = cuda_rc(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(bytes)));
+    if (!rc) done.fetch_or(bit, std::memory_order_acq_rel);
+    return rc;
+}
+
+int smem_optin_current() {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
+}
+
+// The generic kernels take r words of shared memory; beyond 48 KB (r > 6144)
+// their limit is raised once per device to the opt-in maximum.
+template <auto Kernel>
+int gen_smem_attr(size_t smem) {
+    static std::atomic<uint64_t> done{0};  // one flag set per kernel
     if (smem <= 48 * 1024) return XG_OK;
-    return cuda_rc(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
+    if (smem > static_cast<size_t>(smem_optin_current())) return XG_EUNSUPPORTED;
+    return raise_smem_once(Kernel, static_cast<size_t>(smem_optin_current()), done);
 }
 
 template <int GM>
 int launch_gen(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t words, void* out,
                cudaStream_t s) {
     const size_t smem = gen_smem(h->params);
-    int rc = gen_smem_attr(gen_fill_kernel<GM>, smem);
+    int rc = gen_smem_attr<&gen_fill_kernel<GM>>(smem);
     if (rc) return rc;
     gen_fill_kernel<GM><<<g_count, 32, smem, s>>>(gen_params(h->params), h->d_win64, h->d_weyl64,
                                                    g_begin, g_count, words, out);
@@ -295,35 +309,21 @@ int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t wor
         }
         return XG_EUNSUPPORTED;
     }
-    const int var = variant_for(MODE);
     if constexpr (MODE == kRank) {  // pair-lane kernel only (needs r - s < 64)
         if (h->kind == kGP32) return launch_pair<MODE>(GP32{}, h, g_begin, g_count, words, out, hits, s);
         if (h->kind == kRtJ1)
             return launch_pair<MODE>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s);
         return XG_EUNSUPPORTED;
-    } else if (var == kPairs && h->kind != kRtJ2 && pair_aligned<MODE>(out, words)) {
-        if (h->kind == kGP32) return launch_pair<MODE>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-        return launch_pair<MODE>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s);
-    }
-    switch (h->kind) {
-    case kGP32:
-        switch (var) {
-        case 0: return launch_fill_v<MODE, 0>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-        case 1: return launch_fill_v<MODE, 1>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-        case 144: return launch_fill_v<MODE, 144>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-        case 48:
-            // bulk-copy stores: 512-byte bodies need 16-byte aligned rows
-            if constexpr (MODE == kU32 || MODE == kF32 || MODE == kRaw) {
-                if ((reinterpret_cast<uintptr_t>(out) & 15u) == 0 && (words & 3u) == 0)
-                    return launch_fill_v<MODE, 48>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-            }
-            return launch_fill_v<MODE, 16>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-        default: return launch_fill_v<MODE, 16>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+    } else {
+        if (h->kind != kRtJ2 && pair_aligned<MODE>(out, words)) {
+            if (h->kind == kGP32) return launch_pair<MODE>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+            return launch_pair<MODE>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s);
         }
-    case kRtJ1:
-        return launch_fill_v<MODE, 16>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s);
-    default:
-        return launch_fill_v<MODE, 16>(rt_params<2>(h->params), h, g_begin, g_count, words, out, hits, s);
+        switch (h->kind) {
+        case kGP32: return launch_word_lane<MODE>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        case kRtJ1: return launch_word_lane<MODE>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s);
+        default: return launch_word_lane<MODE>(rt_params<2>(h->params), h, g_begin, g_count, words, out, hits, s);
+        }
     }
 }
 
@@ -353,25 +353,24 @@ void prepare_pair_kernels(xg_ensemble* h) {
 
 int launch_seed(xg_ensemble* h, uint64_t seed0, cudaStream_t s) {
     const unsigned grid = grid_for(h->num_streams);
-    const HiMul m = himul(h->params);
     switch (h->kind) {
     case kGeneric: {
         const size_t smem = gen_smem(h->params);
-        int rc = gen_smem_attr(gen_seed_kernel, smem);
+        int rc = gen_smem_attr<&gen_seed_kernel>(smem);
         if (rc) return rc;
         gen_seed_kernel<<<h->num_streams, 32, smem, s>>>(gen_params(h->params), h->d_win64,
                                                         h->d_weyl64, h->num_streams, seed0);
         break;
     }
     case kGP32:
-        seed_kernel<<<grid, kThreads, 0, s>>>(GP32{}, m, h->d_win, h->d_weyl, h->num_streams, seed0);
+        seed_kernel<<<grid, kThreads, 0, s>>>(GP32{}, h->d_win, h->d_weyl, h->num_streams, seed0);
         break;
     case kRtJ1:
-        seed_kernel<<<grid, kThreads, 0, s>>>(rt_params<1>(h->params), m, h->d_win, h->d_weyl,
+        seed_kernel<<<grid, kThreads, 0, s>>>(rt_params<1>(h->params), h->d_win, h->d_weyl,
                                              h->num_streams, seed0);
         break;
     default:
-        seed_kernel<<<grid, kThreads, 0, s>>>(rt_params<2>(h->params), m, h->d_win, h->d_weyl,
+        seed_kernel<<<grid, kThreads, 0, s>>>(rt_params<2>(h->params), h->d_win, h->d_weyl,
                                              h->num_streams, seed0);
         break;
     }
@@ -475,7 +474,8 @@ int launch_bm_long(const uint32_t* data, uint64_t data_words, uint64_t nbits, ui
                    uint32_t per_row, uint64_t row_bits, uint64_t count, unsigned long long* hist,
                    uint32_t* L_out, cudaStream_t s) {
     const size_t smem = 4ull * bm_words(nbits) * sizeof(uint32_t);
-    int rc = gen_smem_attr(bm_long_kernel, smem);
+    static std::atomic<uint64_t> done{0};
+    int rc = raise_smem_once(bm_long_kernel, 4ull * bm_words(kBmMaxBits) * sizeof(uint32_t), done);
     if (rc) return rc;
     bm_long_kernel<<<static_cast<unsigned>(count), 32, smem, s>>>(data, data_words, nbits, stride_bits,
                                                                  per_row, row_bits, hist, L_out);
@@ -745,10 +745,14 @@ int xg_linear_complexity_test(xg_ensemble_t h, unsigned block_length, uint64_t b
         const uint64_t wc = (nb * K + 31) / 32;
         const size_t need = static_cast<size_t>(P * wc) * sizeof(uint32_t);
         if (h->lc_bytes < need) {
-            cudaFree(h->d_lc);
+            // Stream-ordered (re)allocation: no device synchronisation, and
+            // capturable into a CUDA graph like the fills.  The buffer is
+            // per-handle state, ordered like the generator state itself:
+            // calls on one handle must be ordered on the host or by stream.
+            if (h->d_lc) cudaFreeAsync(h->d_lc, s);
             h->d_lc = nullptr;
             h->lc_bytes = 0;
-            rc = cuda_rc(cudaMalloc(&h->d_lc, need));
+            rc = cuda_rc(cudaMallocAsync(reinterpret_cast<void**>(&h->d_lc), need, s));
             if (rc) return rc;
             h->lc_bytes = need;
         }
@@ -776,6 +780,11 @@ int xg_berlekamp_massey(const uint32_t* dev_seqs, uint64_t nbits, uint32_t count
     if (!dev_seqs || !dev_L || nbits == 0 || nbits > kBmMaxBits) return XG_EINVAL;
     if (count == 0) return XG_OK;
     if (count > 1 && stride_words * 32 < nbits) return XG_EINVAL;
+    int dev;
+    int rc = ptr_device(dev_seqs, &dev);
+    if (rc) return rc;
+    DeviceGuard dg(dev);
+    if (!dg.ok) return XG_ECUDA;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const uint64_t data_words = static_cast<uint64_t>(count - 1) * stride_words + (nbits + 31) / 32;
     return launch_bm_long(dev_seqs, data_words, nbits, stride_words * 32, count, 0, count, nullptr,
@@ -786,6 +795,11 @@ int xg_bits_ones_runs(const uint32_t* dev_words, uint64_t nbits, uint64_t* dev_o
                       xg_stream_t stream) {
     if (!dev_words || !dev_out2 || (reinterpret_cast<uintptr_t>(dev_out2) % 8) != 0) return XG_EINVAL;
     if (nbits == 0) return XG_OK;
+    int dev;
+    int rc = ptr_device(dev_words, &dev);
+    if (rc) return rc;
+    DeviceGuard dg(dev);
+    if (!dg.ok) return XG_ECUDA;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const uint64_t nwords = (nbits + 31) / 32;
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((nwords + 255) / 256, 148 * 16));
@@ -802,9 +816,35 @@ int xg_birthday_duplicates(const uint32_t* dev_words, uint32_t n_draws, uint32_t
         n_draws > static_cast<uint32_t>(kBdThreads * kBdItems))
         return XG_EINVAL;
     if (rounds == 0) return XG_OK;
+    int dev;
+    int rc = ptr_device(dev_words, &dev);
+    if (rc) return rc;
+    DeviceGuard dg(dev);
+    if (!dg.ok) return XG_ECUDA;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     birthday_kernel<<<rounds, kBdThreads, 0, s>>>(dev_words, n_draws, 32u - t_bits,
                                                    reinterpret_cast<unsigned long long*>(dev_dup));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cuda_rc(cudaGetLastError());
+}
+
+int xg_digest_u32(const uint32_t* dev_words, uint64_t rows, uint64_t per_row, uint32_t* dev_xor,
+                  uint64_t* dev_sum, uint64_t* dev_wsum, xg_stream_t stream) {
+    if (rows == 0) return XG_OK;
+    if (!dev_words || !dev_xor || !dev_sum || !dev_wsum || rows > 0x7fffffffull) return XG_EINVAL;
+    if ((reinterpret_cast<uintptr_t>(dev_sum) | reinterpret_cast<uintptr_t>(dev_wsum)) % 8 != 0)
+        return XG_EINVAL;
+    uint64_t total;
+    if (mul_overflows(rows, per_row, &total)) return XG_EINVAL;
+    int dev;
+    int rc = ptr_device(dev_xor, &dev);
+    if (!rc && per_row) rc = ptr_device(dev_words, &dev);
+    if (rc) return rc;
+    DeviceGuard dg(dev);
+    if (!dg.ok) return XG_ECUDA;
+    digest_kernel<<<static_cast<unsigned>(rows), kDigestThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        dev_words, per_row, dev_xor, reinterpret_cast<unsigned long long*>(dev_sum),
+        reinterpret_cast<unsigned long long*>(dev_wsum));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cuda_rc(cudaGetLastError());
 }

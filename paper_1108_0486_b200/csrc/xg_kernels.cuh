@@ -1,8 +1,8 @@
 // xg_kernels.cuh -- sm_100a device code for the xorgensGP generation path:
 // the seeding kernel (K1), shared helpers, and the WORD-PER-LANE fill kernel.
 // The default fill kernel is the pair-lane kernel in xg_pairs.cuh; the one
-// here runs the J = 2 parameter sets, output rows the pair stores cannot
-// address, and the XG_VARIANT experiments.
+// here runs the J = 2 parameter sets and output rows the pair stores cannot
+// address (odd lengths / 4-byte aligned rows).
 //
 // Design: ONE WARP PER STREAM, the r = 128 word window in
 // registers.  Lane l holds logical window words W[l], W[32+l], W[64+l],
@@ -14,32 +14,19 @@
 //   x_{i+l} = T(W[l], a, b) ^ T(W[(r-s)+l], c, d)          (xorgens.hpp:39-47)
 //
 // W[l] is the lane's own R[0].  W[(r-s)+l] ((r-s) = 32*J + delta) belongs to
-// another lane: by default it is read from a per-warp shared-memory ring that
-// mirrors the window (one STS of the new block + one LDS per step), or, in the
-// VAR 0 form, taken from lane (l+delta)&31's register J or J+1 with one
-// select + one shuffle.  The new word replaces R[0] and the window rotates by
-// renaming registers (4-step unroll), so there are no moves.  The Weyl term of lane l in
+// another lane: the fill reads it from a per-warp shared-memory ring that
+// mirrors the window (one STS of the new block + one LDS per step); the seeding
+// kernel takes it from lane (l+delta)&31's register J or J+1 with one select +
+// one shuffle.  The new word replaces R[0] and the window rotates by renaming
+// registers (4-step unroll), so there are no moves.  The Weyl term of lane l in
 // step k is weyl + (32k + l + 1)*omega (closed form, parallel.cpp:33-39), and
 // the output is ((w ^ (w >> gamma)) + x) mod 2^32 (xorgens.hpp:58-62).
 //
-// Issue-slot budget (measured, profiles/README.md): the loop is integer-ALU
-// bound.  The VAR template mask selects instruction-placement variants that
-// were measured (XG_VARIANT overrides the default, 16):
-//   bit 0/1/2  Weyl >> gamma, t >> b, t >> d as IMAD.HI by a runtime power of
-//              two on the FMA pipe (slower: IMAD.HI is half rate and co-issues
-//              badly with LOP3);
-//   bit 4      s-tap through a shared-memory ring instead of SEL + SHFL (the
-//              default: one ALU op less per word);
-//   bit 5      u32/f32/raw outputs staged in shared memory and written by the
-//              bulk-copy engine (cp.async.bulk, 1 KB per two bodies) instead
-//              of one STG per step;
-//   bit 7      left shifts forced onto the ALU pipe as SHF.L (slower: ptxas's
-//              IMAD.SHL keeps the ALU pipe free).
-//
 // Each warp step emits one contiguous, 128-byte aligned line of the
 // block-major output (out[g*per_stream + k], parallel.cpp:97-135), stored with
-// one coalesced evict-first STG.32 per step -- the cheapest store in issue
-// slots for this layout (a smem transpose to STG.128 would add STS+LDS per word).
+// one coalesced evict-first STG.32 per step.  (Round-1 placement experiments --
+// IMAD.HI right shifts, SHF.L left shifts, bulk-copy stores -- were measured
+// slower and removed; profiles/README.md keeps the A/B table.)
 #pragma once
 
 #include <cstdint>
@@ -70,11 +57,6 @@ struct RtParams {
     uint32_t omega;
 };
 
-// Runtime multipliers for the IMAD.HI form of the right shifts.
-struct HiMul {
-    uint32_t gamma, b, d;  // 2^(32-gamma), 2^(32-b), 2^(32-d)
-};
-
 // kRaw: the linear recurrence alone (RawXorgens::next = step_linear,
 // proj/include/xg/baselines.hpp:60-71, registry id "xorgens-raw"): emits x_i
 // and leaves the Weyl accumulator untouched.
@@ -85,57 +67,32 @@ struct HiMul {
 // reference's BitSource reads them), ranks binned {32, 31, <= 30}.
 enum Mode : int { kU32 = 0, kF32 = 1, kF64 = 2, kMC = 3, kSkip = 4, kRaw = 5, kWide = 6, kRank = 7 };
 
-template <bool HI>
-__device__ __forceinline__ uint32_t shr(uint32_t x, unsigned k, uint32_t mul) {
-    if constexpr (HI) return __umulhi(x, mul);
-    else return x >> k;
-}
-
-// Left shift; FUNNEL forces SHF.L on the ALU pipe (ptxas otherwise picks
-// IMAD.SHL on the FMA pipe for immediate shifts).
-template <bool FUNNEL>
-__device__ __forceinline__ uint32_t shl(uint32_t x, unsigned k) {
-    if constexpr (FUNNEL) {
-        uint32_t r;
-        asm("shf.l.clamp.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(0u), "r"(x), "r"(k));
-        return r;
-    } else {
-        return x << k;
-    }
-}
-
-// 32-bit funnel: low word of (hi:lo) >> s, s in 0..63 (one SHF.R.U64).
-__device__ __forceinline__ uint32_t funnel_r(uint32_t lo, uint32_t hi, uint32_t s) {
-    return static_cast<uint32_t>(((static_cast<uint64_t>(hi) << 32) | lo) >> s);
-}
-
 // Per-warp loop invariants.
 struct Lane {
-    unsigned src;      // shuffle source lane for the s-tap
+    unsigned src;      // shuffle source lane for the s-tap (seeding kernel)
     bool gives_J;      // this lane provides register J (else J+1) to the s-tap shuffle
-    uint32_t sh_own;   // 32 on odd lanes, 0 on even: funnel shift for the pair consumers
-    // VAR bit 4 (shared-memory s-tap): the block produced at step T (mod 8)
+    // Shared-memory s-tap (fill kernel): the block produced at step T (mod 8)
     // lives in slot T of an 8-slot, 256-word ring, with slot 0 mirrored at
     // words 256..287 so a read never wraps.  At step T the window's block j
     // was produced at step T-4+j, so W[32J + delta + l] is ring word
     // A_T + delta + l with the compile-time A_T = 32(T-4+J) mod 256.
     uint32_t* ring_w;  // ring + lane (stores)
     uint32_t* ring_r;  // ring + delta + lane (s-tap loads)
-    uint32_t* stage;   // f64 with VAR bit 4: 2 x 128-word pair staging; VAR bit 5: 2 x 256-word bulk stage
+    uint32_t* stage;   // f64 / MC: 2 x 128-word pair staging
 };
 
 // One warp step on the register window.  T is the step index mod 8; the
 // register rotation uses T mod 4: logical block j of the window lives in
 // R[(T + j) & 3].  xorshift_transform (proj/include/xg/xorgens.hpp:13-18)
-// twice, then xor.
-template <int T, int VAR, class P>
-__device__ __forceinline__ uint32_t warp_step(uint32_t (&R)[4], const P& p, const HiMul& m,
-                                              const Lane& ln) {
+// twice, then xor.  RING: s-tap from the shared-memory ring (fills), else by
+// select + shuffle (seeding, where no ring is set up).
+template <int T, bool RING, class P>
+__device__ __forceinline__ uint32_t warp_step(uint32_t (&R)[4], const P& p, const Lane& ln) {
     constexpr int i0 = T & 3;
     constexpr int iJ = (T + P::J) & 3;
     constexpr int iJ1 = (T + P::J + 1) & 3;
     uint32_t y;
-    if constexpr ((VAR & 16) != 0) {
+    if constexpr (RING) {
         constexpr int kA = (32 * (T - 4 + P::J)) & 255;
         y = ln.ring_r[kA];
     } else {
@@ -143,11 +100,11 @@ __device__ __forceinline__ uint32_t warp_step(uint32_t (&R)[4], const P& p, cons
         y = __shfl_sync(kFull, give, ln.src);
     }
     const uint32_t x = R[i0];
-    const uint32_t t1 = x ^ shl<(VAR & 128) != 0>(x, p.a);
-    const uint32_t t2 = y ^ shl<(VAR & 128) != 0>(y, p.c);
-    const uint32_t v = t1 ^ shr<(VAR & 2) != 0>(t1, p.b, m.b) ^ t2 ^ shr<(VAR & 4) != 0>(t2, p.d, m.d);
+    const uint32_t t1 = x ^ (x << p.a);
+    const uint32_t t2 = y ^ (y << p.c);
+    const uint32_t v = t1 ^ (t1 >> p.b) ^ t2 ^ (t2 >> p.d);
     R[i0] = v;  // newest block; the old block 0 is no longer needed
-    if constexpr ((VAR & 16) != 0) {
+    if constexpr (RING) {
         ln.ring_w[32 * (T & 7)] = v;
         if constexpr ((T & 7) == 0) ln.ring_w[256] = v;  // mirror of slot 0
         // Hazards: a slot is rewritten 8 steps after it was written and read
@@ -161,29 +118,10 @@ __device__ __forceinline__ uint32_t warp_step(uint32_t (&R)[4], const P& p, cons
     return v;
 }
 
-// VAR bit 5: bulk-copy (TMA engine) stores.  A body's 128 output values are
-// staged in shared memory with four STS; after every second body the lanes
-// fence the generic->async proxy and lane 0 issues one 1 KB cp.async.bulk to
-// HBM.  Two 1 KB stage buffers per warp alternate; a buffer is rewritten
-// only after the copy that read it has retired (wait_group.read 1).
-__device__ __forceinline__ void bulk_fence() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
-    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(ssrc));
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
-                 "cp.async.bulk.commit_group;"
-                 :: "l"(gdst), "r"(s), "r"(bytes) : "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory");
-}
-
 // Output stage (xorgens.hpp:58-62): ((w ^ (w >> gamma)) + x) mod 2^32.
-template <int VAR, class P>
-__device__ __forceinline__ uint32_t weyl_out(uint32_t w, uint32_t v, const P& p, const HiMul& m) {
-    return (w ^ shr<(VAR & 1) != 0>(w, p.gamma, m.gamma)) + v;
+template <class P>
+__device__ __forceinline__ uint32_t weyl_out(uint32_t w, uint32_t v, const P& p) {
+    return (w ^ (w >> p.gamma)) + v;
 }
 
 // Uniform float: (u >> 8) * 2^-24, exact.  The
@@ -191,7 +129,7 @@ __device__ __forceinline__ uint32_t weyl_out(uint32_t w, uint32_t v, const P& p,
 // form compiles to I2F.U32.RM (XU pipe) instead of I2FP (ALU pipe), which is
 // the busiest pipe of this kernel.  (Reading the half-word and the byte
 // straight out of the register with I2F.U16 R.H1 + I2F.U8 R.B1 and one FFMA
-// saves the shift but is 1 % slower: profiles/README.md, r1za.)
+// saves the shift but is 1 % slower: profiles/README.md.)
 __device__ __forceinline__ float u32_to_f32(uint32_t u) {
     return __uint2float_rd(u >> 8) * 0x1p-24f;
 }
@@ -202,32 +140,6 @@ __device__ __forceinline__ float u32_to_f32(uint32_t u) {
 __device__ __forceinline__ double raw_pair_to_f64(uint32_t lo, uint32_t hi) {
     const uint64_t u = (static_cast<uint64_t>(hi) << 32) | (lo & ~0x7ffu);
     return __ull2double_rz(u) * 0x1p-64;
-}
-
-// Uniform double from hi and (lo >> 11): (u64 >> 11) * 2^-53 with
-// u64 = lo | hi << 32, = hi * 2^-32 + (lo >> 11) * 2^-53; every step exact.
-__device__ __forceinline__ double pair_to_f64(uint32_t lo_shr11, uint32_t hi) {
-    return __fma_rn(__uint2double_rn(hi), 0x1p-32, __uint2double_rn(lo_shr11) * 0x1p-53);
-}
-
-// Word pairs (2m, 2m+1) of two consecutive steps A (words 32k..32k+31, in
-// `a`) and B (32k+32..32k+63, in `b`): even lanes take pair l/2 of A, odd
-// lanes pair 16 + l/2 of B, exchanging one word with the xor-1 partner.
-// Even lane: (lo, hi) = (a_l, a_{l+1}); odd lane: (b_{l-1}, b_l).  The
-// selects are exact funnel shifts by 0 or 32 (one SHF.R.U64 each).
-__device__ __forceinline__ void pair_words(uint32_t a, uint32_t b, const Lane& ln, uint32_t& lo,
-                                           uint32_t& hi) {
-    const uint32_t give = funnel_r(b, a, ln.sh_own);   // odd: a, even: b
-    const uint32_t got = __shfl_xor_sync(kFull, give, 1);
-    hi = funnel_r(got, b, ln.sh_own);                  // odd: b, even: got
-    lo = funnel_r(a, got, ln.sh_own);                  // odd: got, even: a
-}
-
-__device__ __forceinline__ void pair_f64(uint32_t a, uint32_t b, const Lane& ln, uint32_t& lo11,
-                                         uint32_t& hi) {
-    uint32_t lo;
-    pair_words(a, b, ln, lo, hi);
-    lo11 = lo >> 11;
 }
 
 // Monte Carlo predicate.  A sample is a pair of CONSECUTIVE words
@@ -259,8 +171,6 @@ __device__ __forceinline__ Lane make_lane(unsigned delta) {
     const unsigned lane = threadIdx.x & 31u;
     ln.src = (lane + delta) & 31u;
     ln.gives_J = lane >= delta;
-    const bool odd = lane & 1u;
-    ln.sh_own = odd ? 32u : 0u;
     ln.ring_w = nullptr;
     ln.ring_r = nullptr;
     ln.stage = nullptr;
@@ -274,7 +184,7 @@ __device__ __forceinline__ Lane make_lane(unsigned delta) {
 // advances the Weyl accumulator in closed form.
 template <class P>
 __global__ void __launch_bounds__(kThreads)
-seed_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl,
+seed_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl,
             uint32_t nstreams, uint64_t seed0) {
     const unsigned lane = threadIdx.x & 31;
     const uint32_t g = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -289,10 +199,10 @@ seed_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
     const Lane ln = make_lane(p.delta);
 #pragma unroll 1
     for (int it = 0; it < 4; ++it) {  // 16 steps = 4r words
-        warp_step<0, 0>(R, p, m, ln);
-        warp_step<1, 0>(R, p, m, ln);
-        warp_step<2, 0>(R, p, m, ln);
-        warp_step<3, 0>(R, p, m, ln);
+        warp_step<0, false>(R, p, ln);
+        warp_step<1, false>(R, p, ln);
+        warp_step<2, false>(R, p, ln);
+        warp_step<3, false>(R, p, ln);
     }
     uint32_t* w = win + static_cast<size_t>(g) * kR;
 #pragma unroll
@@ -310,46 +220,24 @@ __device__ __forceinline__ void* advance(void* o, int n) {
 
 // Four warp steps (one full register rotation) = 128 words of the stream.
 // PH is the body's parity: its steps are T = 4*PH .. 4*PH+3 (mod 8) of the
-// shared-memory ring, and it selects the f64 stage buffer.  Emits at cursor o
-// (single-word modes: o[0], o[32], o[64], o[96]; pair modes: o[0], o[32]);
-// the tail variant masks by `limit` (values of this body still wanted).
-template <int MODE, int VAR, bool TAIL, int PH, int BB = 0, class P>
-__device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul& m, const Lane& ln,
-                                      uint32_t& wl, uint32_t w_step, void* o, uint32_t& hits,
-                                      unsigned limit) {
+// shared-memory ring, and it selects the f64 / MC stage buffer.  Emits at
+// cursor o (single-word modes: o[0], o[32], o[64], o[96]; pair modes: o[0],
+// o[32]); the tail variant masks by `limit` (values of this body still wanted).
+template <int MODE, bool TAIL, int PH, class P>
+__device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const Lane& ln, uint32_t& wl,
+                                      uint32_t w_step, void* o, uint32_t& hits, unsigned limit) {
     constexpr bool kW = MODE != kRaw;  // Weyl output stage applied
-    constexpr int BUF = PH;
-    const uint32_t v0 = warp_step<4 * PH + 0, VAR>(R, p, m, ln);
-    const uint32_t o0 = kW ? weyl_out<VAR>(wl, v0, p, m) : v0;
-    const uint32_t v1 = warp_step<4 * PH + 1, VAR>(R, p, m, ln);
-    const uint32_t o1 = kW ? weyl_out<VAR>(wl + w_step, v1, p, m) : v1;
-    const uint32_t v2 = warp_step<4 * PH + 2, VAR>(R, p, m, ln);
-    const uint32_t o2 = kW ? weyl_out<VAR>(wl + 2u * w_step, v2, p, m) : v2;
-    const uint32_t v3 = warp_step<4 * PH + 3, VAR>(R, p, m, ln);
-    const uint32_t o3 = kW ? weyl_out<VAR>(wl + 3u * w_step, v3, p, m) : v3;
+    const uint32_t v0 = warp_step<4 * PH + 0, true>(R, p, ln);
+    const uint32_t o0 = kW ? weyl_out(wl, v0, p) : v0;
+    const uint32_t v1 = warp_step<4 * PH + 1, true>(R, p, ln);
+    const uint32_t o1 = kW ? weyl_out(wl + w_step, v1, p) : v1;
+    const uint32_t v2 = warp_step<4 * PH + 2, true>(R, p, ln);
+    const uint32_t o2 = kW ? weyl_out(wl + 2u * w_step, v2, p) : v2;
+    const uint32_t v3 = warp_step<4 * PH + 3, true>(R, p, ln);
+    const uint32_t o3 = kW ? weyl_out(wl + 3u * w_step, v3, p) : v3;
     wl += 4u * w_step;
     const unsigned lane = threadIdx.x & 31u;
-    if constexpr ((MODE == kU32 || MODE == kF32 || MODE == kRaw) && (VAR & 32) != 0 && !TAIL) {
-        // Bodies go in pairs (PH 0, 1) into stage buffer BB (256 words); the
-        // PH 1 body issues one 1 KB copy for both.  o is this lane's slot, so
-        // lane 0's o is the body's first value.
-        uint32_t* st = ln.stage + 256 * BB + 128 * PH;
-        if constexpr (PH == 0) {
-            if (lane == 0) bulk_wait_read<1>();  // the copy out of buffer BB (two pairs ago) has read it
-            __syncwarp();
-        }
-        const uint32_t ov[4] = {o0, o1, o2, o3};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if constexpr (MODE == kF32) reinterpret_cast<float*>(st)[32 * j + lane] = u32_to_f32(ov[j]);
-            else st[32 * j + lane] = ov[j];
-        }
-        if constexpr (PH == 1) {
-            bulk_fence();
-            __syncwarp();
-            if (lane == 0) bulk_store(static_cast<uint32_t*>(o) - 128, ln.stage + 256 * BB, 1024);
-        }
-    } else if constexpr (MODE == kU32 || MODE == kF32 || MODE == kRaw) {
+    if constexpr (MODE == kU32 || MODE == kF32 || MODE == kRaw) {
         uint32_t* u = static_cast<uint32_t*>(o);
         const uint32_t ov[4] = {o0, o1, o2, o3};
 #pragma unroll
@@ -365,13 +253,13 @@ __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul&
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             if (!TAIL || lane + 32u * j < limit) __stcs(u + 32 * j, static_cast<unsigned long long>(ov[j]));
-    } else if constexpr (MODE == kF64 && (VAR & 16) != 0) {
-        // Pairs through shared memory: the 64 outputs of two steps are staged
-        // in order, then lane l reads words (2l, 2l+1) with one LDS.64 --
-        // value 32*pair + l in natural order, no shuffles or selects.
-        // Two stage buffers alternate between consecutive bodies (BUF), so the
+    } else if constexpr (MODE == kF64 || MODE == kMC) {
+        // Pairs through shared memory: the 128 outputs of the body are staged
+        // in order, then lane l reads words (2l, 2l+1) and (64+2l, 65+2l) with
+        // one LDS.64 each -- value 32*pair + l in natural order, no shuffles.
+        // Two stage buffers alternate between consecutive bodies (PH), so the
         // publishing __syncwarp of body k+1 also retires body k's reads.
-        uint32_t* st = ln.stage + 128 * BUF;
+        uint32_t* st = ln.stage + 128 * PH;
         st[lane] = o0;
         st[32 + lane] = o1;
         st[64 + lane] = o2;
@@ -379,36 +267,14 @@ __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul&
         __syncwarp();
         const uint2 pa = reinterpret_cast<const uint2*>(st)[lane];
         const uint2 pb = reinterpret_cast<const uint2*>(st + 64)[lane];
-        if (!TAIL || lane < limit) __stcs(static_cast<double*>(o), raw_pair_to_f64(pa.x, pa.y));
-        if (!TAIL || lane + 32u < limit) __stcs(static_cast<double*>(o) + 32, raw_pair_to_f64(pb.x, pb.y));
-    } else if constexpr (MODE == kF64) {
-        const unsigned mpair = (lane >> 1) + ((lane & 1u) << 4);
-        uint32_t lo11, hi;
-        pair_f64(o0, o1, ln, lo11, hi);
-        if (!TAIL || mpair < limit) __stcs(static_cast<double*>(o), pair_to_f64(lo11, hi));
-        pair_f64(o2, o3, ln, lo11, hi);
-        if (!TAIL || mpair + 32u < limit) __stcs(static_cast<double*>(o) + 32, pair_to_f64(lo11, hi));
-    } else if constexpr (MODE == kMC && (VAR & 16) != 0) {
-        // Samples are consecutive word pairs (2m, 2m+1): staged like f64.
-        uint32_t* st = ln.stage + 128 * BUF;
-        st[lane] = o0;
-        st[32 + lane] = o1;
-        st[64 + lane] = o2;
-        st[96 + lane] = o3;
-        __syncwarp();
-        const uint2 pa = reinterpret_cast<const uint2*>(st)[lane];
-        const uint2 pb = reinterpret_cast<const uint2*>(st + 64)[lane];
-        // limit (TAIL) = wanted 64-word blocks of this body (0 or 1): pairs 0..31
-        if (!TAIL || limit > 0u) hits += mc_hit(pa.x, pa.y);
-        if (!TAIL) hits += mc_hit(pb.x, pb.y);
-    } else if constexpr (MODE == kMC) {
-        // Consecutive pairs by shuffle (as pair_f64): a lane pairs words of
-        // steps 0-1 (words 0..63 of the body) and of steps 2-3 (64..127).
-        uint32_t lo, hi;
-        pair_words(o0, o1, ln, lo, hi);
-        if (!TAIL || limit > 0u) hits += mc_hit(lo, hi);
-        pair_words(o2, o3, ln, lo, hi);
-        if (!TAIL) hits += mc_hit(lo, hi);
+        if constexpr (MODE == kF64) {
+            if (!TAIL || lane < limit) __stcs(static_cast<double*>(o), raw_pair_to_f64(pa.x, pa.y));
+            if (!TAIL || lane + 32u < limit) __stcs(static_cast<double*>(o) + 32, raw_pair_to_f64(pb.x, pb.y));
+        } else {
+            // limit (TAIL) = wanted 64-word blocks of this body (0 or 1): pairs 0..31
+            if (!TAIL || limit > 0u) hits += mc_hit(pa.x, pa.y);
+            if (!TAIL) hits += mc_hit(pb.x, pb.y);
+        }
     }
 }
 
@@ -420,10 +286,10 @@ __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const HiMul&
 //   kF64:      `words` must be even; words/2 doubles per stream.
 //   kMC:       `words` a multiple of 64; words/2 samples per stream; the hit
 //              total is added to *hits_out.
-template <class P, int MODE, int VAR>
+template <class P, int MODE>
 __global__ void __launch_bounds__(kThreads)
-fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl,
-            uint32_t g_begin, uint32_t g_count, uint64_t words, void* __restrict__ out,
+fill_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32_t g_begin,
+            uint32_t g_count, uint64_t words, void* __restrict__ out,
             unsigned long long* __restrict__ hits_out) {
     const unsigned lane = threadIdx.x & 31;
     const uint32_t gl = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -439,32 +305,23 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
     uint32_t wl = weyl0 + (lane + 1u) * p.omega;
     const uint32_t w_step = 32u * p.omega;
     Lane ln = make_lane(p.delta);
-    if constexpr ((VAR & 16) != 0) {
-        __shared__ uint32_t ring[kWarpsPerBlock][256 + 32];
-        ln.ring_w = ring[threadIdx.x >> 5] + lane;
-        ln.ring_r = ring[threadIdx.x >> 5] + p.delta + lane;
-        // the window's blocks 0..3 count as produced at steps -4..-1: slots 4..7
+    __shared__ uint32_t ring[kWarpsPerBlock][256 + 32];
+    ln.ring_w = ring[threadIdx.x >> 5] + lane;
+    ln.ring_r = ring[threadIdx.x >> 5] + p.delta + lane;
+    // the window's blocks 0..3 count as produced at steps -4..-1: slots 4..7
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ln.ring_w[32 * (4 + j)] = R[j];
-        __syncwarp();
-        if constexpr (MODE == kF64 || MODE == kMC) {
-            __shared__ __align__(16) uint32_t stage[kWarpsPerBlock][256];
-            ln.stage = stage[threadIdx.x >> 5];
-        }
-    }
-    constexpr bool kBulk = (VAR & 32) != 0 && (MODE == kU32 || MODE == kF32 || MODE == kRaw);
-    if constexpr (kBulk) {
-        __shared__ __align__(128) uint32_t bstage[kWarpsPerBlock][512];
-        ln.stage = bstage[threadIdx.x >> 5];
+    for (int j = 0; j < 4; ++j) ln.ring_w[32 * (4 + j)] = R[j];
+    __syncwarp();
+    if constexpr (kPairs) {
+        __shared__ __align__(16) uint32_t stage[kWarpsPerBlock][256];
+        ln.stage = stage[threadIdx.x >> 5];
     }
 
     // Output cursor: single-word modes index words, pair modes index pairs.
     const uint64_t per_stream_vals = kPairs ? (words >> 1) : words;
     void* o = out;
     if constexpr (MODE == kU32 || MODE == kF32 || MODE == kF64 || MODE == kRaw || MODE == kWide) {
-        constexpr bool kShuffledPairs = kPairs && (VAR & 16) == 0;
-        const uint64_t first = static_cast<uint64_t>(gl) * per_stream_vals +
-                               (kShuffledPairs ? ((lane >> 1) + ((lane & 1u) << 4)) : lane);
+        const uint64_t first = static_cast<uint64_t>(gl) * per_stream_vals + lane;
         if constexpr (MODE == kF64) o = static_cast<double*>(out) + first;
         else if constexpr (MODE == kWide) o = static_cast<unsigned long long*>(out) + first;
         else o = static_cast<uint32_t*>(out) + first;
@@ -478,35 +335,15 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
         iters -= n;
         uint32_t i = 0;
 #pragma unroll 1
-        for (; i + 4 <= n; i += 4) {
-            body4<MODE, VAR, false, 0>(R, p, m, ln, wl, w_step, o, hits, 0);
-            body4<MODE, VAR, false, 1>(R, p, m, ln, wl, w_step, advance<MODE>(o, kValsPerBody), hits, 0);
-            body4<MODE, VAR, false, 0, 1>(R, p, m, ln, wl, w_step, advance<MODE>(o, 2 * kValsPerBody), hits, 0);
-            body4<MODE, VAR, false, 1, 1>(R, p, m, ln, wl, w_step, advance<MODE>(o, 3 * kValsPerBody), hits, 0);
-            o = advance<MODE>(o, 4 * kValsPerBody);
+        for (; i + 2 <= n; i += 2) {
+            body4<MODE, false, 0>(R, p, ln, wl, w_step, o, hits, 0);
+            body4<MODE, false, 1>(R, p, ln, wl, w_step, advance<MODE>(o, kValsPerBody), hits, 0);
+            o = advance<MODE>(o, 2 * kValsPerBody);
         }
-        // 0-3 remaining bodies keep the parity sequence 0, 1, 0 (a chunk of
-        // 2^30 bodies is a multiple of 4, so every chunk starts at parity 0).
-        const uint32_t rem = n - i;
-        if (rem >= 1) {
-            body4<MODE, VAR, false, 0>(R, p, m, ln, wl, w_step, o, hits, 0);
+        // a chunk of 2^30 bodies is even, so every chunk starts at parity 0
+        if (i < n) {
+            body4<MODE, false, 0>(R, p, ln, wl, w_step, o, hits, 0);
             o = advance<MODE>(o, kValsPerBody);
-        }
-        if (rem >= 2) {
-            body4<MODE, VAR, false, 1>(R, p, m, ln, wl, w_step, o, hits, 0);
-            o = advance<MODE>(o, kValsPerBody);
-        }
-        if (rem >= 3) {
-            body4<MODE, VAR, false, 0, 1>(R, p, m, ln, wl, w_step, o, hits, 0);
-            o = advance<MODE>(o, kValsPerBody);
-        }
-        if constexpr (kBulk) {
-            if (rem & 1u) {  // a lone PH 0 body: copy its half-buffer out now
-                bulk_fence();
-                __syncwarp();
-                if (lane == 0)
-                    bulk_store(static_cast<uint32_t*>(o) - 128, ln.stage + (rem == 3 ? 256 : 0), 512);
-            }
         }
     }
 
@@ -517,9 +354,9 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
         const uint32_t O[4] = {R[0], R[1], R[2], R[3]};
         const unsigned lim = MODE == kMC ? tail >> 6 : (kPairs ? tail >> 1 : tail);
         if ((words >> 7) & 1)
-            body4<MODE, VAR, true, 1>(R, p, m, ln, wl, w_step, o, hits, lim);
+            body4<MODE, true, 1>(R, p, ln, wl, w_step, o, hits, lim);
         else
-            body4<MODE, VAR, true, 0>(R, p, m, ln, wl, w_step, o, hits, lim);
+            body4<MODE, true, 0>(R, p, ln, wl, w_step, o, hits, lim);
         // New logical window = words [words-128, words): positions tail..tail+127
         // of the 256 words held in O (old window) followed by R (new block).
 #pragma unroll
@@ -532,9 +369,6 @@ fill_kernel(P p, HiMul m, uint32_t* __restrict__ win, uint32_t* __restrict__ wey
         for (int j = 0; j < 4; ++j) w[32 * j + lane] = R[j];
     }
     if (MODE != kRaw && lane == 0) weyl[g] = weyl0 + static_cast<uint32_t>(words) * p.omega;
-    if constexpr (kBulk) {
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    }
 
     if constexpr (MODE == kMC) {
         unsigned long long t = hits;

@@ -183,6 +183,9 @@ int cmd_gen(const Args& a) {
     if (a.blocks > 1 || a.lanes > 1) {
         if (!g.weyl) return fail("--blocks/--lanes apply only to xorgens generators", exit_bad_args);
         if (a.count % blocks != 0) return fail("--count must be divisible by --blocks", exit_bad_args);
+        // BlockEnsemble(params, seed, blocks, lanes) throws out_of_range for
+        // lanes == 0 (proj/src/parallel.cpp:90-91) -> exit 65 (xgen.cpp:99-101)
+        if (a.lanes == 0) return fail("lane count must be at least 1", exit_lane_range);
     }
     if (lanes > xg_lane_bound(&p)) return fail("lane count exceeds min(s, r - s)", exit_lane_range);
 

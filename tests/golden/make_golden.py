@@ -8,6 +8,8 @@ conventions of DESIGN.md section 3 (numpy, exact) to reference words, since
 the reference has no conversions of its own.
 
 Run in the container that has /root/reference:  python tests/golden/make_golden.py
+(``--full-size`` regenerates only tests/golden/full_size.json, the per-chunk
+digests of the full-size configs 2-5: about a minute on 8 cores).
 """
 from __future__ import annotations
 
@@ -36,8 +38,73 @@ def stream_checksums(ref: Reference, p, seed: int, n: int):
     return x, s, int(w[-1])
 
 
+def full_size(ref: Reference, gp32) -> dict:
+    """Digests of the full-size workloads, base_seed 1, from the reference's
+    own words (xgref_stream_digests), per chunk of 2^14 consecutive streams:
+      u32: streams [0, 2^18) x 2^16 words -- config 4 (2^34 words) and, chunk by
+           chunk, config 2 (chunk 0 = the 2^30-word fill; chunk r = rank r of
+           the weak-scaled config 2 at N <= 16);
+      f32 / f64: streams [0, 2^17) x 2^16 values (f64: 2^17 words) -- config 3
+           per chunk (rank r of the weak-scaled fills at N <= 8);
+      mc: streams [0, 2^17) x 2^15 samples -- exact hit counts for 2^32 samples
+           (config 5's stream set), per chunk so any N in {1, 2, 4, 8} checks its
+           slice.
+    A chunk record is paper_1108_0486_b200.digest.chunk_record of the
+    per-stream (xor, sum, wsum): xor / sum / wsum of the chunk's block-major
+    concatenation and the sha256 of the per-stream records."""
+    from paper_1108_0486_b200.digest import chunk_record
+
+    C, per = 1 << 14, 1 << 16
+    n_u32_chunks, n_conv_chunks = 16, 8
+    piece = 256
+
+    def work(first):
+        conv = first < n_conv_chunks * C
+        return first, ref.stream_digests(gp32, 1, first, piece, per, per if conv else 0,
+                                         (per // 2) if conv else 0)
+
+    res = {}
+    with ThreadPoolExecutor(max_workers=os.cpu_count()) as ex:
+        for first, d in ex.map(work, range(0, n_u32_chunks * C, piece)):
+            res[first] = d
+    out = {"base_seed": 1, "chunk_streams": C, "params": "xorgensgp32",
+           "source": "oracle/_ref/libxgref.so xgref_stream_digests (reference next_word)"}
+
+    def cat(key, i, chunk):
+        parts = [res[f][key] for f in range(chunk * C, (chunk + 1) * C, piece)]
+        if key == "mc":
+            return np.concatenate(parts)
+        return tuple(np.concatenate([p[i] for p in parts]) for i in range(3))
+
+    out["u32"] = {"per_stream": per, "chunks": [chunk_record(*cat("u32", 0, c), per)
+                                                for c in range(n_u32_chunks)]}
+    out["f32"] = {"per_stream": per, "chunks": [chunk_record(*cat("f32", 0, c), per)
+                                                for c in range(n_conv_chunks)]}
+    out["f64"] = {"per_stream": per, "u32_per_stream": 2 * per,
+                  "chunks": [chunk_record(*cat("f64", 0, c), 2 * per) for c in range(n_conv_chunks)]}
+    out["mc"] = {"samples_per_stream": per // 2,
+                 "chunk_hits": [int(cat("mc", 0, c).sum()) for c in range(n_conv_chunks)]}
+    # whole 2^34-word fill (config 4), block-major over all 2^18 streams
+    from paper_1108_0486_b200.digest import slice_digest
+    xs = np.concatenate([res[f]["u32"][0] for f in sorted(res)])
+    ss = np.concatenate([res[f]["u32"][1] for f in sorted(res)])
+    wss = np.concatenate([res[f]["u32"][2] for f in sorted(res)])
+    gx, gs, gws = slice_digest(xs, ss, wss, per)
+    out["u32"]["all"] = {"streams": len(xs), "xor": f"{gx:08x}", "sum": f"{gs:016x}",
+                         "wsum": f"{gws:016x}"}
+    out["mc"]["total_hits_2p32"] = int(sum(out["mc"]["chunk_hits"]))
+    return out
+
+
 def main() -> None:
     ref = Reference()
+    if "--full-size" in sys.argv:
+        fs = full_size(ref, Oracle().gp32())
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "full_size.json")
+        with open(path, "w") as f:
+            json.dump(fs, f, indent=1)
+        print("wrote", path, fs["u32"]["chunks"][0], fs["mc"]["total_hits_2p32"])
+        return
     o = Oracle()
     gp32 = o.gp32()
     out = {"generator": "xorgensgp32 (128,65,15,14,12,17) w=32",

@@ -38,6 +38,8 @@ def test_binary_built():
     (("gen", "-g", "nosuchgen", "--count", "4"), 64),          # test_cli.cpp:95
     (("params", "nosuchgen"), 64),                              # :96
     (("gen", "-g", "xorgensgp32", "--count", "64", "--lanes", "64"), 65),  # :97
+    # lanes 0 with blocks > 1: BlockEnsemble throws out_of_range (parallel.cpp:90-91)
+    (("gen", "-g", "xorgensgp32", "--count", "64", "--blocks", "2", "--lanes", "0"), 65),
     (("gen", "-g", "xorgensgp32", "--count", "7", "--blocks", "2"), 67),   # :98
     (("gen", "-g", "xorgens-raw", "--count", "4", "--blocks", "2"), 67),   # :99 (non-Weyl id)
     (("gen", "-g", "xorgensgp32", "--count", "4", "--format", "bogus"), 67),  # :100

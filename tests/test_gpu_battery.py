@@ -80,3 +80,36 @@ def test_ones_runs_and_birthday_kernels_direct():
         out = torch.zeros(1, dtype=torch.int64, device="cuda")
         assert xg._lib.lib.xg_birthday_duplicates(d.data_ptr(), nd, rounds, t, out.data_ptr(), None) == 0
         assert int(out.item()) == dup, (nd, t)
+
+
+def test_battery_rejects_rank_unsupported_sets_up_front():
+    """A w = 32 set the fused rank test cannot take (r - s >= 64, J = 2) is
+    refused before any test consumes the stream; without the rank test the
+    rest of the battery runs."""
+    from paper_1108_0486_b200.battery import BatteryConfig, run_battery_gpu
+
+    j2 = xg.GeneratorParams(128, 33, 11, 7, 9, 19, 32, 0x6A09E667 | 1, 11)
+    with pytest.raises(xg.UnsupportedParamsError):
+        run_battery_gpu(j2, 1, BatteryConfig.quick())
+    cfg = BatteryConfig.quick()
+    cfg.run_matrix_rank = False
+    rep = run_battery_gpu(j2, 1, cfg)
+    assert rep["num_tests"] == 4
+
+
+def test_handle_less_calls_reject_host_pointers():
+    """The calls without a handle take their device from the input pointer;
+    a host pointer is XG_EINVAL, not a fault."""
+    host = np.zeros(64, dtype=np.uint32)
+    out = torch.zeros(2, dtype=torch.int64, device="cuda")
+    assert xg._lib.lib.xg_bits_ones_runs(host.ctypes.data, 64, out.data_ptr(), None) == xg._lib.XG_EINVAL
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_battery_on_a_non_current_device(reference):  # pragma: no cover - 1-GPU boxes
+    from paper_1108_0486_b200.battery import BatteryConfig, run_battery_gpu
+
+    torch.cuda.set_device(0)
+    a = run_battery_gpu(xg.xorgensgp32_params(), 3, BatteryConfig.quick(), device=1)
+    b = run_battery_gpu(xg.xorgensgp32_params(), 3, BatteryConfig.quick(), device=0)
+    assert a == b

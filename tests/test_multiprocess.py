@@ -7,6 +7,7 @@ the single-process fill -- the schedule-independence test of
 proj/tests/test_parallel.cpp:132-143 lifted to processes.  The Monte Carlo
 workload's one collective (a uint64 hit-count sum) is exercised the same way.
 """
+import json
 import os
 import socket
 
@@ -122,3 +123,102 @@ def test_bench_multirank_logic(world):
     assert firsts == [r * (1 << 14) for r in range(world)]
     assert all(g["fill_u32"][4] == (1 << 30) * world for g in geos)
     assert all(g["fill_f64"][4] == (1 << 31) * world for g in geos)
+
+
+def _bench_cmd(*args, env=None):
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ)
+    e.pop("WORLD_SIZE", None)
+    e.update(env or {})
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), *args], capture_output=True,
+                       text=True, timeout=900, env=e, cwd="/tmp")
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    return r.returncode, (json.loads(lines[-1]) if lines else None), r.stderr
+
+
+def test_bench_self_launches_n_ranks_dry_run():
+    """`python bench.py --gpus 2` outside torchrun re-launches itself with 2
+    ranks (torch.distributed.run, 127.0.0.1) -- the driver's own command is
+    an N-rank job; the dry run checks world, slices and max-over-ranks on CPU."""
+    rc, line, err = _bench_cmd("--gpus", "2", "--dry-run")
+    assert rc == 0, err[-2000:]
+    assert line["n_gpus"] == 2 and line["comm"]["nranks"] == 2
+    assert line["max_over_ranks"] == 2.0
+    assert [s["fill_2p34"][0] for s in line["slices"]] == [0, 1 << 17]
+
+
+def _gpu_slice_worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+
+    import paper_1108_0486_b200 as xg
+    from paper_1108_0486_b200.digest import row_digests
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    first, count = xg.partition(1000, world, rank)
+    e = xg.BlockEnsemble(xg.xorgensgp32_params(), 1, count, 63, first_stream=first)
+    x, s, ws = row_digests(e.fill_u32(4096))
+    hits = torch.tensor([int(xg.BlockEnsemble(xg.xorgensgp32_params(), 1, count, 63,
+                                              first_stream=first).mc_pi(320).item())])
+    dist.all_reduce(hits)
+    g = [None] * world
+    dist.all_gather_object(g, (first, x, s, ws))
+    if rank == 0:
+        q.put((g, int(hits.item())))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_ranks_generate_slices_on_the_gpu(world):
+    """Ranks (sharing one GPU) generate their partition slices with the GPU
+    path; the digests gathered in rank order equal the single-process fill's,
+    and the all-reduced MC count equals the single ensemble's."""
+    import torch
+
+    import paper_1108_0486_b200 as xg
+    from paper_1108_0486_b200.digest import row_digests
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_slice_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    g, hits = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    e = xg.BlockEnsemble(xg.xorgensgp32_params(), 1, 1000, 63)
+    x, s, ws = row_digests(e.fill_u32(4096))
+    assert [f for f, *_ in g] == [xg.partition(1000, world, r)[0] for r in range(world)]
+    assert np.array_equal(np.concatenate([t[1] for t in g]), x)
+    assert np.array_equal(np.concatenate([t[2] for t in g]), s)
+    assert np.array_equal(np.concatenate([t[3] for t in g]), ws)
+    assert hits == int(xg.BlockEnsemble(xg.xorgensgp32_params(), 1, 1000, 63).mc_pi(320).item())
+    del torch
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workload", ["fill_u32", "fill_2p34", "mc_pi"])
+def test_bench_two_ranks_self_launched_gloo(workload):
+    """The driver's N = 2 command through the self-launch path, two gloo ranks
+    on one GPU: n_gpus 2, and every rank's slice passes the full-size parity
+    check (tests/golden/full_size.json)."""
+    rc, line, err = _bench_cmd("--gpus", "2", "--workload", workload, "--steps", "3", "--warmup", "3",
+                               "--no-cpu", "--no-e2e", "--no-extra", "--sustained-s", "0",
+                               env={"XG_BENCH_BACKEND": "gloo"})
+    assert rc == 0, err[-3000:]
+    assert line["n_gpus"] == 2 and line["comm"]["nranks"] == 2
+    assert line["parity"]["checked"] and line["parity"]["ok"], line["parity"]
+    if workload == "mc_pi":
+        assert line["mc"]["allreduce_in_step"]

@@ -369,3 +369,51 @@ def test_berlekamp_massey_known_sequences():
     assert b.berlekamp_massey(np.array(lfsr, dtype=np.uint8)) == 8
     assert b.berlekamp_massey(np.zeros(64, dtype=np.uint8)) == 0
     assert b.berlekamp_massey(np.array([0] * 63 + [1], dtype=np.uint8)) == 64
+
+
+def _row_digests_np(words: np.ndarray):
+    """Per-row (xor, sum, sum e_k (k+1)) of a 2-D uint32 array (mod 2^64)."""
+    w = words.astype(np.uint64)
+    k = np.arange(1, words.shape[1] + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        return (np.bitwise_xor.reduce(words, axis=1).astype(np.uint32),
+                w.sum(axis=1, dtype=np.uint64), (w * k).sum(axis=1, dtype=np.uint64))
+
+
+@pytest.fixture(scope="module")
+def full_size():
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "full_size.json")) as f:
+        return json.load(f)
+
+
+def test_full_size_golden_consistent_with_config2(golden, full_size):
+    """Chunk 0 of the 2^34-word golden is the 2^30-word config-2 fill."""
+    c0 = full_size["u32"]["chunks"][0]
+    assert c0["xor"] == golden["config2"]["xor"] and c0["wsum"] == golden["config2"]["wsum"]
+    assert len(full_size["u32"]["chunks"]) == 16 and len(full_size["mc"]["chunk_hits"]) == 8
+    hits = full_size["mc"]["total_hits_2p32"]
+    assert hits == sum(full_size["mc"]["chunk_hits"])
+    assert abs(4.0 * hits / 2**32 - np.pi) < 6 * 1.6e-6 * 2**4  # sigma(pi_hat) at 2^32 samples ~ 2.5e-5
+
+
+def test_full_size_golden_pinned_by_restatement(oracle, full_size):
+    """The full-size goldens come from the reference's own words
+    (make_golden.py --full-size); the C restatement reproduces the last u32
+    chunk (streams 15*2^14 ...: 2^30 words, config 4) and the last MC chunk
+    (2^14 streams x 2^15 samples) exactly."""
+    from paper_1108_0486_b200.digest import chunk_record
+
+    C, per = full_size["chunk_streams"], full_size["u32"]["per_stream"]
+    piece = 1024
+    parts = []
+    for g0 in range(15 * C, 16 * C, piece):
+        sub = OracleEnsemble(oracle, oracle.gp32(), 1, piece, first_stream=g0)
+        parts.append(_row_digests_np(sub.fill_u32(per)))
+    rec = chunk_record(*(np.concatenate([p[i] for p in parts]) for i in range(3)), per)
+    assert rec == full_size["u32"]["chunks"][15]
+    spp = full_size["mc"]["samples_per_stream"]
+    sub = OracleEnsemble(oracle, oracle.gp32(), 1, C, first_stream=7 * C)
+    assert int(sub.mc_hits(spp).sum()) == full_size["mc"]["chunk_hits"][7]
