@@ -745,6 +745,28 @@ def sustained(fn, stream, seconds: float, world: int, local: int, words_per_step
             "clocks": clk.summary()}
 
 
+def host_api_bench(cb: dict) -> dict:
+    """The reference's two host-side methods over the C++ drop-in
+    (paper_1108_0486_b200/tools/xg_hostbench.cpp): measure_throughput through
+    xg::gpu::XorgensSource (WordSource::next per word) and
+    measure_ensemble_throughput through xg::gpu::BlockEnsemble::generate
+    (vector<vector<uint64_t>>, 2^14 blocks x 2^16), next to the reference's
+    own numbers on the same host (cpu_baseline)."""
+    exe = os.path.join(ROOT, "paper_1108_0486_b200", "lib", "xg_hostbench")
+    try:
+        r = subprocess.run([exe, str(10**8), "5", str(CHUNK), str(1 << 30)], capture_output=True,
+                           text=True, timeout=600)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": str(e)}
+    d["reference"] = {
+        "measure_throughput_rn_per_s": cb.get("serial_1core_rn_per_s"),
+        "measure_ensemble_throughput_rn_per_s": cb.get("value"),
+        "source": "cpu_baseline (oracle/_ref: XorgensState::next_word serial best-chunk rate; "
+                  "BlockEnsemble::generate on all host threads)"}
+    return d
+
+
 def dry_run(args) -> int:
     """CPU-only check of the N-rank plumbing (gloo): world, ranks, slices."""
     world, rank, _ = dist_setup(dry=True)
@@ -854,6 +876,9 @@ def main():
             result["cpu_baseline"] = cpu_baseline_for(wl)
         except Exception as e:  # noqa: BLE001
             result["cpu_baseline"] = {"value": None, "unavailable": str(e)}
+
+    if rank == 0 and world == 1 and wl == "fill_u32" and not args.no_e2e:
+        result["e2e_host_api"] = host_api_bench(result.get("cpu_baseline", {}))
 
     if wl == "fill_u32" and not args.no_extra:
         extras = {}

@@ -19,8 +19,10 @@
 #pragma once
 
 #include <cstdint>
+#include <algorithm>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -90,6 +92,7 @@ public:
     BlockEnsemble(BlockEnsemble&& o) noexcept { *this = std::move(o); }
     BlockEnsemble& operator=(BlockEnsemble&& o) noexcept {
         std::swap(h_, o.h_);
+        std::swap(nc_, o.nc_);
         n_ = o.n_;
         base_seed_ = o.base_seed_;
         lanes_ = o.lanes_;
@@ -102,44 +105,56 @@ public:
     }
 
     // proj/include/xg/parallel.hpp:46-47: block-major, continues every block.
+    // The rows are allocated by `workers` host threads (hardware_concurrency
+    // when 0, as the reference's workers, parallel.cpp:115-116) and filled in
+    // place by xg_generate_host_rows: words cross PCIe once, as u32, and are
+    // widened straight into each block's vector -- no intermediate copy.
     std::vector<std::vector<std::uint64_t>> generate(std::size_t per_block,
                                                      unsigned workers = 0) {
-        (void)workers;  // the device schedule never changes the output
-        std::vector<std::uint64_t> flat(static_cast<std::size_t>(n_) * per_block);
-        if (per_block) check(xg_generate_host_words(h_, per_block, flat.data(), nullptr));
         std::vector<std::vector<std::uint64_t>> out(n_);
-        for (unsigned i = 0; i < n_; ++i)
-            out[i].assign(flat.begin() + static_cast<std::ptrdiff_t>(i * per_block),
-                          flat.begin() + static_cast<std::ptrdiff_t>((i + 1) * per_block));
+        unsigned t = workers ? workers : std::max(1u, std::thread::hardware_concurrency());
+        t = std::min<unsigned>(t, std::max(1u, n_));
+        auto alloc = [&](unsigned id) {
+            for (unsigned i = id; i < n_; i += t) out[i].resize(per_block);
+        };
+        std::vector<std::thread> pool;
+        for (unsigned id = 1; id < t; ++id) pool.emplace_back(alloc, id);
+        alloc(0);
+        for (auto& th : pool) th.join();
+        if (per_block) {
+            std::vector<std::uint64_t*> rows(n_);
+            for (unsigned i = 0; i < n_; ++i) rows[i] = out[i].data();
+            check(xg_generate_host_rows(h(), per_block, rows.data(), nullptr));
+        }
         return out;
     }
 
     // Device-buffer fills (asynchronous on `stream`).
     void fill_u32(std::uint64_t per_block, std::uint32_t* dev, xg_stream_t s = nullptr) {
-        check(xg_fill_u32(h_, per_block, dev, s));
+        check(xg_fill_u32(h(), per_block, dev, s));
     }
     void fill_u64(std::uint64_t per_block, std::uint64_t* dev, xg_stream_t s = nullptr) {
-        check(xg_fill_u64(h_, per_block, dev, s));
+        check(xg_fill_u64(h(), per_block, dev, s));
     }
     void fill_f32(std::uint64_t per_block, float* dev, xg_stream_t s = nullptr) {
-        check(xg_fill_f32(h_, per_block, dev, s));
+        check(xg_fill_f32(h(), per_block, dev, s));
     }
     void fill_f64(std::uint64_t per_block, double* dev, xg_stream_t s = nullptr) {
-        check(xg_fill_f64(h_, per_block, dev, s));
+        check(xg_fill_f64(h(), per_block, dev, s));
     }
     void mc_pi(std::uint64_t samples, std::uint64_t* dev_hits, xg_stream_t s = nullptr) {
-        check(xg_mc_pi(h_, samples, dev_hits, s));
+        check(xg_mc_pi(h(), samples, dev_hits, s));
     }
     // Fused matrix_rank_test counting (proj/src/stattests/tests.cpp:93-109):
     // adds the (rank 32, 31, <= 30) bins to dev_counts[0..2].
     void rank_test(std::uint64_t matrices, std::uint64_t* dev_counts, xg_stream_t s = nullptr) {
-        check(xg_rank_test(h_, matrices, dev_counts, s));
+        check(xg_rank_test(h(), matrices, dev_counts, s));
     }
     // linear_complexity_test's per-block Berlekamp-Massey (tests.cpp:128-178):
     // adds the histogram of complexities to dev_hist[0..block_length].
     void linear_complexity_test(unsigned block_length, std::uint64_t blocks, std::uint64_t* dev_hist,
                                 xg_stream_t s = nullptr) {
-        check(xg_linear_complexity_test(h_, block_length, blocks, dev_hist, s));
+        check(xg_linear_complexity_test(h(), block_length, blocks, dev_hist, s));
     }
 
     unsigned num_blocks() const noexcept { return n_; }
@@ -150,28 +165,47 @@ public:
     std::pair<std::vector<std::uint64_t>, std::uint64_t> block_state(unsigned i) const {
         std::vector<std::uint64_t> buf(r_);
         std::uint64_t w = 0;
-        check(xg_state_export(h_, i, buf.data(), &w));
+        check(xg_state_export(h(), i, buf.data(), &w));
         return {buf, w};
     }
     void set_block_state(unsigned i, const std::vector<std::uint64_t>& buf, std::uint64_t weyl) {
         if (buf.size() != r_) throw std::invalid_argument("buffer size must equal r");
-        check(xg_state_import(h_, i, buf.data(), weyl));
+        check(xg_state_import(h(), i, buf.data(), weyl));
     }
     // Whole-ensemble checkpoint: r window words per block (oldest first) + weyl.
     void export_state(std::vector<std::uint32_t>& window, std::vector<std::uint32_t>& weyl) const {
         window.resize(static_cast<std::size_t>(n_) * r_);
         weyl.resize(n_);
-        check(xg_state_export_all(h_, window.data(), weyl.data()));
+        check(xg_state_export_all(h(), window.data(), weyl.data()));
     }
     void import_state(const std::vector<std::uint32_t>& window, const std::vector<std::uint32_t>& weyl) {
         if (window.size() != static_cast<std::size_t>(n_) * r_ || weyl.size() != n_)
             throw std::invalid_argument("checkpoint size differs from the ensemble");
-        check(xg_state_import_all(h_, window.data(), weyl.data()));
+        check(xg_state_import_all(h(), window.data(), weyl.data()));
     }
-    xg_ensemble_t handle() const noexcept { return h_; }
+    // The C handle, after handing back any next_word words cached here.
+    xg_ensemble_t handle() const { return h(); }
 
 protected:
     BlockEnsemble() = default;
+    // next_word cache (XorgensState): a view of pinned refill words
+    // (xg_next_view); unread ones are returned before any other call.
+    struct NextCache {
+        const void* p = nullptr;
+        std::uint64_t pos = 0, n = 0;
+        unsigned eb = 4;
+    };
+    mutable NextCache nc_;
+    void give_back() const {
+        if (nc_.n) {
+            check(xg_next_return(h_, nc_.n - nc_.pos));
+            nc_ = NextCache{};
+        }
+    }
+    xg_ensemble_t h() const {
+        give_back();
+        return h_;
+    }
     xg_ensemble_t h_ = nullptr;
     unsigned n_ = 0;
     std::uint64_t base_seed_ = 0;
@@ -201,21 +235,26 @@ public:
         return st;
     }
 
+    // Inline on the hot path: one load from the pinned refill slot.
     std::uint64_t next_word() {
-        std::uint64_t v;
-        check(xg_next_word(h_, &v));
-        return v;
+        if (nc_.pos == nc_.n) refill();
+        return nc_.eb == 4 ? static_cast<const std::uint32_t*>(nc_.p)[nc_.pos++]
+                           : static_cast<const std::uint64_t*>(nc_.p)[nc_.pos++];
     }
     std::uint64_t next_u64() {
-        std::uint64_t v;
-        check(xg_next_u64(h_, &v));
-        return v;
+        if (w_ == 64) return next_word();
+        const std::uint64_t lo = next_word();
+        return lo | (next_word() << 32);
     }
     std::vector<std::uint64_t> logical_buffer() const { return block_state(0).first; }
     std::uint64_t weyl_value() const { return block_state(0).second; }
 
 private:
     XorgensState() = default;
+    void refill() {
+        nc_ = NextCache{};
+        check(xg_next_view(h_, &nc_.p, &nc_.n, &nc_.eb));
+    }
 };
 
 // proj/src/parallel.cpp:8-42

@@ -217,14 +217,32 @@ int xg_skip(xg_ensemble_t h, uint64_t words, xg_stream_t stream);
  * overlapping generation.  host_out should be pinned for full speed. */
 int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,
                      xg_stream_t stream);
+/* BlockEnsemble::generate into the reference's own result layout: rows[g]
+ * points at per_stream uint64 elements for stream g (e.g. the data() of
+ * vector<uint64_t> per block).  Words cross PCIe as u32 (w <= 32) through
+ * pinned staging and are widened into the rows by host threads while the next
+ * tile is generated and copied. */
+int xg_generate_host_rows(xg_ensemble_t h, uint64_t per_stream, uint64_t* const* rows,
+                          xg_stream_t stream);
 /* The same with every word in the reference's uint64 container -- exactly
  * the element type of generate()'s result; any w, including 64. */
 int xg_generate_host_words(xg_ensemble_t h, uint64_t per_stream, uint64_t* host_out,
                            xg_stream_t stream);
 /* XorgensState::next_word (proj/include/xg/xorgens.hpp:58-62) on a
  * one-stream handle: the w-bit word in a uint64, served from device-generated
- * refills; interleaving with fills / exports keeps the exact serial stream. */
+ * refills; interleaving with fills / exports keeps the exact serial stream.
+ * Refills are double-buffered: two pinned slots of 2^16 words, the next one
+ * generated and copied on a private stream while this one is served. */
 int xg_next_word(xg_ensemble_t h, uint64_t* out);
+/* Zero-copy batch form of next_word (what xg::gpu::XorgensState inlines):
+ * *words points at the next *count unserved words of the stream in pinned host
+ * memory, elements of *elem_bytes (4: w <= 32, 8: w = 64), valid until the
+ * next call on the handle.  The words count as served; words the caller did
+ * not use are handed back with xg_next_return(h, unread) before any other
+ * call, so the next word / fill / export continues right after the last word
+ * used. */
+int xg_next_view(xg_ensemble_t h, const void** words, uint64_t* count, unsigned* elem_bytes);
+int xg_next_return(xg_ensemble_t h, uint64_t unread);
 /* next_word as uint32 (w <= 32). */
 int xg_next_u32(xg_ensemble_t h, uint32_t* out);
 /* w = 32: two words, lo = first; w = 64: one word. */

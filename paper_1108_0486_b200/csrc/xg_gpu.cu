@@ -14,6 +14,7 @@
 #include <cstring>
 #include <new>
 #include <numeric>
+#include <thread>
 #include <type_traits>
 #include <vector>
 
@@ -31,7 +32,7 @@ namespace {
 std::atomic<uint64_t> g_launches{0};
 
 constexpr uint32_t kMask32 = 0xffffffffu;
-constexpr size_t kNextBuf = 1u << 14;  // words per next_word refill
+constexpr uint64_t kNextBuf = 1u << 16;  // words per next_word refill slot
 constexpr unsigned kGenMaxR = 16384;   // generic path: r words of state in shared memory
 
 // kGP32 / kRtJ*: register-window kernels (w = 32, r = 128, lane_bound >= 32);
@@ -81,14 +82,26 @@ struct xg_ensemble {
     uint32_t* d_weyl = nullptr;  // [num_streams] Weyl accumulator
     uint64_t* d_win64 = nullptr;   // generic path: [num_streams][r] words, oldest first
     uint64_t* d_weyl64 = nullptr;  // generic path: [num_streams]
-    // next_word service (one-stream handles)
-    std::vector<uint64_t> nbuf;
-    size_t npos = 0;
-    void* d_snap = nullptr;  // state snapshot taken before a refill
-    uint64_t* d_scratch = nullptr;
+    // next_word service (one-stream handles): two refill slots of kNextBuf
+    // words in pinned host memory, one being served while the other is
+    // generated and copied on a private stream (NextRing in xg_gpu.cu).
+    struct NextRing {
+        bool active = false;     // slots hold words not yet given back to the device state
+        int cur = 0;             // slot being served
+        uint64_t pos = 0;        // words of slot `cur` served
+        unsigned eb = 4;         // element bytes: 4 (w <= 32) or 8 (w = 64)
+        void* host[2] = {};      // pinned
+        void* dev[2] = {};       // device staging
+        void* snap[2] = {};      // generator state before slot i's words
+        cudaStream_t st = nullptr;
+        cudaEvent_t ev[2] = {};
+    } nr;
     // xg_generate_host staging
     void* d_stage = nullptr;
     size_t stage_words = 0;  // bytes
+    // xg_generate_host_rows pinned staging
+    void* h_stage = nullptr;
+    size_t h_stage_bytes = 0;
     // xg_linear_complexity_test word buffer
     uint32_t* d_lc = nullptr;
     size_t lc_bytes = 0;
@@ -398,9 +411,16 @@ void free_handle(xg_ensemble* h) {
         cudaFree(h->d_weyl);
         cudaFree(h->d_win64);
         cudaFree(h->d_weyl64);
-        cudaFree(h->d_snap);
-        cudaFree(h->d_scratch);
+        if (h->nr.st) cudaStreamSynchronize(h->nr.st);
+        for (int i = 0; i < 2; ++i) {
+            cudaFreeHost(h->nr.host[i]);
+            cudaFree(h->nr.dev[i]);
+            cudaFree(h->nr.snap[i]);
+            if (h->nr.ev[i]) cudaEventDestroy(h->nr.ev[i]);
+        }
+        if (h->nr.st) cudaStreamDestroy(h->nr.st);
         cudaFree(h->d_stage);
+        cudaFreeHost(h->h_stage);
         cudaFree(h->d_lc);
     }
     delete h;
@@ -426,18 +446,19 @@ int copy_state(xg_ensemble* h, void* snap, bool to_snapshot, cudaStream_t s) {
                                : cudaMemcpyAsync(wy, sn + wb, wyb, k, s));
 }
 
-// Buffered next_word values that were generated but not served are given back:
-// restore the pre-refill snapshot and re-advance by the served count, so the
+// next_word words generated but not served are given back before any other
+// use of the handle: wait for the ring's stream, restore the state saved
+// before the slot being served and re-advance it by the words served, so the
 // device state is exactly "after the last word the caller saw".
 int settle_next(xg_ensemble* h, cudaStream_t s) {
-    if (h->nbuf.empty()) return XG_OK;
-    const size_t served = h->npos, held = h->nbuf.size();
-    h->nbuf.clear();
-    h->npos = 0;
-    if (served == held) return XG_OK;
-    int rc = copy_state(h, h->d_snap, /*to_snapshot=*/false, s);
-    if (rc) return rc;
-    return launch_fill<kSkip>(h, 0, 1, served, nullptr, nullptr, s);
+    auto& r = h->nr;
+    if (!r.active) return XG_OK;
+    r.active = false;
+    int rc = cuda_rc(cudaStreamSynchronize(r.st));
+    if (!rc) rc = copy_state(h, r.snap[r.cur], /*to_snapshot=*/false, s);
+    if (!rc && r.pos) rc = launch_fill<kSkip>(h, 0, 1, r.pos, nullptr, nullptr, s);
+    r.pos = 0;
+    return rc;
 }
 
 bool mul_overflows(uint64_t a, uint64_t b, uint64_t* out) {
@@ -940,9 +961,140 @@ int generate_host_impl(xg_ensemble_t h, uint64_t per_stream, T* host_out, xg_str
     return rc ? rc : (rc2 ? rc2 : rc3);
 }
 
+// BlockEnsemble::generate into caller-owned rows (one uint64 row per stream,
+// the reference's vector<vector<uint64_t>> layout): tiles of streams x words
+// are generated on `s` as u32 (w <= 32; 4 PCIe bytes per word instead of 8),
+// copied to pinned staging on a second stream, and widened into the rows by
+// host threads while the device already produces and copies the next tile.
+template <int MODE, class T>
+int generate_rows_impl(xg_ensemble_t h, uint64_t per_stream, uint64_t* const* rows, cudaStream_t s) {
+    constexpr uint64_t kSlotWords = (1ull << 28) / sizeof(T);  // 256 MiB per staging slot
+    constexpr uint64_t kGroup = 2048;
+    uint64_t cnt_max, m_max;
+    if (per_stream <= kSlotWords) {
+        m_max = per_stream;
+        cnt_max = std::min<uint64_t>(std::max<uint64_t>(1, kSlotWords / per_stream), h->num_streams);
+    } else {
+        cnt_max = std::min<uint64_t>(kGroup, h->num_streams);
+        m_max = (kSlotWords / cnt_max) & ~uint64_t{127};
+    }
+    const uint64_t slot_words = cnt_max * m_max;
+    const size_t slot_bytes = slot_words * sizeof(T);
+    int rc = XG_OK;
+    if (h->stage_words < 2 * slot_bytes) {
+        cudaFree(h->d_stage);
+        h->d_stage = nullptr;
+        h->stage_words = 0;
+        rc = cuda_rc(cudaMalloc(&h->d_stage, 2 * slot_bytes));
+        if (rc) return rc;
+        h->stage_words = 2 * slot_bytes;
+    }
+    if (h->h_stage_bytes < 2 * slot_bytes) {
+        cudaFreeHost(h->h_stage);
+        h->h_stage = nullptr;
+        h->h_stage_bytes = 0;
+        rc = cuda_rc(cudaMallocHost(&h->h_stage, 2 * slot_bytes));
+        if (rc) return rc;
+        h->h_stage_bytes = 2 * slot_bytes;
+    }
+    struct Tile {
+        uint64_t g0, k0, cnt, m;
+    };
+    std::vector<Tile> tiles;
+    for (uint64_t g0 = 0; g0 < h->num_streams; g0 += cnt_max) {
+        const uint64_t cnt = std::min<uint64_t>(cnt_max, h->num_streams - g0);
+        for (uint64_t k0 = 0; k0 < per_stream; k0 += m_max)
+            tiles.push_back({g0, k0, cnt, std::min<uint64_t>(m_max, per_stream - k0)});
+    }
+    cudaStream_t cs;
+    rc = cuda_rc(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    if (rc) return rc;
+    cudaEvent_t gen_done[2], copy_done[2];
+    for (int i = 0; i < 2; ++i) {
+        cudaEventCreateWithFlags(&gen_done[i], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&copy_done[i], cudaEventDisableTiming);
+    }
+    auto enqueue = [&](size_t t) {
+        const Tile& tl = tiles[t];
+        const int slot = static_cast<int>(t & 1);
+        T* d = static_cast<T*>(h->d_stage) + slot * slot_words;
+        T* hs = static_cast<T*>(h->h_stage) + slot * slot_words;
+        int e = launch_fill<MODE>(h, static_cast<uint32_t>(tl.g0), static_cast<uint32_t>(tl.cnt), tl.m, d,
+                                  nullptr, s);
+        if (!e) e = cuda_rc(cudaEventRecord(gen_done[slot], s));
+        if (!e) e = cuda_rc(cudaStreamWaitEvent(cs, gen_done[slot], 0));
+        if (!e) e = cuda_rc(cudaMemcpyAsync(hs, d, tl.cnt * tl.m * sizeof(T), cudaMemcpyDeviceToHost, cs));
+        if (!e) e = cuda_rc(cudaEventRecord(copy_done[slot], cs));
+        return e;
+    };
+    const unsigned nthr = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    if (!tiles.empty()) rc = enqueue(0);
+    for (size_t t = 0; t < tiles.size() && !rc; ++t) {
+        // Tile t+1 goes into the slot tile t-1 used, whose rows were written
+        // in the previous iteration.
+        if (t + 1 < tiles.size()) rc = enqueue(t + 1);
+        if (!rc) rc = cuda_rc(cudaEventSynchronize(copy_done[t & 1]));
+        if (rc) break;
+        const Tile tl = tiles[t];
+        const T* hs = static_cast<const T*>(h->h_stage) + (t & 1) * slot_words;
+        auto widen = [&, tl, hs](unsigned id) {
+            // rows split between threads; one long row split by words
+            const uint64_t parts = tl.cnt >= nthr ? tl.cnt : nthr;
+            for (uint64_t q = id; q < parts; q += nthr) {
+                uint64_t i0, i1, k0, k1;
+                if (tl.cnt >= nthr) {
+                    i0 = q; i1 = q + 1; k0 = 0; k1 = tl.m;
+                } else {
+                    const uint64_t per_row = nthr / tl.cnt;  // threads per row (>= 1)
+                    const uint64_t row = q / per_row, sub = q % per_row;
+                    if (row >= tl.cnt) continue;
+                    i0 = row; i1 = row + 1;
+                    k0 = tl.m * sub / per_row; k1 = tl.m * (sub + 1) / per_row;
+                }
+                for (uint64_t i = i0; i < i1; ++i) {
+                    uint64_t* dst = rows[tl.g0 + i] + tl.k0;
+                    const T* src = hs + i * tl.m;
+                    for (uint64_t k = k0; k < k1; ++k) dst[k] = src[k];
+                }
+            }
+        };
+        std::vector<std::thread> pool;
+        pool.reserve(nthr - 1);
+        for (unsigned id = 1; id < nthr; ++id) pool.emplace_back(widen, id);
+        widen(0);
+        for (auto& th : pool) th.join();
+    }
+    const int rc2 = cuda_rc(cudaStreamSynchronize(cs));
+    const int rc3 = cuda_rc(cudaStreamSynchronize(s));
+    for (int i = 0; i < 2; ++i) {
+        cudaEventDestroy(gen_done[i]);
+        cudaEventDestroy(copy_done[i]);
+    }
+    cudaStreamDestroy(cs);
+    return rc ? rc : (rc2 ? rc2 : rc3);
+}
+
 }  // namespace
 
 extern "C" {
+
+int xg_generate_host_rows(xg_ensemble_t h, uint64_t per_stream, uint64_t* const* rows,
+                          xg_stream_t stream) {
+    if (!h) return XG_EINVAL;
+    uint64_t total;
+    if (mul_overflows(per_stream, h->num_streams, &total)) return XG_EINVAL;
+    if (per_stream == 0) return XG_OK;
+    if (!rows) return XG_EINVAL;
+    for (uint32_t g = 0; g < h->num_streams; ++g)
+        if (!rows[g]) return XG_EINVAL;
+    DeviceGuard dg(h->device);
+    if (!dg.ok) return XG_ECUDA;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = settle_next(h, s);
+    if (rc) return rc;
+    if (h->params.w <= 32) return generate_rows_impl<kU32, uint32_t>(h, per_stream, rows, s);
+    return generate_rows_impl<kWide, uint64_t>(h, per_stream, rows, s);
+}
 
 int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,
                      xg_stream_t stream) {
@@ -955,36 +1107,109 @@ int xg_generate_host_words(xg_ensemble_t h, uint64_t per_stream, uint64_t* host_
     return generate_host_impl<kWide>(h, per_stream, host_out, stream);
 }
 
+}  // extern "C"
+
+namespace {
+
+// One refill of ring slot i on the ring's stream: save the state, generate
+// kNextBuf words of the (single) stream, copy them to the pinned slot.
+int ring_refill(xg_ensemble* h, int i) {
+    auto& r = h->nr;
+    int rc = copy_state(h, r.snap[i], /*to_snapshot=*/true, r.st);
+    if (!rc)
+        rc = r.eb == 4 ? launch_fill<kU32>(h, 0, 1, kNextBuf, r.dev[i], nullptr, r.st)
+                       : launch_fill<kWide>(h, 0, 1, kNextBuf, r.dev[i], nullptr, r.st);
+    if (!rc) rc = cuda_rc(cudaMemcpyAsync(r.host[i], r.dev[i], kNextBuf * r.eb, cudaMemcpyDeviceToHost, r.st));
+    if (!rc) rc = cuda_rc(cudaEventRecord(r.ev[i], r.st));
+    return rc;
+}
+
+// Make slot `cur` hold unserved words: the first call (or the first after
+// a settle) orders after all device work, then queues both slots; later
+// calls wait for the slot generated in the background and queue the next
+// refill into the slot just consumed, so generation and the PCIe copy of
+// slot i+1 overlap the host's consumption of slot i.
+int ring_next(xg_ensemble* h) {
+    auto& r = h->nr;
+    DeviceGuard dg(h->device);
+    if (!dg.ok) return XG_ECUDA;
+    int rc = XG_OK;
+    if (!r.st) {
+        r.eb = h->params.w > 32 ? 8 : 4;
+        size_t wb;
+        const size_t sb = state_bytes(h, &wb);
+        rc = cuda_rc(cudaStreamCreateWithFlags(&r.st, cudaStreamNonBlocking));
+        for (int i = 0; i < 2 && !rc; ++i) {
+            rc = cuda_rc(cudaMallocHost(&r.host[i], kNextBuf * r.eb));
+            if (!rc) rc = cuda_rc(cudaMalloc(&r.dev[i], kNextBuf * r.eb));
+            if (!rc) rc = cuda_rc(cudaMalloc(&r.snap[i], sb));
+            if (!rc) rc = cuda_rc(cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming));
+        }
+        if (rc) return rc;
+    }
+    if (!r.active) {
+        // Host-synchronous start: order after any work queued on any stream.
+        rc = cuda_rc(cudaDeviceSynchronize());
+        if (!rc) rc = ring_refill(h, 0);
+        if (!rc) rc = ring_refill(h, 1);
+        if (!rc) rc = cuda_rc(cudaEventSynchronize(r.ev[0]));
+        if (rc) return rc;
+        r.cur = 0;
+    } else {
+        const int nxt = r.cur ^ 1;
+        rc = cuda_rc(cudaEventSynchronize(r.ev[nxt]));
+        if (!rc) rc = ring_refill(h, r.cur);
+        if (rc) return rc;
+        r.cur = nxt;
+    }
+    r.pos = 0;
+    r.active = true;
+    return XG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 // XorgensState::next_word (proj/include/xg/xorgens.hpp:58-62): the w-bit
 // word in a uint64, served from device-generated refills of kNextBuf words.
 int xg_next_word(xg_ensemble_t h, uint64_t* out) {
     if (!h || !out) return XG_EINVAL;
-    if (h->num_streams != 1) return XG_EINVAL;
-    if (h->npos < h->nbuf.size()) {
-        *out = h->nbuf[h->npos++];
+    auto& r = h->nr;
+    if (r.active && r.pos < kNextBuf) {
+        *out = r.eb == 4 ? static_cast<const uint32_t*>(r.host[r.cur])[r.pos++]
+                         : static_cast<const uint64_t*>(r.host[r.cur])[r.pos++];
         return XG_OK;
     }
-    DeviceGuard dg(h->device);
-    if (!dg.ok) return XG_ECUDA;
-    // Host-synchronous call: order after any fill the caller queued on any stream.
-    int rc = cuda_rc(cudaDeviceSynchronize());
-    size_t wb;
-    const size_t snap_bytes = state_bytes(h, &wb);
-    if (!rc && !h->d_snap) rc = cuda_rc(cudaMalloc(&h->d_snap, snap_bytes));
-    if (!rc && !h->d_scratch) rc = cuda_rc(cudaMalloc(&h->d_scratch, kNextBuf * sizeof(uint64_t)));
+    if (h->num_streams != 1) return XG_EINVAL;
+    int rc = ring_next(h);
     if (rc) return rc;
-    cudaStream_t s = nullptr;
-    rc = copy_state(h, h->d_snap, /*to_snapshot=*/true, s);
-    if (!rc) rc = launch_fill<kWide>(h, 0, 1, kNextBuf, h->d_scratch, nullptr, s);
-    h->nbuf.assign(kNextBuf, 0);
-    if (!rc) rc = cuda_rc(cudaMemcpy(h->nbuf.data(), h->d_scratch, kNextBuf * 8, cudaMemcpyDeviceToHost));
-    if (rc) {
-        h->nbuf.clear();
-        h->npos = 0;
-        return rc;
+    *out = r.eb == 4 ? static_cast<const uint32_t*>(r.host[r.cur])[r.pos++]
+                     : static_cast<const uint64_t*>(r.host[r.cur])[r.pos++];
+    return XG_OK;
+}
+
+int xg_next_view(xg_ensemble_t h, const void** words, uint64_t* count, unsigned* elem_bytes) {
+    if (!h || !words || !count || !elem_bytes) return XG_EINVAL;
+    if (h->num_streams != 1) return XG_EINVAL;
+    auto& r = h->nr;
+    if (!r.active || r.pos >= kNextBuf) {
+        int rc = ring_next(h);
+        if (rc) return rc;
     }
-    h->npos = 0;
-    *out = h->nbuf[h->npos++];
+    *elem_bytes = r.eb;
+    *words = static_cast<const char*>(r.host[r.cur]) + r.pos * r.eb;
+    *count = kNextBuf - r.pos;
+    r.pos = kNextBuf;  // served, until xg_next_return gives some back
+    return XG_OK;
+}
+
+int xg_next_return(xg_ensemble_t h, uint64_t unread) {
+    if (!h) return XG_EINVAL;
+    auto& r = h->nr;
+    if (unread == 0) return XG_OK;
+    if (!r.active || unread > r.pos) return XG_ERANGE;
+    r.pos -= unread;
     return XG_OK;
 }
 
@@ -1083,8 +1308,6 @@ int xg_state_import_all(xg_ensemble_t h, const uint32_t* host_window, const uint
     if (!dg.ok) return XG_ECUDA;
     int rc = cuda_rc(cudaDeviceSynchronize());
     if (!rc) rc = settle_next(h, nullptr);
-    h->nbuf.clear();
-    h->npos = 0;
     const size_t n = h->num_streams;
     if (!rc) rc = cuda_rc(cudaMemcpy(h->d_win, host_window, n * kR * 4, cudaMemcpyHostToDevice));
     if (!rc) rc = cuda_rc(cudaMemcpy(h->d_weyl, host_weyl, n * 4, cudaMemcpyHostToDevice));

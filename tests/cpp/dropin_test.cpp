@@ -5,6 +5,7 @@
 // libxg_gpu.so.  Every check compares xg:: (reference, CPU) with xg::gpu::
 // (this framework, B200) on the same inputs, through the same calls a C++
 // user of the reference makes.  Exit 0 = all equal.
+#include <cstdint>
 #include <cstdio>
 #include <stdexcept>
 #include <vector>
@@ -49,7 +50,22 @@ int main() {
         xg::gpu::XorgensSource<xg::WordSource> gsrc(p, 77);
         xg::WordSource& as_base = gsrc;
         CHECK(as_base.word_bits() == rsrc.word_bits());
-        for (int i = 0; i < 40000; ++i) CHECK(rsrc.next() == as_base.next());
+        for (int i = 0; i < 300000; ++i) CHECK(rsrc.next() == as_base.next());  // > 4 refill slots
+    }
+    // next_word across refill slots, interleaved with generate(): the unread
+    // words of the inline cache are handed back first, so the stream continues
+    // exactly after the last word the caller saw.
+    {
+        xg::XorgensState r2(p, 2024);
+        xg::gpu::XorgensState g2(p, 2024);
+        for (int round = 0; round < 3; ++round) {
+            for (int i = 0; i < 70001; ++i) CHECK(r2.next_word() == g2.next_word());
+            const auto blk = g2.generate(1001);
+            for (std::uint64_t w : blk[0]) CHECK(r2.next_word() == w);
+        }
+        CHECK(r2.logical_buffer() == g2.logical_buffer());
+        CHECK(r2.weyl_value() == g2.weyl_value());
+        for (int i = 0; i < 10; ++i) CHECK(r2.next_word() == g2.next_word());
     }
     // Checkpoint / resume continues every block exactly.
     {

@@ -728,3 +728,67 @@ def test_gpu_berlekamp_massey_vs_reference(nbits):
     dev = torch.from_numpy(packed.view(np.int32)).cuda()
     got = np_u32(xg.berlekamp_massey(dev, nbits)).tolist()
     assert got == [b.berlekamp_massey(sq) for sq in seqs]
+
+
+def test_next_view_and_return_continue_exactly(oracle):
+    """xg_next_view hands out pinned refill words (double-buffered slots of
+    2^16); xg_next_return gives unread ones back; fills, next_word and the
+    state export then continue right after the last word used."""
+    import ctypes
+
+    L = xg._lib.lib
+    st = xg.XorgensState(GP32, 99)
+    h = st.ensemble.handle
+    ref = oracle.stream(99, 400000)
+    got = []
+    ptr, cnt, eb = ctypes.c_void_p(), ctypes.c_uint64(), ctypes.c_uint()
+    for take in (5, 65531, 70000, 1, 140000):
+        left = take
+        while left:
+            assert L.xg_next_view(h, ctypes.byref(ptr), ctypes.byref(cnt), ctypes.byref(eb)) == 0
+            assert eb.value == 4
+            n = min(left, cnt.value)
+            got += np.ctypeslib.as_array((ctypes.c_uint32 * cnt.value).from_address(ptr.value))[:n].tolist()
+            assert L.xg_next_return(h, cnt.value - n) == 0
+            left -= n
+        got.append(st.next_word())
+        got += np_u32(st.ensemble.fill_u32(777))[0].tolist()
+    assert np.array_equal(np.array(got, dtype=np.uint32), ref[:len(got)])
+    assert L.xg_next_return(h, 1) == xg._lib.XG_ERANGE  # nothing held after the fill
+    b, w = st.logical_buffer(), st.weyl_value()
+    o = oracle.ensemble(99, 1)
+    o.fill_u32(len(got))
+    assert np.array_equal(np.array(b, dtype=np.uint64), o.logical_buffer(0)) and w == o.weyl(0)
+
+
+def test_next_word_many_slots_w64_and_tiny(reference):
+    """The ring for the general-parameter path: w = 64 (8-byte slots) and a
+    tiny w = 8 set, against the reference sources, across slot boundaries."""
+    w64 = xg.GeneratorParams(64, 53, 33, 26, 27, 29, 64, 0x9E3779B97F4A7C15, 32)
+    for p in (w64, xg.tiny_r2w8_params()):
+        st = xg.XorgensState(p, 3)
+        got = [st.next_word() for _ in range(140000)]
+        pr = Params(p.r, p.s, p.a, p.b, p.c, p.d, p.w, p.omega, p.gamma)
+        assert np.array_equal(np.array(got, dtype=np.uint64), reference.stream(3, 140000, pr))
+
+
+def test_generate_host_rows_tiles_and_rows(oracle):
+    """xg_generate_host_rows (the C++ generate() path): caller-owned uint64
+    rows, u32 over PCIe widened by host threads; multi-tile shapes (a stream
+    longer than one 256 MiB staging slot; many streams per tile) equal the
+    device fill of a twin ensemble, and calls continue the streams."""
+    import ctypes
+
+    L = xg._lib.lib
+    for P, per in ((3, (1 << 26) + 77), (5000, 6000), (1, 1)):
+        a = xg.BlockEnsemble(GP32, 17, P, 63)
+        b = xg.BlockEnsemble(GP32, 17, P, 63)
+        for _ in range(2):
+            rows = [np.full(per, 0xDEADBEEFDEADBEEF, dtype=np.uint64) for _ in range(P)]
+            arr = (ctypes.c_void_p * P)(*[r.ctypes.data for r in rows])
+            assert L.xg_generate_host_rows(a.handle, per, arr, None) == 0
+            dev = np_u32(b.fill_u32(per))
+            for g in (0, P // 2, P - 1):
+                assert np.array_equal(rows[g], dev[g].astype(np.uint64)), (P, per, g)
+            del dev
+    assert L.xg_generate_host_rows(a.handle, 4, None, None) == xg._lib.XG_EINVAL
