@@ -421,6 +421,8 @@ def write_ceiling(out, stream, reps: int = 5) -> dict:
         "memset": lambda: lib.xg_probe_memset(ptr, nbytes, sp),
         "rows_stg64_4w_cap4": lambda: lib.xg_probe_rows(ptr, nbytes, row, 8, 4, 4, sp),
         "rows_stg128_4w_cap4": lambda: lib.xg_probe_rows(ptr, nbytes, row, 16, 4, 4, sp),
+        "rows_stg256_4w_cap4": lambda: lib.xg_probe_rows(ptr, nbytes, row, 32, 4, 4, sp),
+        "rows_stg64_4w_cap2": lambda: lib.xg_probe_rows(ptr, nbytes, row, 8, 4, 2, sp),
         "rows_stg128_8w_nocap": lambda: lib.xg_probe_rows(ptr, nbytes, row, 16, 8, 0, sp),
         "gridstride_stg128": lambda: lib.xg_probe_gridstride(ptr, nbytes, sp),
     }

@@ -177,7 +177,7 @@ __device__ __forceinline__ void pair_emit(uint2 v, void* o, int j, unsigned limi
     } else if constexpr (MODE == kF64) {
         if (!TAIL || 32u * j + lane < limit) __stcs(static_cast<double*>(o) + 32 * j, raw_pair_to_f64(v.x, v.y));
     } else if constexpr (MODE == kMC) {
-        if (!TAIL || 32u * j + lane < limit) hits += mc_hit(v.x, v.y);
+        if (!TAIL || 32u * j + lane < limit) mc_count(hits, mc_hit(v.x, v.y));
     } else if constexpr (MODE == kRank) {
         // this double step holds matrices 2j and 2j+1 of the body
         unsigned ra, rb;

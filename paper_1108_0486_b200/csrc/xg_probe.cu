@@ -6,7 +6,8 @@
 //   xg_probe_memset       cudaMemsetAsync over the buffer (the driver's fill)
 //   xg_probe_rows         the fill kernel's store shape without the generator:
 //                         one warp per row of `row_bytes`, `vec` = 8 (STG.64,
-//                         as pair_kernel stores u32 pairs) or 16 (STG.128)
+//                         as pair_kernel stores u32 pairs), 16 (STG.128) or 32
+//                         (STG.256)
 //                         byte evict-first stores, `warps` rows per CTA and at
 //                         most `cap` resident CTAs per SM (0 = no cap) -- the
 //                         same occupancy trick as launch_pair (xg_gpu.cu).
@@ -31,11 +32,18 @@ __global__ void __launch_bounds__(1024) row_store(char* __restrict__ dst, uint64
         const uint2 val = make_uint2(v, v ^ lane);
 #pragma unroll 4
         for (uint64_t i = 0; i < n; ++i) __stcs(p + 32 * i, val);
-    } else {
+    } else if constexpr (VEC == 16) {
         uint4* p = reinterpret_cast<uint4*>(r) + lane;
         const uint4 val = make_uint4(v, v ^ lane, v, v);
 #pragma unroll 4
         for (uint64_t i = 0; i < n; ++i) __stcs(p + 32 * i, val);
+    } else {  // 32-byte stores (STG.E.ENL2.256, sm_100)
+        char* p = r + 32 * lane;
+        const uint32_t a = v, b = v ^ lane;
+#pragma unroll 4
+        for (uint64_t i = 0; i < n; ++i)
+            asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%1,%2,%1,%2,%1,%2};"
+                         :: "l"(p + 1024 * i), "r"(a), "r"(b) : "memory");
     }
 }
 
@@ -64,7 +72,7 @@ int xg_probe_memset(void* dst, size_t bytes, void* stream) {
 
 int xg_probe_rows(void* dst, size_t bytes, uint64_t row_bytes, int vec, int warps, int cap,
                   void* stream) {
-    if (row_bytes == 0 || row_bytes % (32 * 16) != 0 || warps < 1 || warps > 32) return 2;
+    if (row_bytes == 0 || row_bytes % (32 * 32) != 0 || warps < 1 || warps > 32) return 2;
     const uint32_t rows = static_cast<uint32_t>(bytes / row_bytes);
     const unsigned grid = (rows + warps - 1) / warps;
     size_t smem = 0;
@@ -84,7 +92,7 @@ int xg_probe_rows(void* dst, size_t bytes, uint64_t row_bytes, int vec, int warp
             static_cast<char*>(dst), row_bytes, rows, 0x9e3779b9u);
         return cudaGetLastError() == cudaSuccess ? 0 : 1;
     };
-    return vec == 8 ? launch(row_store<8>) : launch(row_store<16>);
+    return vec == 8 ? launch(row_store<8>) : vec == 16 ? launch(row_store<16>) : launch(row_store<32>);
 }
 
 int xg_probe_gridstride(void* dst, size_t bytes, void* stream) {

@@ -45,3 +45,23 @@ from paper_1108_0486_b200.battery import BatteryConfig, run_battery_gpu  # noqa:
 rep = run_battery_gpu(p, 3, BatteryConfig.quick())
 assert rep["num_tests"] == 5
 print("sanitize stattests ok")
+
+# round 2: the digest kernel, the next_word ring (past two slots, interleaved
+# with a fill) and generate() into caller rows
+from paper_1108_0486_b200.digest import row_digests  # noqa: E402
+w = e.fill_u32(1000)
+x, s, ws = row_digests(w)
+ref = w.cpu().numpy()
+assert np.array_equal(x, np.bitwise_xor.reduce(ref, axis=1))
+st = xg.XorgensState(p, 77)
+got = [st.next_word() for _ in range(70000)]
+got += st.ensemble.fill_u32(333).cpu().numpy()[0].tolist()
+got += [st.next_word() for _ in range(70000)]
+assert np.array_equal(np.array(got, dtype=np.uint64), o.stream(77, len(got)))
+import ctypes  # noqa: E402
+rows = [np.zeros(777, dtype=np.uint64) for _ in range(9)]
+arr = (ctypes.c_void_p * 9)(*[r.ctypes.data for r in rows])
+e2 = xg.BlockEnsemble(p, 5, 9, 63)
+assert xg._lib.lib.xg_generate_host_rows(e2.handle, 777, arr, None) == 0
+assert np.array_equal(np.stack(rows), o.ensemble(5, 9).fill_u32(777).astype(np.uint64))
+print("sanitize round-2 paths ok")

@@ -792,3 +792,20 @@ def test_generate_host_rows_tiles_and_rows(oracle):
                 assert np.array_equal(rows[g], dev[g].astype(np.uint64)), (P, per, g)
             del dev
     assert L.xg_generate_host_rows(a.handle, 4, None, None) == xg._lib.XG_EINVAL
+
+
+def test_hostbench_runs_reference_methods_over_dropin():
+    """xg_hostbench (the reference's measure_throughput and
+    measure_ensemble_throughput over xg::gpu) runs and reports rates."""
+    import json
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "paper_1108_0486_b200", "lib", "xg_hostbench")
+    r = subprocess.run([exe, str(10**6), "3", "64", str(1 << 20)], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr
+    d = json.loads(r.stdout)
+    assert d["measure_throughput"]["rn_per_s"]["mean"] > 0
+    assert d["measure_ensemble_throughput"]["rn_per_s"]["mean"] > 0
