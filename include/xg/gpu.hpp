@@ -105,27 +105,30 @@ public:
     }
 
     // proj/include/xg/parallel.hpp:46-47: block-major, continues every block.
-    // The rows are allocated by `workers` host threads (hardware_concurrency
-    // when 0, as the reference's workers, parallel.cpp:115-116) and filled in
-    // place by xg_generate_host_rows: words cross PCIe once, as u32, and are
-    // widened straight into each block's vector -- no intermediate copy.
+    // The rows are reserved by the host threads (no page is touched) and
+    // filled tile by tile straight from pinned staging by
+    // xg_generate_host_tiles: words cross PCIe once, as u32, and each block's
+    // vector<uint64_t> is appended to in one pass (insert widens u32 ->
+    // uint64) while the device generates and copies the next tile.
+    // `workers` = host threads (0: hardware_concurrency), as the reference's
+    // workers (parallel.cpp:115-116); the output never depends on it.
     std::vector<std::vector<std::uint64_t>> generate(std::size_t per_block,
                                                      unsigned workers = 0) {
         std::vector<std::vector<std::uint64_t>> out(n_);
+        if (!per_block) return out;
+        const xg_ensemble_t hh = h();
         unsigned t = workers ? workers : std::max(1u, std::thread::hardware_concurrency());
-        t = std::min<unsigned>(t, std::max(1u, n_));
-        auto alloc = [&](unsigned id) {
-            for (unsigned i = id; i < n_; i += t) out[i].resize(per_block);
-        };
-        std::vector<std::thread> pool;
-        for (unsigned id = 1; id < t; ++id) pool.emplace_back(alloc, id);
-        alloc(0);
-        for (auto& th : pool) th.join();
-        if (per_block) {
-            std::vector<std::uint64_t*> rows(n_);
-            for (unsigned i = 0; i < n_; ++i) rows[i] = out[i].data();
-            check(xg_generate_host_rows(h(), per_block, rows.data(), nullptr));
+        t = std::min(t, 32u);
+        {
+            const unsigned ta = std::min<unsigned>(t, std::max(1u, n_));
+            std::vector<std::thread> pool;
+            for (unsigned id = 0; id < ta; ++id)
+                pool.emplace_back([&, id] {
+                    for (unsigned i = id; i < n_; i += ta) out[i].reserve(per_block);
+                });
+            for (auto& th : pool) th.join();
         }
+        check(xg_generate_host_tiles(hh, per_block, &append_tile, &out, t, nullptr));
         return out;
     }
 
@@ -205,6 +208,24 @@ protected:
     xg_ensemble_t h() const {
         give_back();
         return h_;
+    }
+    // xg_tile_fn of generate(): part `part` of `parts` appends rows
+    // stream0 + part, + parts, ... of the tile (a stream's tiles arrive in
+    // word order, one thread per row).
+    static void append_tile(void* ctx, std::uint64_t stream0, std::uint64_t, std::uint64_t streams,
+                            std::uint64_t words, const void* tile, unsigned elem_bytes, unsigned part,
+                            unsigned parts) {
+        auto& out = *static_cast<std::vector<std::vector<std::uint64_t>>*>(ctx);
+        for (std::uint64_t i = part; i < streams; i += parts) {
+            auto& row = out[stream0 + i];
+            if (elem_bytes == 4) {
+                const auto* src = static_cast<const std::uint32_t*>(tile) + i * words;
+                row.insert(row.end(), src, src + words);
+            } else {
+                const auto* src = static_cast<const std::uint64_t*>(tile) + i * words;
+                row.insert(row.end(), src, src + words);
+            }
+        }
     }
     xg_ensemble_t h_ = nullptr;
     unsigned n_ = 0;

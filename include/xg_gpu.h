@@ -183,6 +183,18 @@ int xg_linear_complexity_test(xg_ensemble_t h, unsigned block_length, uint64_t b
  * i / 32): dev_L[q] = its linear complexity.  One warp per sequence. */
 int xg_berlekamp_massey(const uint32_t* dev_seqs, uint64_t nbits, uint32_t count,
                         uint64_t stride_words, uint32_t* dev_L, xg_stream_t stream);
+/* matrix_rank_test's counting loop (tests.cpp:93-109) over a device word
+ * buffer: matrix k = words [32k, 32k+32), row i = word i (bits MSB first);
+ * dev_counts[0..2] += matrices of rank 32, 31, <= 30.  For any word source
+ * (file words, the raw stream, sets xg_rank_test does not take). */
+int xg_rank_words(const uint32_t* dev_words, uint64_t matrices, uint64_t* dev_counts,
+                  xg_stream_t stream);
+/* linear_complexity_test's per-block Berlekamp-Massey (tests.cpp:128-178)
+ * over a device word buffer read MSB first: `blocks` blocks of block_length
+ * bits (<= 2^18) from bit 0; dev_hist[L] += 1 per block (XG_EINVAL if the
+ * buffer holds fewer than block_length * blocks bits). */
+int xg_lc_words(const uint32_t* dev_words, uint64_t nwords, unsigned block_length, uint64_t blocks,
+                uint64_t* dev_hist, xg_stream_t stream);
 /* Counting loops of monobit and runs_test (proj/src/stattests/tests.cpp:33-79)
  * over the first nbits bits of a device word buffer read MSB first (as
  * BitSource reads 32-bit words): dev_out2[0] += ones, dev_out2[1] +=
@@ -224,6 +236,20 @@ int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,
  * tile is generated and copied. */
 int xg_generate_host_rows(xg_ensemble_t h, uint64_t per_stream, uint64_t* const* rows,
                           xg_stream_t stream);
+/* generate() handed to the caller tile by tile, straight from pinned
+ * staging: for each tile (streams [stream0, stream0 + streams), words
+ * [word0, word0 + words) of each, row-major, elements of elem_bytes = 4 for
+ * w <= 32 else 8), fn is called once on each of `parts` host threads (part =
+ * 0 .. parts-1, threads = 0: hardware_concurrency up to 32) and may split the
+ * tile between them; the next tile is generated and copied meanwhile.  A
+ * stream's tiles arrive in word order, so fn can append (what
+ * xg::gpu::BlockEnsemble::generate does: vector<uint64_t>::insert into
+ * reserved rows, one pass over host memory). */
+typedef void (*xg_tile_fn)(void* ctx, uint64_t stream0, uint64_t word0, uint64_t streams,
+                           uint64_t words, const void* tile, unsigned elem_bytes, unsigned part,
+                           unsigned parts);
+int xg_generate_host_tiles(xg_ensemble_t h, uint64_t per_stream, xg_tile_fn fn, void* ctx,
+                           unsigned threads, xg_stream_t stream);
 /* The same with every word in the reference's uint64 container -- exactly
  * the element type of generate()'s result; any w, including 64. */
 int xg_generate_host_words(xg_ensemble_t h, uint64_t per_stream, uint64_t* host_out,

@@ -67,6 +67,8 @@ SIGNATURES = {
     "xg_rank_test": (_int, [_vp, _u64, _vp, _vp]),
     "xg_linear_complexity_test": (_int, [_vp, ctypes.c_uint, _u64, _vp, _vp]),
     "xg_berlekamp_massey": (_int, [_vp, _u64, _u32, _u64, _vp, _vp]),
+    "xg_rank_words": (_int, [_vp, _u64, _vp, _vp]),
+    "xg_lc_words": (_int, [_vp, _u64, ctypes.c_uint, _u64, _vp, _vp]),
     "xg_bits_ones_runs": (_int, [_vp, _u64, _vp, _vp]),
     "xg_birthday_duplicates": (_int, [_vp, _u32, _u32, ctypes.c_uint, _vp, _vp]),
     "xg_digest_u32": (_int, [_vp, _u64, _u64, _vp, _vp, _vp, _vp]),
@@ -74,6 +76,7 @@ SIGNATURES = {
     "xg_generate_host": (_int, [_vp, _u64, _vp, _vp]),
     "xg_generate_host_words": (_int, [_vp, _u64, _vp, _vp]),
     "xg_generate_host_rows": (_int, [_vp, _u64, _vp, _vp]),
+    "xg_generate_host_tiles": (_int, [_vp, _u64, _vp, _vp, ctypes.c_uint, _vp]),
     "xg_next_word": (_int, [_vp, _P(_u64)]),
     "xg_next_view": (_int, [_vp, _P(_vp), _P(_u64), _P(ctypes.c_uint)]),
     "xg_next_return": (_int, [_vp, _u64]),

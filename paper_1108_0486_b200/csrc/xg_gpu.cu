@@ -812,6 +812,49 @@ int xg_berlekamp_massey(const uint32_t* dev_seqs, uint64_t nbits, uint32_t count
                           dev_L, s);
 }
 
+int xg_rank_words(const uint32_t* dev_words, uint64_t matrices, uint64_t* dev_counts,
+                  xg_stream_t stream) {
+    if (!dev_words || !dev_counts || (reinterpret_cast<uintptr_t>(dev_counts) % 8) != 0) return XG_EINVAL;
+    if (matrices == 0) return XG_OK;
+    if (matrices > (1ull << 58)) return XG_EINVAL;
+    int dev;
+    int rc = ptr_device(dev_words, &dev);
+    if (rc) return rc;
+    DeviceGuard dg(dev);
+    if (!dg.ok) return XG_ECUDA;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t pairs = (matrices + 1) / 2;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((pairs + 7) / 8, 8ull * sms));
+    rank_words_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        dev_words, matrices, reinterpret_cast<unsigned long long*>(dev_counts));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cuda_rc(cudaGetLastError());
+}
+
+int xg_lc_words(const uint32_t* dev_words, uint64_t nwords, unsigned block_length, uint64_t blocks,
+                uint64_t* dev_hist, xg_stream_t stream) {
+    if (!dev_words || !dev_hist || (reinterpret_cast<uintptr_t>(dev_hist) % 8) != 0) return XG_EINVAL;
+    if (block_length == 0 || block_length > kBmMaxBits || blocks > 0xffffffffull) return XG_EINVAL;
+    if (blocks == 0) return XG_OK;
+    if (nwords * 32 < static_cast<uint64_t>(block_length) * blocks) return XG_EINVAL;
+    int dev;
+    int rc = ptr_device(dev_words, &dev);
+    if (rc) return rc;
+    DeviceGuard dg(dev);
+    if (!dg.ok) return XG_ECUDA;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    auto* hist = reinterpret_cast<unsigned long long*>(dev_hist);
+    if (block_length <= kLcMaxK) {
+        lc_kernel<<<static_cast<unsigned>((blocks + 7) / 8), 256, 0, s>>>(
+            dev_words, 1, nwords, block_length, static_cast<uint32_t>(blocks), hist);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return cuda_rc(cudaGetLastError());
+    }
+    return launch_bm_long(dev_words, nwords, block_length, block_length, static_cast<uint32_t>(blocks),
+                          static_cast<uint64_t>(block_length) * blocks, blocks, hist, nullptr, s);
+}
+
 int xg_bits_ones_runs(const uint32_t* dev_words, uint64_t nbits, uint64_t* dev_out2,
                       xg_stream_t stream) {
     if (!dev_words || !dev_out2 || (reinterpret_cast<uintptr_t>(dev_out2) % 8) != 0) return XG_EINVAL;
@@ -961,13 +1004,15 @@ int generate_host_impl(xg_ensemble_t h, uint64_t per_stream, T* host_out, xg_str
     return rc ? rc : (rc2 ? rc2 : rc3);
 }
 
-// BlockEnsemble::generate into caller-owned rows (one uint64 row per stream,
-// the reference's vector<vector<uint64_t>> layout): tiles of streams x words
-// are generated on `s` as u32 (w <= 32; 4 PCIe bytes per word instead of 8),
-// copied to pinned staging on a second stream, and widened into the rows by
-// host threads while the device already produces and copies the next tile.
-template <int MODE, class T>
-int generate_rows_impl(xg_ensemble_t h, uint64_t per_stream, uint64_t* const* rows, cudaStream_t s) {
+// BlockEnsemble::generate through host tiles: tiles of streams x words are
+// generated on `s` as u32 (w <= 32; 4 PCIe bytes per word instead of 8),
+// copied to pinned staging on a second stream, and handed to `consume` on
+// nthr host threads (consume(g0, k0, streams, words, tile, id, nthr)) while
+// the device already produces and copies the next tile.  Tiles of one stream
+// arrive in word order.
+template <int MODE, class T, class Consume>
+int generate_tiles_impl(xg_ensemble_t h, uint64_t per_stream, unsigned nthr, Consume consume,
+                        cudaStream_t s) {
     constexpr uint64_t kSlotWords = (1ull << 28) / sizeof(T);  // 256 MiB per staging slot
     constexpr uint64_t kGroup = 2048;
     uint64_t cnt_max, m_max;
@@ -1027,7 +1072,6 @@ int generate_rows_impl(xg_ensemble_t h, uint64_t per_stream, uint64_t* const* ro
         if (!e) e = cuda_rc(cudaEventRecord(copy_done[slot], cs));
         return e;
     };
-    const unsigned nthr = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
     if (!tiles.empty()) rc = enqueue(0);
     for (size_t t = 0; t < tiles.size() && !rc; ++t) {
         // Tile t+1 goes into the slot tile t-1 used, whose rows were written
@@ -1038,25 +1082,7 @@ int generate_rows_impl(xg_ensemble_t h, uint64_t per_stream, uint64_t* const* ro
         const Tile tl = tiles[t];
         const T* hs = static_cast<const T*>(h->h_stage) + (t & 1) * slot_words;
         auto widen = [&, tl, hs](unsigned id) {
-            // rows split between threads; one long row split by words
-            const uint64_t parts = tl.cnt >= nthr ? tl.cnt : nthr;
-            for (uint64_t q = id; q < parts; q += nthr) {
-                uint64_t i0, i1, k0, k1;
-                if (tl.cnt >= nthr) {
-                    i0 = q; i1 = q + 1; k0 = 0; k1 = tl.m;
-                } else {
-                    const uint64_t per_row = nthr / tl.cnt;  // threads per row (>= 1)
-                    const uint64_t row = q / per_row, sub = q % per_row;
-                    if (row >= tl.cnt) continue;
-                    i0 = row; i1 = row + 1;
-                    k0 = tl.m * sub / per_row; k1 = tl.m * (sub + 1) / per_row;
-                }
-                for (uint64_t i = i0; i < i1; ++i) {
-                    uint64_t* dst = rows[tl.g0 + i] + tl.k0;
-                    const T* src = hs + i * tl.m;
-                    for (uint64_t k = k0; k < k1; ++k) dst[k] = src[k];
-                }
-            }
+            consume(tl.g0, tl.k0, tl.cnt, tl.m, hs, id, nthr);
         };
         std::vector<std::thread> pool;
         pool.reserve(nthr - 1);
@@ -1092,8 +1118,50 @@ int xg_generate_host_rows(xg_ensemble_t h, uint64_t per_stream, uint64_t* const*
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     int rc = settle_next(h, s);
     if (rc) return rc;
-    if (h->params.w <= 32) return generate_rows_impl<kU32, uint32_t>(h, per_stream, rows, s);
-    return generate_rows_impl<kWide, uint64_t>(h, per_stream, rows, s);
+    const unsigned nthr = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    // rows split between threads; one long row split by words
+    auto copy = [rows](uint64_t g0, uint64_t kb, uint64_t cnt, uint64_t m, const auto* hs, unsigned id,
+                       unsigned nt) {
+        const uint64_t parts = cnt >= nt ? cnt : nt;
+        for (uint64_t q = id; q < parts; q += nt) {
+            uint64_t i, k0, k1;
+            if (cnt >= nt) {
+                i = q; k0 = 0; k1 = m;
+            } else {
+                const uint64_t per_row = nt / cnt;  // threads per row (>= 1)
+                i = q / per_row;
+                const uint64_t sub = q % per_row;
+                if (i >= cnt) continue;
+                k0 = m * sub / per_row; k1 = m * (sub + 1) / per_row;
+            }
+            uint64_t* dst = rows[g0 + i] + kb;
+            const auto* src = hs + i * m;
+            for (uint64_t k = k0; k < k1; ++k) dst[k] = src[k];
+        }
+    };
+    if (h->params.w <= 32) return generate_tiles_impl<kU32, uint32_t>(h, per_stream, nthr, copy, s);
+    return generate_tiles_impl<kWide, uint64_t>(h, per_stream, nthr, copy, s);
+}
+
+int xg_generate_host_tiles(xg_ensemble_t h, uint64_t per_stream, xg_tile_fn fn, void* ctx,
+                           unsigned threads, xg_stream_t stream) {
+    if (!h || !fn) return XG_EINVAL;
+    uint64_t total;
+    if (mul_overflows(per_stream, h->num_streams, &total)) return XG_EINVAL;
+    if (per_stream == 0) return XG_OK;
+    DeviceGuard dg(h->device);
+    if (!dg.ok) return XG_ECUDA;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int rc = settle_next(h, s);
+    if (rc) return rc;
+    const unsigned nthr = threads ? std::min(threads, 256u)
+                                  : std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    auto call = [fn, ctx](uint64_t g0, uint64_t kb, uint64_t cnt, uint64_t m, const auto* hs, unsigned id,
+                          unsigned nt) {
+        fn(ctx, g0, kb, cnt, m, hs, static_cast<unsigned>(sizeof(*hs)), id, nt);
+    };
+    if (h->params.w <= 32) return generate_tiles_impl<kU32, uint32_t>(h, per_stream, nthr, call, s);
+    return generate_tiles_impl<kWide, uint64_t>(h, per_stream, nthr, call, s);
 }
 
 int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,

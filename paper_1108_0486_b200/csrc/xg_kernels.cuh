@@ -146,28 +146,19 @@ __device__ __forceinline__ double raw_pair_to_f64(uint32_t lo, uint32_t hi) {
 // (w[2m], w[2m+1]) of the stream -- in the pair-lane
 // kernel (xg_pairs.cuh) exactly the pair a lane holds.  Each word, read as a
 // signed 32-bit integer, is a coordinate in [-2^31, 2^31); the sample hits
-// the disc iff x^2 + y^2 < 2^62 (exact).  Returns 1 for a hit.
-// x^2 + y^2 - 2^62 lies in [-2^62, 2^62], so its sign is bit 63 of
-// x^2 + y^2 + 0xC000000000000000 (mod 2^64): per sample ptxas emits
-// IMAD.WIDE (x^2 + C, the constant folded into the 64-bit addend) + IMAD.HI
-// (high word of y^2 + that) + a LEA.HI that accumulates the sign bit -- no
-// shifts, no selects, no separate compare.  C is offset by threadIdx.y (0 in
-// these 1-D launches) so ptxas keeps it in a per-lane register pair, which
-// IMAD.WIDE can take as its addend (a uniform constant costs an extra 64-bit
-// IADD3 pair on the ALU pipe instead).
+// the disc iff x^2 + y^2 < 2^62 (exact).  Returns 1 for a hit.  Per sample
+// ptxas emits IMAD.WIDE + IMAD.HI (the high word of x^2 + y^2), one VIADD and
+// a LEA.HI that accumulates the sign bit -- no shifts, no selects.  (Folding
+// the -2^62 into IMAD.WIDE's 64-bit addend saves the VIADD -- 245 instead of
+// 253 instructions per 512 words -- but an IMAD.WIDE with a register-pair
+// addend co-issues worse: 1.707e12 against 1.784e12 RN/s, measured A/B in
+// profiles/s2b_mc_ab.txt.)
 __device__ __forceinline__ uint32_t mc_hit(uint32_t a, uint32_t b) {
     const int64_t x = static_cast<int32_t>(a), y = static_cast<int32_t>(b);
-    const uint64_t C = 0xC000000000000000ull + threadIdx.y;
-    const uint64_t q = static_cast<uint64_t>(x * x) + C + static_cast<uint64_t>(y * y);
-    return static_cast<uint32_t>(q >> 32);  // hit iff bit 31 is set
-}
-
-// hits += the sign bit of mc_hit's word; kept as its own shift-add so ptxas
-// fuses it into one LEA.HI per sample (left alone it sums two samples with
-// two SHF + one IADD3).
-__device__ __forceinline__ void mc_count(uint32_t& hits, uint32_t hi) {
-    asm volatile("{\n\t.reg .u32 t;\n\tshr.u32 t, %1, 31;\n\tadd.u32 %0, %0, t;\n\t}"
-                 : "+r"(hits) : "r"(hi));
+    // x^2 + y^2 <= 2^63 fits in uint64; hit iff its high word is < 2^30,
+    // i.e. iff (high word - 2^30), in [-2^30, 2^30], has its sign bit set.
+    const uint64_t q = static_cast<uint64_t>(x * x) + static_cast<uint64_t>(y * y);
+    return (static_cast<uint32_t>(q >> 32) - 0x40000000u) >> 31;
 }
 
 // SplitMix64 draw k (1-based) from `seed` in closed form: the chain of
@@ -285,8 +276,8 @@ __device__ __forceinline__ void body4(uint32_t (&R)[4], const P& p, const Lane& 
             if (!TAIL || lane + 32u < limit) __stcs(static_cast<double*>(o) + 32, raw_pair_to_f64(pb.x, pb.y));
         } else {
             // limit (TAIL) = wanted 64-word blocks of this body (0 or 1): pairs 0..31
-            if (!TAIL || limit > 0u) mc_count(hits, mc_hit(pa.x, pa.y));
-            if (!TAIL) mc_count(hits, mc_hit(pb.x, pb.y));
+            if (!TAIL || limit > 0u) hits += mc_hit(pa.x, pa.y);
+            if (!TAIL) hits += mc_hit(pb.x, pb.y);
         }
     }
 }

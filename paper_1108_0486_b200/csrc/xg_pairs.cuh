@@ -153,6 +153,42 @@ __device__ __forceinline__ void rank_pair(uint2 v, unsigned& rank_a, unsigned& r
     rank_b = nb;
 }
 
+// matrix_rank_test's counting loop over a word buffer (any source: file
+// words, the Weyl-ablated stream, sets the fused kRank mode does not take):
+// matrix k = words [32k, 32k + 32), row i = word i.  One warp per pair of
+// matrices (grid-stride), rank_pair as in the fused mode; bins (rank 32, 31,
+// <= 30) added to counts[0..2].
+__global__ void __launch_bounds__(256)
+rank_words_kernel(const uint32_t* __restrict__ words, uint64_t matrices,
+                  unsigned long long* __restrict__ counts) {
+    const unsigned lane = threadIdx.x & 31u;
+    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+    uint32_t full = 0, minus1 = 0, rest = 0;
+    for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+         2 * j < matrices; j += warps) {
+        const bool second = 2 * j + 1 < matrices;
+        const uint64_t w = 64 * j + 2 * lane;
+        uint2 v;
+        v.x = (lane < 16u || second) ? words[w] : 0u;
+        v.y = (lane < 16u || second) ? words[w + 1] : 0u;
+        unsigned ra, rb;
+        rank_pair(v, ra, rb);
+        full += ra == 32u;
+        minus1 += ra == 31u;
+        rest += ra < 31u;
+        if (second) {
+            full += rb == 32u;
+            minus1 += rb == 31u;
+            rest += rb < 31u;
+        }
+    }
+    if (lane == 0) {
+        if (full) atomicAdd(counts, static_cast<unsigned long long>(full));
+        if (minus1) atomicAdd(counts + 1, static_cast<unsigned long long>(minus1));
+        if (rest) atomicAdd(counts + 2, static_cast<unsigned long long>(rest));
+    }
+}
+
 // Per-lane accumulators: MC hits, or the rank-test bins.
 struct RankAcc {
     uint32_t full = 0, minus1 = 0, rest = 0;  // rank 32, 31, <= 30
@@ -177,7 +213,7 @@ __device__ __forceinline__ void pair_emit(uint2 v, void* o, int j, unsigned limi
     } else if constexpr (MODE == kF64) {
         if (!TAIL || 32u * j + lane < limit) __stcs(static_cast<double*>(o) + 32 * j, raw_pair_to_f64(v.x, v.y));
     } else if constexpr (MODE == kMC) {
-        if (!TAIL || 32u * j + lane < limit) mc_count(hits, mc_hit(v.x, v.y));
+        if (!TAIL || 32u * j + lane < limit) hits += mc_hit(v.x, v.y);
     } else if constexpr (MODE == kRank) {
         // this double step holds matrices 2j and 2j+1 of the body
         unsigned ra, rb;

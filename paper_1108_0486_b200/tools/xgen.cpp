@@ -8,14 +8,18 @@
 //
 // Generators: every xorgens id of the reference registry
 // (proj/src/registry.cpp:27-42): xorgensgp32, xorgens-raw (linear part only),
-// tiny:r2w8, tiny:r2w16, tiny:r4w16 and their tiny-raw: forms.  The
-// statistical battery (`test`) and the CPU baselines (xorwow, mt19937) are not
-// part of the GPU backend: they exit 67 / 64.
+// tiny:r2w8, tiny:r2w16, tiny:r4w16 and their tiny-raw: forms.  `test` (the
+// statistical battery, xgen.cpp:132-191) runs the GPU battery of the Python
+// host layer over the same library: this binary execs
+// `python3 -m paper_1108_0486_b200.xgen_test` with the subcommand's arguments
+// (exit codes 0 / 2 suspect / 3 fail as the reference).  The CPU baselines
+// (xorwow, mt19937) are not part of the GPU backend: 64.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cinttypes>
 #include <cmath>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -23,6 +27,8 @@
 #include <iostream>
 #include <string>
 #include <vector>
+
+#include <unistd.h>
 
 #include "xg_gpu.h"
 
@@ -328,10 +334,34 @@ int cmd_params(const Args& a) {
 
 }  // namespace
 
+// `xgen test ...`: exec the GPU battery CLI (paper_1108_0486_b200/xgen_test.py)
+// with the repository root (three levels above this binary) on PYTHONPATH.
+int exec_test(int argc, char** argv) {
+    char self[PATH_MAX];
+    const ssize_t n = readlink("/proc/self/exe", self, sizeof self - 1);
+    if (n <= 0) return fail("cannot locate the xgen binary", exit_io);
+    self[n] = 0;
+    std::string root(self);
+    for (int up = 0; up < 3; ++up) root = root.substr(0, root.find_last_of('/'));
+    const char* old = getenv("PYTHONPATH");
+    const std::string pp = old && *old ? root + ":" + old : root;
+    setenv("PYTHONPATH", pp.c_str(), 1);
+    std::vector<char*> args;
+    static char py[] = "python3", m[] = "-m", mod[] = "paper_1108_0486_b200.xgen_test";
+    args.push_back(py);
+    args.push_back(m);
+    args.push_back(mod);
+    for (int i = 2; i < argc; ++i) args.push_back(argv[i]);
+    args.push_back(nullptr);
+    execvp(py, args.data());
+    return fail("cannot run python3 for the battery", exit_io);
+}
+
 int main(int argc, char** argv) {
+    if (argc >= 2 && std::strcmp(argv[1], "test") == 0) return exec_test(argc, argv);
     Args a;
     if (int rc = parse(argc, argv, &a)) {
-        std::cerr << "usage: xgen gen|bench|params [options]  (GPU backend)\n";
+        std::cerr << "usage: xgen gen|test|bench|params [options]  (GPU backend)\n";
         return rc;
     }
     if (a.cmd == "gen") return cmd_gen(a);
@@ -340,6 +370,5 @@ int main(int argc, char** argv) {
         if (a.positional.empty()) return fail("params needs a generator id", exit_bad_args);
         return cmd_params(a);
     }
-    if (a.cmd == "test") return fail("the statistical battery is not part of the GPU backend", exit_bad_args);
     return fail(("unknown subcommand: " + a.cmd).c_str(), exit_bad_args);
 }

@@ -146,3 +146,112 @@ def test_gen_tiny_generators(oracle, gid, ps, weyl, tmp_path):
     assert rc == 0
     dt = {8: "<u1", 16: "<u2"}[ps[6]]
     assert np.array_equal(np.fromfile(path, dtype=dt).astype(np.uint64), want)
+
+
+# ---- `xgen test` (proj/tools/xgen.cpp:132-191; exit-by-verdict goldens
+# proj/tests/test_cli.cpp:117-176) -------------------------------------------
+
+QUICK_CFG = """# the reference's BatteryConfig::quick (battery.cpp:11-20) as a config file
+monobit.bits = 1000000
+runs.bits = 1000000
+matrix_rank.matrices = 1000
+linear_complexity.block_length = 500
+linear_complexity.blocks = 200
+birthday.rounds = 8
+"""
+
+
+def test_test_exit_codes_before_device_work(tmp_path):
+    """Argument / config / file errors exit as the reference's xgen does,
+    before any device work (CPU)."""
+    cfg = tmp_path / "q.cfg"
+    cfg.write_text(QUICK_CFG)
+    bad = tmp_path / "bad.cfg"
+    bad.write_text("monobit.bits 12\n")
+    unknown = tmp_path / "unknown.cfg"
+    unknown.write_text("nosuch.key = 1\n")
+    assert run("test", "-g", "nosuchgen")[0] == 64
+    assert run("test", "--config", str(tmp_path / "missing.cfg"))[0] == 66
+    assert run("test", "--config", str(bad))[0] == 67
+    assert run("test", "--config", str(unknown))[0] == 67
+    assert run("test", "--input", str(tmp_path / "missing.bin"), "--config", str(cfg))[0] == 66
+    assert run("test", "--bogus-flag")[0] == 67
+
+
+def _ref_report(words, quick=True):
+    from oracle import Battery
+
+    try:
+        b = Battery()
+    except FileNotFoundError as e:  # pragma: no cover
+        pytest.skip(str(e))
+    verdict, js = b.run(words, quick=quick, label="ref")
+    import json
+
+    return verdict, json.loads(js)
+
+
+def _same_tests(mine, ref):
+    assert mine["overall"] == ref["overall"]
+    assert mine["num_tests"] == ref["num_tests"]
+    for a, b in zip(mine["tests"], ref["tests"]):
+        assert (a["name"], a["n"], a["statistic"], a["p"], a["verdict"]) == \
+               (b["name"], b["n"], b["statistic"], b["p"], b["verdict"]), a["name"]
+
+
+@gpu
+def test_test_generator_report_equals_reference(oracle, tmp_path):
+    """`xgen test -g xorgensgp32` (GPU battery) reports exactly what the
+    reference's run_battery reports over the same stream; exit 0 on pass."""
+    import json
+
+    cfg = tmp_path / "q.cfg"
+    cfg.write_text(QUICK_CFG)
+    out = tmp_path / "rep.json"
+    rc, _ = run("test", "-g", "xorgensgp32", "--seed", "3", "--config", str(cfg), "-o", str(out))
+    mine = json.loads(out.read_text())
+    words = oracle.stream(3, 200000)
+    verdict, ref = _ref_report(words)
+    _same_tests(mine, ref)
+    assert mine["generator"] == "xorgensgp32" and mine["seed"] == 3
+    assert rc == {"pass": 0, "suspect": 2, "fail": 3}.get(ref["overall"], 0)
+
+
+@gpu
+def test_test_raw_stream_fails_linear_complexity(golden, tmp_path):
+    """The Weyl-ablated stream (xorgens-raw) is the battery's negative
+    control: its linear complexity saturates at 4096 bits, so blocks of 5000
+    bits fail the test -- exit 3, as the reference reports it over the same
+    words."""
+    import json
+
+    cfg = tmp_path / "lc.cfg"
+    cfg.write_text("monobit.enabled = false\nruns.enabled = false\nmatrix_rank.enabled = false\n"
+                   "birthday.enabled = false\nlinear_complexity.block_length = 5000\n"
+                   "linear_complexity.blocks = 40\n")
+    rc, out = run("test", "-g", "xorgens-raw", "--seed", "1", "--config", str(cfg))
+    rep = json.loads(out)
+    assert rc == 3 and rep["overall"] == "fail"
+    assert rep["tests"][0]["name"] == "linear_complexity" and rep["tests"][0]["verdict"] == "fail"
+
+
+@gpu
+def test_test_input_file_equals_reference(oracle, tmp_path):
+    """`xgen test --input words.bin`: raw-le words consumed in the
+    reference's order (FileWordSource); report equal to the reference's over
+    the same words; a file too short for the configuration exits 66."""
+    import json
+
+    cfg = tmp_path / "q.cfg"
+    cfg.write_text(QUICK_CFG)
+    words = oracle.stream(77, 140000)
+    path = tmp_path / "w.bin"
+    words.astype("<u4").tofile(path)
+    rc, out = run("test", "--input", str(path), "--config", str(cfg))
+    mine = json.loads(out)
+    _, ref = _ref_report(words)
+    _same_tests(mine, ref)
+    assert mine["generator"] == "file:" + str(path) and mine["seed"] == 0
+    short = tmp_path / "s.bin"
+    words[:50000].astype("<u4").tofile(short)
+    assert run("test", "--input", str(short), "--config", str(cfg))[0] == 66

@@ -82,19 +82,53 @@ def test_ones_runs_and_birthday_kernels_direct():
         assert int(out.item()) == dup, (nd, t)
 
 
-def test_battery_rejects_rank_unsupported_sets_up_front():
-    """A w = 32 set the fused rank test cannot take (r - s >= 64, J = 2) is
-    refused before any test consumes the stream; without the rank test the
-    rest of the battery runs."""
+def test_battery_runs_every_w32_set_and_the_raw_stream():
+    """A w = 32 set the fused rank test cannot take (r - s >= 64, J = 2) and
+    the Weyl-ablated stream run the whole battery: the matrix-rank test over
+    stored words (xg_rank_words), the linear complexity test over stored raw
+    words (xg_lc_words).  Reports equal the reference's run_battery over the
+    same words."""
     from paper_1108_0486_b200.battery import BatteryConfig, run_battery_gpu
 
-    j2 = xg.GeneratorParams(128, 33, 11, 7, 9, 19, 32, 0x6A09E667 | 1, 11)
-    with pytest.raises(xg.UnsupportedParamsError):
-        run_battery_gpu(j2, 1, BatteryConfig.quick())
+    b = _battery()
     cfg = BatteryConfig.quick()
-    cfg.run_matrix_rank = False
-    rep = run_battery_gpu(j2, 1, cfg)
-    assert rep["num_tests"] == 4
+    j2 = xg.GeneratorParams(128, 33, 11, 7, 9, 19, 32, 0x6A09E667 | 1, 11)
+    for p, raw in ((j2, False), (xg.xorgensgp32_params(), True)):
+        rep = run_battery_gpu(p, 5, cfg, raw=raw)
+        e = xg.BlockEnsemble(p, 5, 1, xg.lane_bound(p))
+        n = _words_consumed(cfg)
+        words = (e.fill_raw_u32(n) if raw else e.fill_u32(n)).cpu().numpy()[0]
+        verdict, js = b.run(words, quick=True, label="x")
+        ref = json.loads(js)
+        assert rep["overall"] == ref["overall"] == verdict
+        for mine, theirs in zip(rep["tests"], ref["tests"]):
+            assert (mine["statistic"], mine["p"], mine["verdict"]) == \
+                   (theirs["statistic"], theirs["p"], theirs["verdict"]), (raw, mine["name"])
+
+
+def test_rank_and_lc_over_word_buffers():
+    """xg_rank_words / xg_lc_words against the reference's own gf2_rank and
+    berlekamp_massey on random words (odd matrix counts, blocks straddling
+    words, K above the register path's 1023)."""
+    from oracle import Battery
+
+    b = _battery()
+    rng = np.random.default_rng(11)
+    w = rng.integers(0, 2**32, size=32 * 41, dtype=np.uint64).astype(np.uint32)
+    dev = torch.from_numpy(w.view(np.int32)).cuda()
+    for m in (1, 2, 7, 41):
+        out = torch.zeros(3, dtype=torch.int64, device="cuda")
+        assert xg._lib.lib.xg_rank_words(dev.data_ptr(), m, out.data_ptr(), None) == 0
+        ranks = [b.gf2_rank32(w[32 * k:32 * k + 32]) for k in range(m)]
+        want = [sum(r == 32 for r in ranks), sum(r == 31 for r in ranks), sum(r < 31 for r in ranks)]
+        assert out.tolist() == want, m
+    for k, nb in ((128, 9), (1000, 3), (1023, 2), (2000, 2)):
+        hist = torch.zeros(k + 1, dtype=torch.int64, device="cuda")
+        assert xg._lib.lib.xg_lc_words(dev.data_ptr(), dev.numel(), k, nb, hist.data_ptr(), None) == 0
+        assert np.array_equal(hist.cpu().numpy(), b.lc_histogram(w, k, nb).astype(np.int64)), k
+    hist = torch.zeros(2001, dtype=torch.int64, device="cuda")
+    assert xg._lib.lib.xg_lc_words(dev.data_ptr(), 10, 2000, 1, hist.data_ptr(), None) == \
+        xg._lib.XG_EINVAL
 
 
 def test_handle_less_calls_reject_host_pointers():

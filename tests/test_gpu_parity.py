@@ -809,3 +809,37 @@ def test_hostbench_runs_reference_methods_over_dropin():
     d = json.loads(r.stdout)
     assert d["measure_throughput"]["rn_per_s"]["mean"] > 0
     assert d["measure_ensemble_throughput"]["rn_per_s"]["mean"] > 0
+
+
+def test_generate_host_tiles_callback_order_and_content(oracle):
+    """xg_generate_host_tiles (what xg::gpu::BlockEnsemble::generate uses):
+    every (stream, word) range arrives exactly once, a stream's tiles in word
+    order, with the stream's words; elements of 4 bytes for w = 32."""
+    import ctypes
+
+    L = xg._lib.lib
+    P, per = 3, (1 << 26) + 99   # longer than one staging slot: several tiles per stream
+    e = xg.BlockEnsemble(GP32, 8, P, 63)
+    seen = {g: [] for g in range(P)}
+    ref = oracle.ensemble(8, P)
+    want = ref.fill_u32(per)
+    bad = []
+    FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                          ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint)
+
+    def cb(ctx, s0, w0, ns, nw, tile, eb, part, parts):
+        if part != 0:
+            return
+        if eb != 4:
+            bad.append(eb)
+        t = np.ctypeslib.as_array((ctypes.c_uint32 * (ns * nw)).from_address(tile)).reshape(ns, nw)
+        for i in range(ns):
+            seen[s0 + i].append(w0)
+            if not np.array_equal(t[i], want[s0 + i, w0:w0 + nw]):
+                bad.append((s0 + i, w0))
+
+    f = FN(cb)
+    assert L.xg_generate_host_tiles(e.handle, per, f, None, 2, None) == 0
+    assert not bad
+    for g in range(P):
+        assert seen[g] == sorted(seen[g]) and seen[g][0] == 0 and len(seen[g]) > 1
