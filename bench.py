@@ -156,6 +156,15 @@ def _free_port() -> int:
     return port
 
 
+def _nccl_debug_env(env) -> None:
+    """NCCL INFO logging (communicator init lines: rank, nRanks, NVLS/P2P
+    transport) so the ranks of every N-GPU run are visible in the log; a
+    quieter preset (VERSION / WARN / unset) is raised to INFO."""
+    if env.get("NCCL_DEBUG", "").upper() in ("", "VERSION", "WARN"):
+        env["NCCL_DEBUG"] = "INFO"
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT,ENV")
+
+
 def self_launch(args) -> int:
     """--gpus N > 1 outside torchrun: re-run this script under
     torch.distributed.run with N ranks on this node (the driver's own
@@ -164,7 +173,7 @@ def self_launch(args) -> int:
            f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
            f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
     env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "INFO")
+    _nccl_debug_env(env)
     env.setdefault("OMP_NUM_THREADS", "1")
     return subprocess.call(cmd, env=env)
 
@@ -185,7 +194,7 @@ def dist_setup(dry: bool = False):
         torch.cuda.set_device(local)
     if world > 1 and not dist.is_initialized():
         if backend == "nccl":
-            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            _nccl_debug_env(os.environ)
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         else:
             dist.init_process_group(backend)

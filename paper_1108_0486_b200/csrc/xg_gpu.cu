@@ -195,7 +195,7 @@ int launch_pair(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count, 
     // busiest SM carries at most one stream more than the average, and small
     // ensembles use every SM (8-stream CTAs put 64 streams on 8 SMs: 1.32e11
     // against 0.95e11 RN/s; 4096 streams: 1.57e12 against 1.44e12;
-    // profiles/README.md, r1p).  Larger ensembles: below.
+    // profiles/ab_r1/README_round1.md, r1p).  Larger ensembles: below.
     const uint64_t sms = static_cast<uint64_t>(std::max(1, h->sms));
     // u32 / raw fills of large ensembles: 4-stream CTAs, at most
     // kFillCtasPerSm = 4 of them resident per SM (16 write streams per SM
@@ -204,7 +204,7 @@ int launch_pair(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count, 
     // saturate an SM's ALU pipe), and fewer concurrent write streams, started
     // in small staggered CTA waves, write faster: 1.596e12 against 1.53e12
     // RN/s under the power cap, 1.737e12 against 1.72e12 in bursts (r1u,
-    // r1zg in profiles/README.md).  The conversions gain nothing from the cap
+    // r1zg in profiles/ab_r1/README_round1.md).  The conversions gain nothing from the cap
     // and run full (8-stream CTAs, 64 streams per SM).
     constexpr bool kCapped = MODE == kU32 || MODE == kRaw;
     const bool large = g_count > 32 * sms;

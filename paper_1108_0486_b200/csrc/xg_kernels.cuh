@@ -26,7 +26,7 @@
 // block-major output (out[g*per_stream + k], parallel.cpp:97-135), stored with
 // one coalesced evict-first STG.32 per step.  (Round-1 placement experiments --
 // IMAD.HI right shifts, SHF.L left shifts, bulk-copy stores -- were measured
-// slower and removed; profiles/README.md keeps the A/B table.)
+// slower and removed; profiles/ab_r1/README_round1.md keeps the A/B table.)
 #pragma once
 
 #include <cstdint>
@@ -129,7 +129,7 @@ __device__ __forceinline__ uint32_t weyl_out(uint32_t w, uint32_t v, const P& p)
 // form compiles to I2F.U32.RM (XU pipe) instead of I2FP (ALU pipe), which is
 // the busiest pipe of this kernel.  (Reading the half-word and the byte
 // straight out of the register with I2F.U16 R.H1 + I2F.U8 R.B1 and one FFMA
-// saves the shift but is 1 % slower: profiles/README.md.)
+// saves the shift but is 1 % slower: profiles/ab_r1/README_round1.md, r1za.)
 __device__ __forceinline__ float u32_to_f32(uint32_t u) {
     return __uint2float_rd(u >> 8) * 0x1p-24f;
 }

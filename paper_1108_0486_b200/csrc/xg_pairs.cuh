@@ -75,7 +75,7 @@ __device__ __forceinline__ uint2 double_step(const uint2 A, const uint2 B, const
         // does not depend on the previous step, so one IMAD sits on the
         // step-to-step chain (MC +3 %, one stream +16 %); GIVE 1:
         // B.y + is31 * (A.y - B.y) (IADD + IMAD, both on the chain), 2 % faster
-        // for f32 (profiles/README.md, r1w/r1z).
+        // for f32 (profiles/ab_r1/README_round1.md, r1w/r1z).
         uint32_t give;
         if constexpr (GIVE == 0)
             asm("{\n\t.reg .u32 t;\n\tmul.lo.u32 t, %1, %3;\n\tmad.lo.u32 %0, %2, %4, t;\n\t}"
@@ -110,7 +110,7 @@ __device__ __forceinline__ uint32_t weyl_mix(uint32_t w, uint32_t v, const P& p)
 // the number of columns with a pivot.  Same rank as the row-by-row
 // elimination of proj/src/stattests/gf2.cpp:8-33.  (Getting the pivot value
 // with redux.sync.max instead of ballot + bfind + shuffle is 6 % slower;
-// profiles/README.md, r1zm.)
+// profiles/ab_r1/README_round1.md, r1zm.)
 __device__ __forceinline__ void rank_pair(uint2 v, unsigned& rank_a, unsigned& rank_b) {
     const unsigned lane = threadIdx.x & 31u;
     const unsigned half = lane >> 1;

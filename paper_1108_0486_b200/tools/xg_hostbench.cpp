@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <functional>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "xg/gpu.hpp"
@@ -124,13 +125,43 @@ int main(int argc, char** argv) {
     };
     const Report ens_rep = run_trials(trials, etrial);
 
+    // The host-side ceiling of that result type: the same allocation
+    // (blocks x reserve(per_block)) and the same u32 -> uint64 appends from a
+    // resident 256 MiB u32 source, on the same threads, with no GPU, no PCIe
+    // and no generator -- what building vector<vector<uint64_t>> costs on
+    // this host by itself.
+    const unsigned nthr = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<std::uint32_t> srcbuf(std::min<std::uint64_t>(total, 1ull << 26), 0x9e3779b9u);
+    auto htrial = [&]() -> double {
+        const auto start = std::chrono::steady_clock::now();
+        std::vector<std::vector<std::uint64_t>> out(blocks);
+        std::vector<std::thread> pool;
+        for (unsigned id = 0; id < nthr; ++id)
+            pool.emplace_back([&, id] {
+                for (unsigned i = id; i < blocks; i += nthr) {
+                    out[i].reserve(per_block);
+                    const std::uint32_t* src =
+                        srcbuf.data() + (static_cast<std::uint64_t>(i) * per_block) % (srcbuf.size() - per_block + 1);
+                    out[i].insert(out[i].end(), src, src + per_block);
+                }
+            });
+        for (auto& th : pool) th.join();
+        const std::chrono::duration<double> elapsed = std::chrono::steady_clock::now() - start;
+        for (const auto& b : out) sink ^= b.back();
+        return static_cast<double>(total) / elapsed.count();
+    };
+    const Report host_rep = run_trials(trials, htrial);
+
     std::printf("{\"measure_throughput\": {\"api\": \"xg::gpu::XorgensSource<WordSource>::next "
                 "(virtual, next_word inline from pinned refills)\", \"count\": %llu, \"trials\": %u, "
                 "\"rn_per_s\": %s, \"wall_rn_per_s\": %.6g}, "
                 "\"measure_ensemble_throughput\": {\"api\": \"xg::gpu::BlockEnsemble::generate -> "
                 "vector<vector<uint64_t>>\", \"blocks\": %u, \"per_block\": %zu, \"trials\": %u, "
-                "\"rn_per_s\": %s, \"bytes_per_word_host\": 8}, \"sink\": %llu}\n",
+                "\"rn_per_s\": %s, \"bytes_per_word_host\": 8}, "
+                "\"host_result_ceiling\": {\"what\": \"the same vector<vector<uint64_t>> built from a "
+                "resident u32 buffer on %u threads, no GPU\", \"rn_per_s\": %s}, \"sink\": %llu}\n",
                 static_cast<unsigned long long>(count), trials, json(src_rep).c_str(), src_wall, blocks,
-                per_block, trials, json(ens_rep).c_str(), static_cast<unsigned long long>(sink));
+                per_block, trials, json(ens_rep).c_str(), nthr, json(host_rep).c_str(),
+                static_cast<unsigned long long>(sink));
     return 0;
 }
