@@ -728,26 +728,24 @@ def run_reference_arm(args):
 # our arm
 # --------------------------------------------------------------------------
 
-def sustained(fn, stream, seconds: float, world: int, local: int, words_per_step: int) -> dict:
+def sustained(fn, stream, seconds: float, world: int, local: int, words_per_step: int,
+              ms_per_step: float) -> dict:
     """The same step back to back for ~`seconds` (power-capped steady state),
-    timed with CUDA events; clocks sampled throughout."""
+    timed with CUDA events, max over ranks; clocks sampled throughout.  The
+    step count comes from the burst timing (max over ranks), so every rank
+    runs the same number of steps."""
     import torch
 
-    t0 = time.perf_counter()
-    steps = 0
+    steps = max(100, int(seconds * 1e3 / max(ms_per_step, 1e-3)) // 100 * 100)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        while True:
-            for _ in range(100):
-                fn()
-            steps += 100
-            if time.perf_counter() - t0 > seconds:
-                break
-            if steps % 1000 == 0:
-                torch.cuda.synchronize()
+        for i in range(steps):
+            fn()
+            if i % 1000 == 999:
+                torch.cuda.synchronize()  # bound the launch queue
         e1.record(stream)
         torch.cuda.synchronize()
         barrier(world)
@@ -863,7 +861,8 @@ def main():
         except OSError:
             pass
     if wl == "fill_u32" and args.sustained_s > 0:
-        result["sustained"] = sustained(fn, stream, args.sustained_s, world, local, job_words)
+        result["sustained"] = sustained(fn, stream, args.sustained_s, world, local, job_words,
+                                        result["ms_per_step"])
     # e2e through the public host API (generate into pinned host memory)
     if not args.no_e2e and wl == "fill_u32":
         host = torch.empty((count, per), dtype=torch.uint32, pin_memory=True)
