@@ -653,26 +653,23 @@ def cpu_baseline_for(wl: str) -> dict:
         except Exception:  # noqa: BLE001
             pass
         return cb
-    if wl in ("fill_f32", "fill_f64"):
-        # The reference has no conversions: the C restatement's words + the
-        # same conversion, all threads (kind "port").
-        streams, per = 4096, 1 << 16
-        o.threads = threads
-        e = o.ensemble(1, streams)
-        f = e.fill_f32 if wl == "fill_f32" else e.fill_f64
-        f(1024)
-        t = time.perf_counter()
-        f(per)
-        dt = time.perf_counter() - t
-        words = streams * per * (2 if wl == "fill_f64" else 1)
-        return {"value": words / dt, "unit": "RN/s", "cores": threads, "kind": "port",
-                "values_per_s": streams * per / dt, "cpu_model": cpu_model(),
-                "sample": f"oracle/xg_oracle.c ensemble {streams} streams x {per} values "
-                          f"({wl[5:]} conversion of DESIGN.md section 3; the reference has none), "
-                          f"{threads} threads"}
     ref = Reference()
+    if wl in ("fill_f32", "fill_f64"):
+        # The reference has no conversions: its XorgensState words + the same
+        # conversion, per-stream loops on all threads.
+        f64 = wl == "fill_f64"
+        streams, per = 8192, 1 << 16
+        t = time.perf_counter()
+        _threaded(lambda f, c: ref.streams_convert(p, 1, f, c, per, f64), 0, streams, 64)
+        dt = time.perf_counter() - t
+        words = streams * per * (2 if f64 else 1)
+        return {"value": words / dt, "unit": "RN/s", "cores": threads, "kind": "reference",
+                "values_per_s": streams * per / dt, "cpu_model": cpu_model(),
+                "sample": f"{streams} per-stream XorgensState loops (proj/src/xorgens.cpp) x {per} "
+                          f"{wl[5:]} values (conversion of DESIGN.md section 3 on reference words; the "
+                          f"reference has none), {threads} threads"}
     if wl == "fill_2p34":
-        streams, per = 2048, 1 << 16
+        streams, per = 8192, 1 << 16
         t = time.perf_counter()
         _threaded(lambda f, c: ref.streams_xor(p, 1, f, c, per), 0, streams, 64)
         dt = time.perf_counter() - t
@@ -682,7 +679,7 @@ def cpu_baseline_for(wl: str) -> dict:
                           f"2^34 config's streams x {per} words, {threads} threads "
                           "(BASELINE.md: generate() would need 128 GiB)"}
     if wl == "mc_pi":
-        streams, spp = 2048, 1 << 15
+        streams, spp = 8192, 1 << 15
         t = time.perf_counter()
         parts = _threaded(lambda f, c: ref.stream_digests(p, 1, f, c, 0, 0, spp)["mc"], 0, streams, 64)
         dt = time.perf_counter() - t

@@ -305,6 +305,7 @@ class Reference:
         L.xgref_stream_digests.argtypes = [arr, _u64, ctypes.c_uint, _u64, _u64, _u64, _u64, _u64,
                                            _u64] + [_vp] * 10
         L.xgref_streams_xor.argtypes = [arr, _u64, ctypes.c_uint, _u64, _u64, _u64, _u64, _vp]
+        L.xgref_streams_convert.argtypes = [arr, _u64, ctypes.c_uint, _u64, _u64, _u64, _u64, _int, _vp]
         L.xgref_serial_rate.restype = ctypes.c_double
         L.xgref_serial_rate.argtypes = [_u64, _u64, ctypes.c_uint, ctypes.POINTER(_u64)]
 
@@ -419,6 +420,17 @@ class Reference:
         out = np.zeros(count, dtype=np.uint32)
         rc = self.lib.xgref_streams_xor(self._arr(p), p.omega, p.gamma, base_seed & (2**64 - 1),
                                         first, count, n, _ptr(out))
+        if rc:
+            raise ValueError("reference rejected the parameters")
+        return out
+
+    def streams_convert(self, p, base_seed: int, first: int, count: int, n: int, f64: bool) -> np.ndarray:
+        """n f32 (or f64) values of each of streams [first, first + count)
+        from XorgensState loops (xgref_streams_convert); per-stream xor of
+        the value bits.  Releases the GIL."""
+        out = np.zeros(count, dtype=np.uint64)
+        rc = self.lib.xgref_streams_convert(self._arr(p), p.omega, p.gamma, base_seed & (2**64 - 1),
+                                            first, count, n, int(f64), _ptr(out))
         if rc:
             raise ValueError("reference rejected the parameters")
         return out

@@ -273,6 +273,41 @@ int xgref_streams_xor(const unsigned* rsabcdw, std::uint64_t omega, unsigned gam
     }
 }
 
+// The CPU equivalent of the fused conversion fills for the bench baseline:
+// streams [first, first + count) as XorgensState loops, n values each,
+// mode 0 = f32 (w >> 8) * 2^-24 of one word, 1 = f64 (u64 >> 11) * 2^-53 of
+// the word pair (lo first) -- the DESIGN.md section 3 conventions applied to
+// reference words; the value bits fold into a per-stream xor sink.
+int xgref_streams_convert(const unsigned* rsabcdw, std::uint64_t omega, unsigned gamma,
+                          std::uint64_t base_seed, std::uint64_t first, std::uint64_t count,
+                          std::uint64_t n, int mode, std::uint64_t* sink_out) {
+    try {
+        const auto p = to_params(rsabcdw, omega, gamma);
+        for (std::uint64_t i = 0; i < count; ++i) {
+            xg::XorgensState st(p, base_seed + first + i);
+            std::uint64_t sink = 0;
+            for (std::uint64_t k = 0; k < n; ++k) {
+                if (mode == 0) {
+                    const float f = static_cast<float>(static_cast<std::uint32_t>(st.next_word()) >> 8) * 0x1p-24f;
+                    std::uint32_t b;
+                    std::memcpy(&b, &f, 4);
+                    sink ^= b;
+                } else {
+                    const std::uint64_t lo = st.next_word(), hi = st.next_word();
+                    const double d = static_cast<double>((lo | (hi << 32)) >> 11) * 0x1p-53;
+                    std::uint64_t b;
+                    std::memcpy(&b, &d, 8);
+                    sink ^= b;
+                }
+            }
+            sink_out[i] = sink;
+        }
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 // Serial next_word throughput, the measure_throughput method
 // (proj/src/bench.cpp:67-93): best chunk rate on thread CPU time.
 double xgref_serial_rate(std::uint64_t seed, std::uint64_t count, unsigned chunks,
