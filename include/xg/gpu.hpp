@@ -194,9 +194,8 @@ protected:
     // next_word cache (XorgensState): a view of pinned refill words
     // (xg_next_view); unread ones are returned before any other call.
     struct NextCache {
-        const void* p = nullptr;
+        const std::uint64_t* p = nullptr;
         std::uint64_t pos = 0, n = 0;
-        unsigned eb = 4;
     };
     mutable NextCache nc_;
     void give_back() const {
@@ -259,8 +258,7 @@ public:
     // Inline on the hot path: one load from the pinned refill slot.
     std::uint64_t next_word() {
         if (nc_.pos == nc_.n) refill();
-        return nc_.eb == 4 ? static_cast<const std::uint32_t*>(nc_.p)[nc_.pos++]
-                           : static_cast<const std::uint64_t*>(nc_.p)[nc_.pos++];
+        return nc_.p[nc_.pos++];
     }
     std::uint64_t next_u64() {
         if (w_ == 64) return next_word();
@@ -274,7 +272,7 @@ private:
     XorgensState() = default;
     void refill() {
         nc_ = NextCache{};
-        check(xg_next_view(h_, &nc_.p, &nc_.n, &nc_.eb));
+        check(xg_next_view(h_, &nc_.p, &nc_.n));
     }
 };
 

@@ -262,12 +262,11 @@ int xg_generate_host_words(xg_ensemble_t h, uint64_t per_stream, uint64_t* host_
 int xg_next_word(xg_ensemble_t h, uint64_t* out);
 /* Zero-copy batch form of next_word (what xg::gpu::XorgensState inlines):
  * *words points at the next *count unserved words of the stream in pinned host
- * memory, elements of *elem_bytes (4: w <= 32, 8: w = 64), valid until the
- * next call on the handle.  The words count as served; words the caller did
- * not use are handed back with xg_next_return(h, unread) before any other
- * call, so the next word / fill / export continues right after the last word
- * used. */
-int xg_next_view(xg_ensemble_t h, const void** words, uint64_t* count, unsigned* elem_bytes);
+ * memory, each in a uint64 as next_word returns it, valid until the next call
+ * on the handle.  The words count as served; words the caller did not use
+ * are handed back with xg_next_return(h, unread) before any other call, so
+ * the next word / fill / export continues right after the last word used. */
+int xg_next_view(xg_ensemble_t h, const uint64_t** words, uint64_t* count);
 int xg_next_return(xg_ensemble_t h, uint64_t unread);
 /* next_word as uint32 (w <= 32). */
 int xg_next_u32(xg_ensemble_t h, uint32_t* out);

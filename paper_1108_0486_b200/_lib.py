@@ -78,7 +78,7 @@ SIGNATURES = {
     "xg_generate_host_rows": (_int, [_vp, _u64, _vp, _vp]),
     "xg_generate_host_tiles": (_int, [_vp, _u64, _vp, _vp, ctypes.c_uint, _vp]),
     "xg_next_word": (_int, [_vp, _P(_u64)]),
-    "xg_next_view": (_int, [_vp, _P(_vp), _P(_u64), _P(ctypes.c_uint)]),
+    "xg_next_view": (_int, [_vp, _P(_vp), _P(_u64)]),
     "xg_next_return": (_int, [_vp, _u64]),
     "xg_next_u32": (_int, [_vp, _P(_u32)]),
     "xg_next_u64": (_int, [_vp, _P(_u64)]),

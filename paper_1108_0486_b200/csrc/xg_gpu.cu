@@ -89,7 +89,6 @@ struct xg_ensemble {
         bool active = false;     // slots hold words not yet given back to the device state
         int cur = 0;             // slot being served
         uint64_t pos = 0;        // words of slot `cur` served
-        unsigned eb = 4;         // element bytes: 4 (w <= 32) or 8 (w = 64)
         void* host[2] = {};      // pinned
         void* dev[2] = {};       // device staging
         void* snap[2] = {};      // generator state before slot i's words
@@ -1180,14 +1179,15 @@ int xg_generate_host_words(xg_ensemble_t h, uint64_t per_stream, uint64_t* host_
 namespace {
 
 // One refill of ring slot i on the ring's stream: save the state, generate
-// kNextBuf words of the (single) stream, copy them to the pinned slot.
+// kNextBuf words of the (single) stream in the reference's uint64 container
+// (so the host's next_word is one load, whatever w), copy them to the pinned
+// slot.
 int ring_refill(xg_ensemble* h, int i) {
     auto& r = h->nr;
     int rc = copy_state(h, r.snap[i], /*to_snapshot=*/true, r.st);
     if (!rc)
-        rc = r.eb == 4 ? launch_fill<kU32>(h, 0, 1, kNextBuf, r.dev[i], nullptr, r.st)
-                       : launch_fill<kWide>(h, 0, 1, kNextBuf, r.dev[i], nullptr, r.st);
-    if (!rc) rc = cuda_rc(cudaMemcpyAsync(r.host[i], r.dev[i], kNextBuf * r.eb, cudaMemcpyDeviceToHost, r.st));
+        rc = launch_fill<kWide>(h, 0, 1, kNextBuf, r.dev[i], nullptr, r.st);
+    if (!rc) rc = cuda_rc(cudaMemcpyAsync(r.host[i], r.dev[i], kNextBuf * sizeof(uint64_t), cudaMemcpyDeviceToHost, r.st));
     if (!rc) rc = cuda_rc(cudaEventRecord(r.ev[i], r.st));
     return rc;
 }
@@ -1203,13 +1203,12 @@ int ring_next(xg_ensemble* h) {
     if (!dg.ok) return XG_ECUDA;
     int rc = XG_OK;
     if (!r.st) {
-        r.eb = h->params.w > 32 ? 8 : 4;
         size_t wb;
         const size_t sb = state_bytes(h, &wb);
         rc = cuda_rc(cudaStreamCreateWithFlags(&r.st, cudaStreamNonBlocking));
         for (int i = 0; i < 2 && !rc; ++i) {
-            rc = cuda_rc(cudaMallocHost(&r.host[i], kNextBuf * r.eb));
-            if (!rc) rc = cuda_rc(cudaMalloc(&r.dev[i], kNextBuf * r.eb));
+            rc = cuda_rc(cudaMallocHost(&r.host[i], kNextBuf * sizeof(uint64_t)));
+            if (!rc) rc = cuda_rc(cudaMalloc(&r.dev[i], kNextBuf * sizeof(uint64_t)));
             if (!rc) rc = cuda_rc(cudaMalloc(&r.snap[i], sb));
             if (!rc) rc = cuda_rc(cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming));
         }
@@ -1245,28 +1244,25 @@ int xg_next_word(xg_ensemble_t h, uint64_t* out) {
     if (!h || !out) return XG_EINVAL;
     auto& r = h->nr;
     if (r.active && r.pos < kNextBuf) {
-        *out = r.eb == 4 ? static_cast<const uint32_t*>(r.host[r.cur])[r.pos++]
-                         : static_cast<const uint64_t*>(r.host[r.cur])[r.pos++];
+        *out = static_cast<const uint64_t*>(r.host[r.cur])[r.pos++];
         return XG_OK;
     }
     if (h->num_streams != 1) return XG_EINVAL;
     int rc = ring_next(h);
     if (rc) return rc;
-    *out = r.eb == 4 ? static_cast<const uint32_t*>(r.host[r.cur])[r.pos++]
-                     : static_cast<const uint64_t*>(r.host[r.cur])[r.pos++];
+    *out = static_cast<const uint64_t*>(r.host[r.cur])[r.pos++];
     return XG_OK;
 }
 
-int xg_next_view(xg_ensemble_t h, const void** words, uint64_t* count, unsigned* elem_bytes) {
-    if (!h || !words || !count || !elem_bytes) return XG_EINVAL;
+int xg_next_view(xg_ensemble_t h, const uint64_t** words, uint64_t* count) {
+    if (!h || !words || !count) return XG_EINVAL;
     if (h->num_streams != 1) return XG_EINVAL;
     auto& r = h->nr;
     if (!r.active || r.pos >= kNextBuf) {
         int rc = ring_next(h);
         if (rc) return rc;
     }
-    *elem_bytes = r.eb;
-    *words = static_cast<const char*>(r.host[r.cur]) + r.pos * r.eb;
+    *words = static_cast<const uint64_t*>(r.host[r.cur]) + r.pos;
     *count = kNextBuf - r.pos;
     r.pos = kNextBuf;  // served, until xg_next_return gives some back
     return XG_OK;

@@ -741,14 +741,13 @@ def test_next_view_and_return_continue_exactly(oracle):
     h = st.ensemble.handle
     ref = oracle.stream(99, 400000)
     got = []
-    ptr, cnt, eb = ctypes.c_void_p(), ctypes.c_uint64(), ctypes.c_uint()
+    ptr, cnt = ctypes.c_void_p(), ctypes.c_uint64()
     for take in (5, 65531, 70000, 1, 140000):
         left = take
         while left:
-            assert L.xg_next_view(h, ctypes.byref(ptr), ctypes.byref(cnt), ctypes.byref(eb)) == 0
-            assert eb.value == 4
+            assert L.xg_next_view(h, ctypes.byref(ptr), ctypes.byref(cnt)) == 0
             n = min(left, cnt.value)
-            got += np.ctypeslib.as_array((ctypes.c_uint32 * cnt.value).from_address(ptr.value))[:n].tolist()
+            got += np.ctypeslib.as_array((ctypes.c_uint64 * cnt.value).from_address(ptr.value))[:n].tolist()
             assert L.xg_next_return(h, cnt.value - n) == 0
             left -= n
         got.append(st.next_word())
