@@ -222,3 +222,28 @@ def test_bench_two_ranks_self_launched_gloo(workload):
     assert line["parity"]["checked"] and line["parity"]["ok"], line["parity"]
     if workload == "mc_pi":
         assert line["mc"]["allreduce_in_step"]
+
+
+@pytest.mark.gpu
+def test_bench_default_line_contract():
+    """The driver's default command (short): one JSON line with the contract
+    keys, a roofline with the measured write ceiling, the sustained leg, e2e
+    with the copied bytes, and every BASELINE config in extra_workloads with
+    its roofline and a passing full-size parity check."""
+    rc, line, err = _bench_cmd("--gpus", "1", "--steps", "3", "--warmup", "3", "--sustained-s", "0.3",
+                               "--no-cpu")
+    assert rc == 0, err[-3000:]
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "gpu_launches", "clocks", "roofline",
+              "e2e", "parity", "sustained", "extra_workloads"):
+        assert k in line, k
+    assert line["n_gpus"] == 1 and line["gpu_launches"] == 3
+    r = line["roofline"]
+    assert r["bound"] == "hbm" and r["frac"] > 0.5 and r["write_ceiling_gbs"] > 1000
+    assert line["e2e"]["d2h_bytes_per_step"] == 4 << 30 and line["e2e"]["h2d_bytes_per_step"] == 0
+    assert line["parity"]["checked"] and line["parity"]["ok"]
+    assert set(line["extra_workloads"]) == {"fill_f32", "fill_f64", "fill_2p34", "mc_pi"}
+    for name, e in line["extra_workloads"].items():
+        assert e["parity"]["checked"] and e["parity"]["ok"], name
+        assert e["roofline"]["frac"] and e["roofline"]["frac"] > 0.5, name
+    assert abs(line["extra_workloads"]["mc_pi"]["mc"]["pi_estimate"] - 3.14159265) < 1e-4
