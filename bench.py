@@ -773,6 +773,46 @@ def host_api_bench(cb: dict) -> dict:
     return d
 
 
+def extra_e2e(wl: str, ens, fn, ctx, world: int, rank: int) -> dict:
+    """End to end through the public API for the extra workloads: the f32 /
+    f64 fills into pinned host memory (xg_generate_host_f32/f64: device fill
+    + PCIe copy inside the timed region); MC with the job's hit count read
+    back to the host every step.  The 2^34 fill would need 64 GiB of host
+    memory per job and is not copied."""
+    import torch
+
+    first, count, per, _, job_words = workload_geometry(wl, world, rank)
+    if wl in ("fill_f32", "fill_f64"):
+        dt_ = torch.float32 if wl == "fill_f32" else torch.float64
+        host = torch.empty((count, per), dtype=dt_, pin_memory=True)
+        call = ens.generate_f32_into_host if wl == "fill_f32" else ens.generate_f64_into_host
+        call(per, host)
+        barrier(world)
+        t = time.perf_counter()
+        steps = 3
+        for _ in range(steps):
+            call(per, host)
+        dt = max_over_ranks(time.perf_counter() - t, world)
+        nbytes = host.numel() * host.element_size()
+        del host
+        return {"value": job_words * steps / dt, "unit": "RN/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": nbytes, "steps": steps,
+                "api": f"BlockEnsemble.generate_{wl[5:]}_into_host -> xg_generate_host_{wl[5:]} "
+                       "(pinned host buffer)"}
+    if wl == "mc_pi":
+        barrier(world)
+        t = time.perf_counter()
+        steps = 2
+        for _ in range(steps):
+            fn()
+            int(ctx["total"].item())  # the job's hit count on the host
+        dt = max_over_ranks(time.perf_counter() - t, world)
+        return {"value": job_words * steps / dt, "unit": "RN/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 8, "steps": steps,
+                "api": "BlockEnsemble.mc_pi (+ NCCL all-reduce at N > 1) -> hit count read back"}
+    return {"value": None, "why": "the 2^34-word output (64 GiB per job) is not copied to the host"}
+
+
 def dry_run(args) -> int:
     """CPU-only check of the N-rank plumbing (gloo): world, ranks, slices."""
     world, rank, _ = dist_setup(dry=True)
@@ -891,8 +931,10 @@ def main():
         extras = {}
         for xw in EXTRA:
             steps = min(args.steps, 5) if xw == "mc_pi" else args.steps
-            e, _, xctx, xens = run_workload(xw, steps, args.warmup, world, rank, local, hbm_peak,
-                                            peak_src)
+            e, xfn, xctx, xens = run_workload(xw, steps, args.warmup, world, rank, local, hbm_peak,
+                                              peak_src)
+            if not args.no_e2e:
+                e["e2e"] = extra_e2e(xw, xens, xfn, xctx, world, rank)
             xout = xctx.get("out")
             if xout is not None:
                 try:
@@ -903,7 +945,7 @@ def main():
                 except OSError:
                     pass
             e["parity"] = parity_check(xw, world, rank, local, out=xout)
-            del xctx, xens, xout
+            del xctx, xens, xout, xfn
             torch.cuda.empty_cache()
             if rank == 0 and world == 1 and not args.no_cpu:
                 try:

@@ -229,6 +229,11 @@ int xg_skip(xg_ensemble_t h, uint64_t words, xg_stream_t stream);
  * overlapping generation.  host_out should be pinned for full speed. */
 int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,
                      xg_stream_t stream);
+/* Uniform f32 / f64 values (DESIGN.md section 3 conventions) into host
+ * memory, block-major like xg_generate_host, fused conversion on the device;
+ * w = 32 register-window sets (XG_EUNSUPPORTED otherwise). */
+int xg_generate_host_f32(xg_ensemble_t h, uint64_t per_stream, float* host_out, xg_stream_t stream);
+int xg_generate_host_f64(xg_ensemble_t h, uint64_t per_stream, double* host_out, xg_stream_t stream);
 /* BlockEnsemble::generate into the reference's own result layout: rows[g]
  * points at per_stream uint64 elements for stream g (e.g. the data() of
  * vector<uint64_t> per block).  Words cross PCIe as u32 (w <= 32) through

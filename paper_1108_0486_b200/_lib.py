@@ -76,6 +76,8 @@ SIGNATURES = {
     "xg_generate_host": (_int, [_vp, _u64, _vp, _vp]),
     "xg_generate_host_words": (_int, [_vp, _u64, _vp, _vp]),
     "xg_generate_host_rows": (_int, [_vp, _u64, _vp, _vp]),
+    "xg_generate_host_f32": (_int, [_vp, _u64, _vp, _vp]),
+    "xg_generate_host_f64": (_int, [_vp, _u64, _vp, _vp]),
     "xg_generate_host_tiles": (_int, [_vp, _u64, _vp, _vp, ctypes.c_uint, _vp]),
     "xg_next_word": (_int, [_vp, _P(_u64)]),
     "xg_next_view": (_int, [_vp, _P(_vp), _P(_u64)]),

@@ -982,7 +982,8 @@ int generate_host_impl(xg_ensemble_t h, uint64_t per_stream, T* host_out, xg_str
             const uint64_t m = std::min<uint64_t>(m_max, per_stream - k0);
             T* d = reinterpret_cast<T*>(h->d_stage) + slot * slot_words;
             cudaStreamWaitEvent(s, copy_done[slot], 0);
-            rc = launch_fill<MODE>(h, static_cast<uint32_t>(g0), cnt, m, d, nullptr, s);
+            rc = launch_fill<MODE>(h, static_cast<uint32_t>(g0), cnt, (MODE == kF64 ? 2 : 1) * m, d,
+                                   nullptr, s);
             if (rc) break;
             cudaEventRecord(gen_done[slot], s);
             cudaStreamWaitEvent(cs, gen_done[slot], 0);
@@ -1172,6 +1173,18 @@ int xg_generate_host(xg_ensemble_t h, uint64_t per_stream, uint32_t* host_out,
 int xg_generate_host_words(xg_ensemble_t h, uint64_t per_stream, uint64_t* host_out,
                            xg_stream_t stream) {
     return generate_host_impl<kWide>(h, per_stream, host_out, stream);
+}
+
+int xg_generate_host_f32(xg_ensemble_t h, uint64_t per_stream, float* host_out, xg_stream_t stream) {
+    if (h && h->kind == kGeneric) return XG_EUNSUPPORTED;
+    return generate_host_impl<kF32>(h, per_stream, host_out, stream);
+}
+
+int xg_generate_host_f64(xg_ensemble_t h, uint64_t per_stream, double* host_out, xg_stream_t stream) {
+    if (h && h->kind == kGeneric) return XG_EUNSUPPORTED;
+    uint64_t words;
+    if (mul_overflows(per_stream, 2, &words)) return XG_EINVAL;
+    return generate_host_impl<kF64>(h, per_stream, host_out, stream);
 }
 
 }  // extern "C"

@@ -423,6 +423,20 @@ class BlockEnsemble:
         _raise(lib.xg_generate_host(self._h.ptr, per_block, ctypes.c_void_p(ptr),
                                     self._stream(stream)), "generate")
 
+    def generate_f32_into_host(self, per_block: int, host_out, stream=None) -> None:
+        """per_block uniform f32 values of every block into a host buffer
+        (block-major), converted on the device."""
+        ptr = host_out.data_ptr() if hasattr(host_out, "data_ptr") else host_out.ctypes.data
+        _raise(lib.xg_generate_host_f32(self._h.ptr, per_block, ctypes.c_void_p(ptr),
+                                        self._stream(stream)), "generate_f32")
+
+    def generate_f64_into_host(self, per_block: int, host_out, stream=None) -> None:
+        """per_block uniform f64 values (two words each) of every block into a
+        host buffer (block-major), converted on the device."""
+        ptr = host_out.data_ptr() if hasattr(host_out, "data_ptr") else host_out.ctypes.data
+        _raise(lib.xg_generate_host_f64(self._h.ptr, per_block, ctypes.c_void_p(ptr),
+                                        self._stream(stream)), "generate_f64")
+
     def _fill(self, fn, per_block: int, out, torch_dtype, vals_per_block: int, stream):
         torch = _torch()
         if out is None:

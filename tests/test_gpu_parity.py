@@ -842,3 +842,24 @@ def test_generate_host_tiles_callback_order_and_content(oracle):
     assert not bad
     for g in range(P):
         assert seen[g] == sorted(seen[g]) and seen[g][0] == 0 and len(seen[g]) > 1
+
+
+def test_generate_host_f32_f64_equal_device_fills(oracle):
+    """xg_generate_host_f32/f64 (the e2e path of config 3): the same values
+    as the device fills, block-major in host memory, continuing the streams;
+    odd lengths and streams longer than a staging slot."""
+    for P, per in ((5, 1001), (3, 1000), (2, (1 << 26) + 3)):
+        a = xg.BlockEnsemble(GP32, 21, P, 63)
+        b = xg.BlockEnsemble(GP32, 21, P, 63)
+        for _ in range(2):
+            h32 = np.empty((P, per), dtype=np.float32)
+            a.generate_f32_into_host(per, h32)
+            assert np.array_equal(h32.view(np.uint32), np_u32(b.fill_f32(per)).view(np.uint32)), (P, per)
+        h64 = np.empty((P, per // 2), dtype=np.float64)
+        a.generate_f64_into_host(per // 2, h64)
+        assert np.array_equal(h64.view(np.uint64), np_u32(b.fill_f64(per // 2)).view(np.uint64))
+    o = oracle.ensemble(21, 5)
+    c = xg.BlockEnsemble(GP32, 21, 5, 63)
+    h = np.empty((5, 777), dtype=np.float64)
+    c.generate_f64_into_host(777, h)
+    assert np.array_equal(h.view(np.uint64), o.fill_f64(777).view(np.uint64))

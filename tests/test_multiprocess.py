@@ -247,3 +247,7 @@ def test_bench_default_line_contract():
         assert e["parity"]["checked"] and e["parity"]["ok"], name
         assert e["roofline"]["frac"] and e["roofline"]["frac"] > 0.5, name
     assert abs(line["extra_workloads"]["mc_pi"]["mc"]["pi_estimate"] - 3.14159265) < 1e-4
+    for name in ("fill_f32", "fill_f64", "mc_pi"):
+        e2e = line["extra_workloads"][name]["e2e"]
+        assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] == 0, name
+    assert line["extra_workloads"]["fill_f64"]["e2e"]["d2h_bytes_per_step"] == 8 << 30
