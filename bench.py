@@ -86,6 +86,7 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.samples = []
+        self.power = []
         self.max_mhz = None
         self._stop = threading.Event()
         self._t = None
@@ -110,7 +111,13 @@ class ClockSampler:
                         rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
                     except Exception:
                         rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+                    try:
+                        pw = nv.nvmlDeviceGetPowerUsage(self._h) / 1e3
+                    except Exception:
+                        pw = None
                     self.samples.append((float(sm), int(rs)))
+                    if pw is not None:
+                        self.power.append(pw)
                     self._stop.wait(0.002)
                 else:
                     out = subprocess.run(
@@ -139,9 +146,13 @@ class ClockSampler:
         sm = [s for s, _ in self.samples]
         reasons = sorted({name for _, r in self.samples for bit, name in self.REASONS.items()
                           if r & bit})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
-                "samples": len(self.samples), "sm_mhz_min": min(sm),
-                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+               "samples": len(self.samples), "sm_mhz_min": min(sm),
+               "source": "nvml" if self._nvml is not None else "nvidia-smi"}
+        if self.power:
+            out["power_w_median"] = statistics.median(self.power)
+            out["power_w_max"] = max(self.power)
+        return out
 
 
 # --------------------------------------------------------------------------
