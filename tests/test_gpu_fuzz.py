@@ -55,7 +55,8 @@ def test_random_call_sequence(oracle, name, seed):
     base = int(rng.integers(0, 2**63))
     e = xg.BlockEnsemble(p, base, streams, 32)
     o = oracle.ensemble(base, streams, oracle.params(r, s, a, b, c, d, w, omega, gamma))
-    ops = ["u32", "f32", "f64", "u64", "raw", "words", "mc", "skip", "host", "rank"]
+    ops = ["u32", "f32", "f64", "u64", "raw", "words", "mc", "skip", "host", "rank", "rows", "hf32",
+           "hf64"]
     for step in range(40):
         op = ops[int(rng.integers(len(ops)))]
         n = int(rng.integers(1, 700))
@@ -94,6 +95,21 @@ def test_random_call_sequence(oracle, name, seed):
                 assert name == "rt_j2", tag
                 continue
             assert np.array_equal(_host(got).astype(np.uint64), o.rank_counts(k).sum(axis=0)), tag
+        elif op == "rows":  # generate() into caller rows (xg_generate_host_rows)
+            import ctypes
+
+            rows = [np.zeros(n, dtype=np.uint64) for _ in range(streams)]
+            arr = (ctypes.c_void_p * streams)(*[x.ctypes.data for x in rows])
+            assert xg._lib.lib.xg_generate_host_rows(e.handle, n, arr, None) == 0, tag
+            assert np.array_equal(np.stack(rows), o.fill_u32(n).astype(np.uint64)), tag
+        elif op == "hf32":
+            h = np.empty((streams, n), dtype=np.float32)
+            e.generate_f32_into_host(n, h)
+            assert np.array_equal(h.view(np.uint32), o.fill_f32(n).view(np.uint32)), tag
+        elif op == "hf64":
+            h = np.empty((streams, n), dtype=np.float64)
+            e.generate_f64_into_host(n, h)
+            assert np.array_equal(h.view(np.uint64), o.fill_f64(n).view(np.uint64)), tag
         else:
             assert np.array_equal(e.generate(n), o.fill_u32(n)), tag
     # the states agree at the end too
@@ -101,3 +117,56 @@ def test_random_call_sequence(oracle, name, seed):
         buf, wy = e.block_state(g)
         assert np.array_equal(np.array(buf, dtype=np.uint32), o.logical_buffer(g).astype(np.uint32))
         assert wy == o.weyl(g)
+
+
+@pytest.mark.parametrize("name", list(SETS))
+def test_random_single_stream_sequence(oracle, name):
+    """One-stream handles: next_word (the double-buffered pinned ring), the
+    xg_next_view / xg_next_return batch form, next_u64, fills, skips and state
+    exports in random order -- the ring's give-back keeps the serial stream
+    exact across every transition (slot boundaries at 2^16 words)."""
+    import ctypes
+
+    rng = np.random.default_rng(7 + len(name))
+    r, s_, a, b, c, d, w, omega, gamma = SETS[name]
+    p = xg.GeneratorParams(r, s_, a, b, c, d, w, omega, gamma)
+    seed = int(rng.integers(0, 2**63))
+    st = xg.XorgensState(p, seed)
+    ref = oracle.stream(seed, 2600000, oracle.params(r, s_, a, b, c, d, w, omega, gamma))
+    pos = 0
+    L = xg._lib.lib
+    h = st.ensemble.handle
+    ptr, cnt = ctypes.c_void_p(), ctypes.c_uint64()
+    for step in range(60):
+        op = ["word", "view", "u64", "fill", "skip", "state"][int(rng.integers(6))]
+        n = int(rng.integers(1, 40000))
+        tag = f"{name} step {step}: {op}({n}) at {pos}"
+        if op == "word":
+            k = min(n, 300)
+            got = [st.next_word() for _ in range(k)]
+            assert got == ref[pos:pos + k].tolist(), tag
+            pos += k
+        elif op == "view":
+            assert L.xg_next_view(h, ctypes.byref(ptr), ctypes.byref(cnt)) == 0, tag
+            k = min(n, cnt.value)
+            got = np.ctypeslib.as_array((ctypes.c_uint64 * cnt.value).from_address(ptr.value))[:k]
+            assert np.array_equal(got, ref[pos:pos + k].astype(np.uint64)), tag
+            assert L.xg_next_return(h, cnt.value - k) == 0, tag
+            pos += k
+        elif op == "u64":
+            v = st.next_u64()
+            assert v == int(ref[pos]) | (int(ref[pos + 1]) << 32), tag
+            pos += 2
+        elif op == "fill":
+            got = _host(st.ensemble.fill_u32(n))[0]
+            assert np.array_equal(got, ref[pos:pos + n]), tag
+            pos += n
+        elif op == "skip":
+            st.ensemble.skip(n)
+            pos += n
+        else:
+            o = oracle.ensemble(seed, 1, oracle.params(r, s_, a, b, c, d, w, omega, gamma))
+            o.fill_u32(pos)
+            assert np.array_equal(np.array(st.logical_buffer(), dtype=np.uint64), o.logical_buffer(0)), tag
+            assert st.weyl_value() == o.weyl(0), tag
+        assert pos < 2600000 - 80000
