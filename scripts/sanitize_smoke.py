@@ -65,3 +65,27 @@ e2 = xg.BlockEnsemble(p, 5, 9, 63)
 assert xg._lib.lib.xg_generate_host_rows(e2.handle, 777, arr, None) == 0
 assert np.array_equal(np.stack(rows), o.ensemble(5, 9).fill_u32(777).astype(np.uint64))
 print("sanitize round-2 paths ok")
+
+# generate() through host tiles (the C++ drop-in path) and the f32/f64 host generates
+FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                      ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint)
+seen = []
+cb = FN(lambda ctx, s0, w0, ns, nw, tile, eb, part, parts: seen.append((s0, w0, ns, nw)) if part == 0 else None)
+e3 = xg.BlockEnsemble(p, 6, 7, 63)
+assert xg._lib.lib.xg_generate_host_tiles(e3.handle, 999, cb, None, 2, None) == 0 and seen
+h32 = np.empty((7, 333), dtype=np.float32)
+e3.generate_f32_into_host(333, h32)
+h64 = np.empty((7, 200), dtype=np.float64)
+e3.generate_f64_into_host(200, h64)
+oe3 = o.ensemble(6, 7)
+oe3.fill_u32(999)
+assert np.array_equal(h32.view(np.uint32), oe3.fill_f32(333).view(np.uint32))
+assert np.array_equal(h64.view(np.uint64), oe3.fill_f64(200).view(np.uint64))
+w2 = torch.randint(0, 2**31, (64 * 9,), dtype=torch.int32, device="cuda")
+cnt = torch.zeros(3, dtype=torch.int64, device="cuda")
+assert xg._lib.lib.xg_rank_words(w2.data_ptr(), 17, cnt.data_ptr(), None) == 0
+hist = torch.zeros(129, dtype=torch.int64, device="cuda")
+assert xg._lib.lib.xg_lc_words(w2.data_ptr(), w2.numel(), 128, 40, hist.data_ptr(), None) == 0
+torch.cuda.synchronize()
+assert int(cnt.sum()) == 17 and int(hist.sum()) == 40
+print("sanitize round-2 host tiles / f32-f64 host / word-buffer tests ok")
