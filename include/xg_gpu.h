@@ -195,6 +195,13 @@ int xg_rank_words(const uint32_t* dev_words, uint64_t matrices, uint64_t* dev_co
  * buffer holds fewer than block_length * blocks bits). */
 int xg_lc_words(const uint32_t* dev_words, uint64_t nwords, unsigned block_length, uint64_t blocks,
                 uint64_t* dev_hist, xg_stream_t stream);
+/* w-bit words (w = 8, 16, 32; each in the low bits of a uint32, e.g. a fill of
+ * a tiny set) -> the bit stream BitSource reads (w bits per word, MSB first,
+ * proj/include/xg/stream.hpp:95-110) packed into ceil(n w / 32) uint32 words,
+ * the input for the counting calls below; left_align = 1: n words, each
+ * shifted to the top of its 32 bits (birthday spacings' draws). */
+int xg_pack_words(const uint32_t* dev_in, uint64_t n, unsigned w, int left_align, uint32_t* dev_out,
+                  xg_stream_t stream);
 /* Counting loops of monobit and runs_test (proj/src/stattests/tests.cpp:33-79)
  * over the first nbits bits of a device word buffer read MSB first (as
  * BitSource reads 32-bit words): dev_out2[0] += ones, dev_out2[1] +=

@@ -222,6 +222,9 @@ class Battery:
         self.lib = ctypes.CDLL(path)
         self.lib.xgref_battery_on_words.argtypes = [_vp, _u64, _int, ctypes.c_char_p,
                                                     ctypes.c_char_p, _u64]
+        self.lib.xgref_battery_config_on_words.argtypes = [_vp, _u64, ctypes.c_uint, ctypes.c_char_p,
+                                                           ctypes.c_char_p, ctypes.c_char_p, _u64,
+                                                           ctypes.c_char_p, _u64]
         self.lib.xgref_gf2_rank32.argtypes = [_vp]
         self.lib.xgref_gf2_rank32.restype = ctypes.c_uint
         self.lib.xgref_berlekamp_massey.argtypes = [_vp, _u64]
@@ -272,6 +275,17 @@ class Battery:
                                                ctypes.byref(pv)):
             raise ValueError("matrix_rank_test failed (buffer too short or < 38 matrices)")
         return st.value, pv.value
+
+    def run_config(self, words: np.ndarray, bits: int, config_text: str = "", generator: str = "gpu",
+                   params: str = "", seed: int = 0):
+        """run_battery over `bits`-wide words (one per element) with a
+        BatteryConfig::parse text: (verdict, report JSON)."""
+        w = np.ascontiguousarray(words, dtype=np.uint64).reshape(-1)
+        buf = ctypes.create_string_buffer(1 << 16)
+        v = self.lib.xgref_battery_config_on_words(_ptr(w), w.size, bits, config_text.encode(),
+                                                   generator.encode(), params.encode(),
+                                                   seed & (2**64 - 1), buf, len(buf))
+        return self.VERDICTS.get(v, str(v)), buf.value.decode()
 
     def run(self, words: np.ndarray, quick: bool = False, label: str = "gpu"):
         w = np.ascontiguousarray(words, dtype=np.uint32).reshape(-1)

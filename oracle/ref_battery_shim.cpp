@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -33,6 +34,41 @@ int xgref_battery_on_words(const std::uint32_t* words, std::uint64_t n, int quic
     try {
         auto cfg = quick ? xg::stats::BatteryConfig::quick() : xg::stats::BatteryConfig::defaults();
         auto report = xg::stats::run_battery(src, cfg, label, "GPU-generated words", 0);
+        std::string js = xg::stats::to_json(report);
+        if (json_out && cap) {
+            std::strncpy(json_out, js.c_str(), cap - 1);
+            json_out[cap - 1] = 0;
+        }
+        return static_cast<int>(report.overall);
+    } catch (const std::exception& e) {
+        if (json_out && cap) {
+            std::strncpy(json_out, e.what(), cap - 1);
+            json_out[cap - 1] = 0;
+        }
+        return -1;
+    }
+}
+
+// run_battery over `bits`-wide words (bits = 8, 16, 32, 64: each buffer
+// element holds one word) with a BatteryConfig parsed from `config_text`
+// (BatteryConfig::parse, battery.cpp:38-70; empty = defaults); the report's
+// generator / params / seed fields are the caller's.  Returns the overall
+// verdict as xgref_battery_on_words does (-1: exhausted / threw, message in
+// json_out).
+int xgref_battery_config_on_words(const std::uint64_t* words, std::uint64_t n, unsigned bits,
+                                  const char* config_text, const char* generator, const char* params,
+                                  std::uint64_t seed, char* json_out, std::uint64_t cap) {
+    std::uint64_t pos = 0;
+    xg::CallbackSource src(
+        [&]() -> std::uint64_t {
+            if (pos >= n) throw std::runtime_error("word buffer exhausted");
+            return words[pos++];
+        },
+        bits);
+    try {
+        std::istringstream in(config_text ? config_text : "");
+        auto cfg = xg::stats::BatteryConfig::parse(in);
+        auto report = xg::stats::run_battery(src, cfg, generator, params, seed);
         std::string js = xg::stats::to_json(report);
         if (json_out && cap) {
             std::strncpy(json_out, js.c_str(), cap - 1);

@@ -67,6 +67,7 @@ SIGNATURES = {
     "xg_rank_test": (_int, [_vp, _u64, _vp, _vp]),
     "xg_linear_complexity_test": (_int, [_vp, ctypes.c_uint, _u64, _vp, _vp]),
     "xg_berlekamp_massey": (_int, [_vp, _u64, _u32, _u64, _vp, _vp]),
+    "xg_pack_words": (_int, [_vp, _u64, ctypes.c_uint, _int, _vp, _vp]),
     "xg_rank_words": (_int, [_vp, _u64, _vp, _vp]),
     "xg_lc_words": (_int, [_vp, _u64, ctypes.c_uint, _u64, _vp, _vp]),
     "xg_bits_ones_runs": (_int, [_vp, _u64, _vp, _vp]),

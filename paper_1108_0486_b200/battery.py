@@ -117,55 +117,86 @@ class BatteryInputError(RuntimeError):
 
 class _GenWords:
     """The stream of XorgensState(params, seed) on the GPU (raw=True: the
-    Weyl-ablated RawXorgens stream).  Each call consumes the next words, as
-    each of the reference's tests reads the same WordSource in turn."""
+    Weyl-ablated RawXorgens stream), w = 8, 16 or 32.  Each call consumes the
+    next words, as each of the reference's tests reads the same WordSource in
+    turn through a fresh BitSource (w bits per word, MSB first)."""
 
     def __init__(self, params: GeneratorParams, seed: int, device: int, raw: bool):
         self.e = BlockEnsemble(params, seed, 1, lane_bound(params), device=device)
         self.raw = raw
-        self.fused_rank = not raw and fast_path(params) and params.r - params.s < 64
+        self.w = params.w
+        self.fused = not raw and self.w == 32 and fast_path(params)
+        self.fused_rank = self.fused and params.r - params.s < 64
 
-    def take(self, n: int):
+    def _words(self, n: int):
         return (self.e.fill_raw_u32(n) if self.raw else self.e.fill_u32(n))[0]
 
     def stream(self):
         return self.e._stream()
 
+    def take_bits(self, nbits: int):
+        """The next ceil(nbits / w) words as a 32-bit MSB-first bit stream."""
+        words = self._words((nbits + self.w - 1) // self.w)
+        return words if self.w == 32 else _pack(words, self.w, False, self.stream())
+
+    def take_draws(self, n: int):
+        """The next n words, each at the top of 32 bits (birthday draws)."""
+        words = self._words(n)
+        return words if self.w == 32 else _pack(words, self.w, True, self.stream())
+
     def rank_bins(self, m: int, dev: str):
         if self.fused_rank:  # fused in the generator: no words stored
             return self.e.rank_test(m)
-        return _rank_words(self.take(32 * m), m, dev, self.stream())
+        return _rank_words(self.take_bits(1024 * m), m, dev, self.stream())
 
     def lc_hist(self, k: int, nb: int, dev: str):
-        if not self.raw:  # words staged by the library, the BitSource tail dropped
+        if self.fused:  # words staged by the library, the BitSource tail dropped
             return self.e.linear_complexity_test(k, nb)
-        return _lc_words(self.take((k * nb + 31) // 32), k, nb, dev, self.stream())
+        bits = self.take_bits(k * nb)
+        return _lc_words(bits, k, nb, dev, self.stream())
 
 
 class _BufWords:
     """32-bit words already on the device (e.g. a raw-le file), consumed in
     order like the reference's FileWordSource."""
 
+    w = 32
+
     def __init__(self, words, stream):
-        self.w = words
+        self.words = words
         self.pos = 0
         self.s = stream
 
-    def take(self, n: int):
-        if self.pos + n > self.w.numel():
+    def _take(self, n: int):
+        if self.pos + n > self.words.numel():
             raise BatteryInputError("input exhausted: the battery needs more words than the input holds")
-        out = self.w[self.pos:self.pos + n]
+        out = self.words[self.pos:self.pos + n]
         self.pos += n
         return out
+
+    def take_bits(self, nbits: int):
+        return self._take((nbits + 31) // 32)
+
+    def take_draws(self, n: int):
+        return self._take(n)
 
     def stream(self):
         return self.s
 
     def rank_bins(self, m: int, dev: str):
-        return _rank_words(self.take(32 * m), m, dev, self.s)
+        return _rank_words(self.take_bits(1024 * m), m, dev, self.s)
 
     def lc_hist(self, k: int, nb: int, dev: str):
-        return _lc_words(self.take((k * nb + 31) // 32), k, nb, dev, self.s)
+        return _lc_words(self.take_bits(k * nb), k, nb, dev, self.s)
+
+
+def _pack(words, w: int, left_align: bool, stream):
+    torch = _torch()
+    n = words.numel()
+    out = torch.empty(n if left_align else (n * w + 31) // 32, dtype=torch.int32, device=words.device)
+    _raise(lib.xg_pack_words(ctypes.c_void_p(words.data_ptr()), n, w, int(left_align),
+                             ctypes.c_void_p(out.data_ptr()), stream))
+    return out
 
 
 def _rank_words(words, m: int, dev: str, stream):
@@ -195,8 +226,8 @@ def run_battery_gpu(params: GeneratorParams, seed: int, config: BatteryConfig = 
     else it runs over stored words (xg_rank_words)."""
     torch = _torch()
     cfg = config or BatteryConfig.defaults()
-    if params.w != 32:
-        raise ValueError("the GPU battery reads 32-bit words")
+    if params.w not in (8, 16, 32):
+        raise ValueError("the GPU battery reads 8-, 16- or 32-bit words")
     with torch.cuda.device(device):
         return _run_battery(_GenWords(params, seed, device, raw), cfg, device, seed)
 
@@ -222,7 +253,7 @@ def _run_battery(src, cfg: BatteryConfig, device: int, seed: int) -> Dict:
     tests: List[Dict] = []
 
     def bits_counts(nbits: int):
-        words = src.take((nbits + 31) // 32)
+        words = src.take_bits(nbits)
         out = torch.zeros(2, dtype=torch.int64, device=dev)
         _raise(lib.xg_bits_ones_runs(ctypes.c_void_p(words.data_ptr()), nbits,
                                      ctypes.c_void_p(out.data_ptr()), src.stream()))
@@ -270,20 +301,20 @@ def _run_battery(src, cfg: BatteryConfig, device: int, seed: int) -> Dict:
                       "verdict": _verdict(p)})
     if cfg.run_birthday:  # tests.cpp:175-212
         n, t, rounds = cfg.birthday_draws, cfg.birthday_bits, cfg.birthday_rounds
-        if t == 0 or t > 32:
+        if t == 0 or t > src.w:
             raise ValueError("t_bits must fit in the source word size")
         if rounds == 0 or n < 2:
             raise ValueError("birthday spacings needs draws and rounds")
         lam = float(n) * float(n) * float(n) / math.pow(2.0, t + 2.0)
         if lam < 1.0 or lam > 16.0:
             raise ValueError("n^3 / 2^{t+2} must lie in [1, 16]")
-        words = src.take(n * rounds)
+        words = src.take_draws(n * rounds)
         dup = torch.zeros(1, dtype=torch.int64, device=dev)
         _raise(lib.xg_birthday_duplicates(ctypes.c_void_p(words.data_ptr()), n, rounds, t,
                                           ctypes.c_void_p(dup.data_ptr()), src.stream()))
         d = int(dup.item())
         p = poisson_upper_tail(d, lam * rounds)
-        tests.append({"name": "birthday_spacings", "n": rounds * n * 32, "statistic": float(d),
+        tests.append({"name": "birthday_spacings", "n": rounds * n * src.w, "statistic": float(d),
                       "p": p, "verdict": _verdict(p)})
     overall = "pass"
     for tr in tests:

@@ -854,6 +854,25 @@ int xg_lc_words(const uint32_t* dev_words, uint64_t nwords, unsigned block_lengt
                           static_cast<uint64_t>(block_length) * blocks, blocks, hist, nullptr, s);
 }
 
+int xg_pack_words(const uint32_t* dev_in, uint64_t n, unsigned w, int left_align, uint32_t* dev_out,
+                  xg_stream_t stream) {
+    if (!dev_in || !dev_out || (w != 8 && w != 16 && w != 32)) return XG_EINVAL;
+    if (n == 0) return XG_OK;
+    int dev;
+    int rc = ptr_device(dev_in, &dev);
+    if (rc) return rc;
+    DeviceGuard dg(dev);
+    if (!dg.ok) return XG_ECUDA;
+    const uint64_t nout = left_align ? n : (n * w + 31) / 32;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((nout + 255) / 256, 8ull * sms));
+    pack_words_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(dev_in, n, w, left_align,
+                                                                              dev_out, nout);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cuda_rc(cudaGetLastError());
+}
+
 int xg_bits_ones_runs(const uint32_t* dev_words, uint64_t nbits, uint64_t* dev_out2,
                       xg_stream_t stream) {
     if (!dev_words || !dev_out2 || (reinterpret_cast<uintptr_t>(dev_out2) % 8) != 0) return XG_EINVAL;

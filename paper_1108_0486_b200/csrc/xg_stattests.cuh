@@ -180,6 +180,39 @@ birthday_kernel(const uint32_t* __restrict__ words, uint32_t n, unsigned drop,
 
 }  // namespace xgk
 
+// ---- w-bit words -> the 32-bit MSB-first bit stream -------------------------
+namespace xgk {
+
+// The statistical tests read a WordSource through BitSource: w bits per word,
+// MSB first (proj/include/xg/stream.hpp:95-110).  For w < 32 the counting
+// kernels take the same bit stream packed into 32-bit words: output word j =
+// input words [j * 32/w, (j+1) * 32/w) concatenated, the first in the top
+// bits (zero past the end).  left_align: each word shifted to the top of its
+// 32 bits instead (birthday spacings reads the top t bits of every w-bit
+// word).  Grid-stride.
+__global__ void __launch_bounds__(256)
+pack_words_kernel(const uint32_t* __restrict__ in, uint64_t n, unsigned w, int left_align,
+                  uint32_t* __restrict__ out, uint64_t nout) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint32_t mask = w >= 32 ? ~0u : ((1u << w) - 1u);
+    for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < nout; j += stride) {
+        if (left_align) {
+            out[j] = w >= 32 ? in[j] : (in[j] & mask) << (32u - w);
+            continue;
+        }
+        const unsigned per = 32u / w;
+        uint32_t v = 0;
+        for (unsigned k = 0; k < per; ++k) {
+            const uint64_t idx = j * per + k;
+            const uint32_t x = idx < n ? (in[idx] & mask) : 0u;
+            v = w >= 32 ? x : ((v << w) | x);
+        }
+        out[j] = v;
+    }
+}
+
+}  // namespace xgk
+
 // ---- Berlekamp-Massey for long sequences (up to 2^18 bits) ----------------
 namespace xgk {
 

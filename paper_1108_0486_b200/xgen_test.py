@@ -9,9 +9,10 @@ layout as the reference's to_json (battery.cpp:114-130: keys sorted as
 nlohmann::json sorts them, two-space indent) and the same exit codes: 0 pass
 (or not applicable), 2 suspect, 3 fail, 64 unknown generator, 66 I/O (config
 or input unreadable, input exhausted), 67 bad arguments / bad config.
-Generators: the xorgens ids with 32-bit words (xorgensgp32 and its
-Weyl-ablated form xorgens-raw); --input reads raw-le 32-bit words
-("file:<path>", seed 0), copied to the device once.
+Generators: every xorgens id of the reference registry (xorgensgp32,
+xorgens-raw, tiny:r2w8 / r2w16 / r4w16 and their tiny-raw: forms -- the
+8- and 16-bit sets read w bits per word, as BitSource does); --input reads
+raw-le 32-bit words ("file:<path>", seed 0), copied to the device once.
 """
 from __future__ import annotations
 
@@ -23,11 +24,20 @@ import numpy as np
 EXIT_OK, EXIT_SUSPECT, EXIT_FAIL = 0, 2, 3
 EXIT_UNKNOWN_GENERATOR, EXIT_IO, EXIT_BAD_ARGS = 64, 66, 67
 
-# registry ids with 32-bit words (proj/src/registry.cpp:27-42): (raw, params display)
-GENERATORS = {
-    "xorgensgp32": (False, "(r,s,a,b,c,d)=(128,65,15,14,12,17) w=32 gamma=16 omega=2654435769"),
-    "xorgens-raw": (True, "(r,s,a,b,c,d)=(128,65,15,14,12,17) w=32 (no Weyl stage)"),
-}
+# the xorgens ids of the registry (proj/src/registry.cpp:27-42): (params factory, raw)
+def _generators():
+    from . import xorgens as x
+
+    return {"xorgensgp32": (x.xorgensgp32_params, False), "xorgens-raw": (x.xorgensgp32_params, True),
+            "tiny:r2w8": (x.tiny_r2w8_params, False), "tiny:r2w16": (x.tiny_r2w16_params, False),
+            "tiny:r4w16": (x.tiny_r4w16_params, False), "tiny-raw:r2w8": (x.tiny_r2w8_params, True),
+            "tiny-raw:r2w16": (x.tiny_r2w16_params, True), "tiny-raw:r4w16": (x.tiny_r4w16_params, True)}
+
+
+def params_display(p, raw: bool) -> str:
+    """proj/tools/xgen.cpp:116-129."""
+    s = f"(r,s,a,b,c,d)=({p.r},{p.s},{p.a},{p.b},{p.c},{p.d}) w={p.w}"
+    return s + (" (no Weyl stage)" if raw else f" gamma={p.gamma} omega={p.omega}")
 
 
 def _err(msg: str, code: int) -> int:
@@ -101,13 +111,13 @@ def main(argv=None) -> int:
             report = run_battery_on_words(words, cfg, seed=0)
             gen_id, params = "file:" + a["input"], "32-bit little-endian words"
         else:
-            if a["generator"] not in GENERATORS:
+            gens = _generators()
+            if a["generator"] not in gens:
                 return _err(f"unknown generator: {a['generator']}", EXIT_UNKNOWN_GENERATOR)
-            from .xorgens import xorgensgp32_params
-
-            raw, params = GENERATORS[a["generator"]]
-            report = run_battery_gpu(xorgensgp32_params(), a["seed"], cfg, raw=raw)
-            gen_id = a["generator"]
+            factory, raw = gens[a["generator"]]
+            p = factory()
+            report = run_battery_gpu(p, a["seed"], cfg, raw=raw)
+            gen_id, params = a["generator"], params_display(p, raw)
     except BatteryInputError as e:
         return _err(str(e), EXIT_IO)
     except ValueError as e:

@@ -270,3 +270,19 @@ def test_test_input_file_equals_reference(oracle, tmp_path):
     short = tmp_path / "s.bin"
     words[:50000].astype("<u4").tofile(short)
     assert run("test", "--input", str(short), "--config", str(cfg))[0] == 66
+
+
+@gpu
+def test_test_tiny_raw_negative_control_exits_3(tmp_path):
+    """`xgen test -g tiny-raw:r2w8` (8-bit words, no Weyl stage): the
+    reference's negative control fails the battery -- exit 3."""
+    import json
+
+    cfg = tmp_path / "nb.cfg"
+    cfg.write_text(QUICK_CFG + "birthday.enabled = false\n")
+    rc, out = run("test", "-g", "tiny-raw:r2w8", "--seed", "1", "--config", str(cfg))
+    rep = json.loads(out)
+    assert rc == 3 and rep["overall"] == "fail"
+    assert rep["params"] == "(r,s,a,b,c,d)=(2,1,1,1,5,7) w=8 (no Weyl stage)"
+    # default config: birthday's 32-bit draws cannot apply to 8-bit words -> 67
+    assert run("test", "-g", "tiny:r2w8")[0] == 67

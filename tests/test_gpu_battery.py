@@ -147,3 +147,73 @@ def test_battery_on_a_non_current_device(reference):  # pragma: no cover - 1-GPU
     a = run_battery_gpu(xg.xorgensgp32_params(), 3, BatteryConfig.quick(), device=1)
     b = run_battery_gpu(xg.xorgensgp32_params(), 3, BatteryConfig.quick(), device=0)
     assert a == b
+
+
+def _words_consumed_w(cfg, w):
+    """Words a run_battery consumes from a w-bit source (BitSource reads w
+    bits per word; each test starts a fresh BitSource)."""
+    per = lambda bits: (bits + w - 1) // w  # noqa: E731
+    n = 0
+    if cfg.run_monobit:
+        n += per(cfg.monobit_bits)
+    if cfg.run_runs:
+        n += per(cfg.runs_bits)
+    if cfg.run_matrix_rank:
+        n += per(1024 * cfg.rank_matrices)
+    if cfg.run_linear_complexity:
+        n += per(cfg.lc_block_length * cfg.lc_blocks)
+    if cfg.run_birthday:
+        n += cfg.birthday_draws * cfg.birthday_rounds
+    return n
+
+
+def _cfg_text(cfg):
+    b = lambda v: "true" if v else "false"  # noqa: E731
+    return (f"monobit.enabled = {b(cfg.run_monobit)}\nmonobit.bits = {cfg.monobit_bits}\n"
+            f"runs.enabled = {b(cfg.run_runs)}\nruns.bits = {cfg.runs_bits}\n"
+            f"matrix_rank.enabled = {b(cfg.run_matrix_rank)}\nmatrix_rank.matrices = {cfg.rank_matrices}\n"
+            f"linear_complexity.enabled = {b(cfg.run_linear_complexity)}\n"
+            f"linear_complexity.block_length = {cfg.lc_block_length}\n"
+            f"linear_complexity.blocks = {cfg.lc_blocks}\n"
+            f"birthday.enabled = {b(cfg.run_birthday)}\nbirthday.draws = {cfg.birthday_draws}\n"
+            f"birthday.bits = {cfg.birthday_bits}\nbirthday.rounds = {cfg.birthday_rounds}\n")
+
+
+@pytest.mark.parametrize("tiny,raw,quick", [("r2w8", True, False), ("r4w16", False, True),
+                                            ("r2w16", True, True)])
+def test_battery_on_8_and_16_bit_sets_equals_reference(reference, tiny, raw, quick):
+    """The 8- and 16-bit verification sets read w bits per word (BitSource):
+    packed into the 32-bit bit stream on the GPU (xg_pack_words), the report
+    equals the reference's run_battery over the same w-bit words.  r2w8 raw
+    is the reference's own negative control (acceptance.cpp:253-265)."""
+    from oracle import Params
+
+    b = _battery()
+    p = getattr(xg, f"tiny_{tiny}_params")()
+    cfg = BatteryConfig.quick() if quick else BatteryConfig.defaults()
+    cfg.run_birthday = False  # t_bits = 32 cannot apply to w < 32 words (tests.cpp:179-180)
+    rep = run_battery_gpu(p, 1, cfg, raw=raw)
+    pr = Params(p.r, p.s, p.a, p.b, p.c, p.d, p.w, p.omega, p.gamma)
+    n = _words_consumed_w(cfg, p.w)
+    words = (reference.raw_stream(1, n, pr) if raw else reference.stream(1, n, pr))
+    verdict, js = b.run_config(words, p.w, _cfg_text(cfg))
+    ref = json.loads(js)
+    assert rep["overall"] == ref["overall"] == verdict
+    for mine, theirs in zip(rep["tests"], ref["tests"]):
+        assert (mine["name"], mine["n"], mine["statistic"], mine["p"], mine["verdict"]) == \
+               (theirs["name"], theirs["n"], theirs["statistic"], theirs["p"], theirs["verdict"])
+
+
+def test_quality_split_on_gpu():
+    """acceptance.cpp:241-270 (criterion 4) with the counting on the GPU:
+    xorgensgp32 passes the default battery; the Weyl-ablated tiny r2w8
+    (birthday disabled) fails, caught by linear complexity or matrix rank
+    with p < 1e-10."""
+    good = run_battery_gpu(xg.xorgensgp32_params(), 1, BatteryConfig.defaults())
+    assert good["overall"] == "pass"
+    cfg = BatteryConfig.defaults()
+    cfg.run_birthday = False
+    bad = run_battery_gpu(xg.tiny_r2w8_params(), 1, cfg, raw=True)
+    assert bad["overall"] == "fail"
+    assert any(t["name"] in ("linear_complexity", "matrix_rank") and t["verdict"] == "fail"
+               and t["p"] < 1e-10 for t in bad["tests"])
