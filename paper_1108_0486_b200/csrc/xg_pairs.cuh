@@ -275,10 +275,14 @@ __device__ __forceinline__ void pair_body(uint2& A, uint2& B, const P& p, const 
 // `words`), u64 rows 16-byte aligned, f64 `words` even, MC `words` a
 // multiple of 64, rank `words` a multiple of 32.
 // CTAs of 1..32 warps (one stream each).  GP32 fits 32 registers (64 warps
-// per SM); the runtime-parameter sets (CTAs of <= 8 warps) keep their extra
-// shift registers rather than spill.
+// per SM) -- except the Monte Carlo mode, which is bound by its integer pipes
+// at any occupancy and schedules better with the 52 registers ptxas takes when
+// allowed 64 (32 warps per SM: +1.4 %, profiles/s2m_lib_ab.txt); the
+// runtime-parameter sets (CTAs of <= 8 warps) keep their extra shift
+// registers rather than spill.
 template <class P, int MODE>
-__global__ void __launch_bounds__(std::is_same_v<P, GP32> ? 1024 : 256, std::is_same_v<P, GP32> ? 2 : 5)
+__global__ void __launch_bounds__(std::is_same_v<P, GP32> ? 1024 : 256,
+                                  std::is_same_v<P, GP32> ? (MODE == kMC ? 1 : 2) : 5)
 pair_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32_t g_begin,
             uint32_t g_count, uint64_t words, void* __restrict__ out,
             unsigned long long* __restrict__ hits_out) {
