@@ -32,6 +32,7 @@ import os
 import socket
 import statistics
 import subprocess
+import tempfile
 import sys
 import threading
 import time
@@ -174,6 +175,27 @@ def _nccl_debug_env(env) -> None:
     if env.get("NCCL_DEBUG", "").upper() in ("", "VERSION", "WARN"):
         env["NCCL_DEBUG"] = "INFO"
         env.setdefault("NCCL_DEBUG_SUBSYS", "INIT,ENV")
+    # NCCL logs to stdout by default; stdout carries only the JSON line, so
+    # the log goes to a per-process file that forward_nccl_log() copies to
+    # stderr.
+    env.setdefault("NCCL_DEBUG_FILE", os.path.join(tempfile.gettempdir(), "xg_bench_nccl.%h.%p.log"))
+
+
+def forward_nccl_log() -> None:
+    """Copy this process's NCCL log (communicator init: rank, nRanks,
+    channels) to stderr and remove it."""
+    path = os.environ.get("NCCL_DEBUG_FILE", "")
+    if not path.startswith(os.path.join(tempfile.gettempdir(), "xg_bench_nccl.")):
+        return
+    import glob
+
+    for f in glob.glob(path.replace("%h", "*").replace("%p", str(os.getpid()))):
+        try:
+            with open(f) as fh:
+                sys.stderr.write(fh.read())
+            os.remove(f)
+        except OSError:
+            pass
 
 
 def self_launch(args) -> int:
@@ -209,7 +231,25 @@ def dist_setup(dry: bool = False):
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         else:
             dist.init_process_group(backend)
+    elif world == 1 and not dry and backend == "nccl" and not dist.is_initialized():
+        # N = 1: a one-rank NCCL communicator, so the job's collective (the
+        # MC hit-count all-reduce) runs through NCCL at every N, this one too.
+        _nccl_debug_env(os.environ)
+        try:
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}",
+                                    rank=0, world_size=1, device_id=torch.device(f"cuda:{local}"))
+        except Exception as e:  # noqa: BLE001 -- reported in the line's `comm`
+            _COMM_ERR.append(f"{type(e).__name__}: {e}"[:200])
     return world, rank, local
+
+
+_COMM_ERR: list = []
+
+
+def _dist_ready() -> bool:
+    import torch.distributed as dist
+
+    return dist.is_initialized()
 
 
 def barrier(world):
@@ -248,9 +288,10 @@ def all_ok(ok: bool, world: int) -> bool:
 
 
 def comm_info(world: int) -> dict:
-    if world == 1:
-        return {"backend": None, "nranks": 1}
     import torch.distributed as dist
+
+    if world == 1 and not dist.is_initialized():
+        return {"backend": None, "nranks": 1, "init_error": _COMM_ERR[0] if _COMM_ERR else None}
 
     return {"backend": dist.get_backend(), "nranks": dist.get_world_size(),
             "nccl_debug": os.environ.get("NCCL_DEBUG")}
@@ -420,13 +461,12 @@ def parity_check(wl: str, world: int, rank: int, local: int, out=None) -> dict:
     return res
 
 
-def write_ceiling(out, stream, reps: int = 5) -> dict:
-    """Write-only HBM ceilings on the same buffer, same run (libxg_probe.so):
-    memset, the fill's store shape (one warp per row, 8- or 16-byte stores,
-    4 rows per CTA, <= 4 resident CTAs per SM) and a grid-stride stream."""
+def probe_shapes(out, stream) -> dict:
+    """Write-only store patterns over `out` (libxg_probe.so): memset, the
+    fill's store shape (one warp per row, 8- or 16-byte stores, 4 rows per
+    CTA, <= 4 resident CTAs per SM) and a grid-stride stream; each returns
+    nonzero on failure."""
     import ctypes
-
-    import torch
 
     lib = ctypes.CDLL(os.path.join(ROOT, "paper_1108_0486_b200", "lib", "libxg_probe.so"))
     vp = ctypes.c_void_p
@@ -446,6 +486,16 @@ def write_ceiling(out, stream, reps: int = 5) -> dict:
         "rows_stg128_8w_nocap": lambda: lib.xg_probe_rows(ptr, nbytes, row, 16, 8, 0, sp),
         "gridstride_stg128": lambda: lib.xg_probe_gridstride(ptr, nbytes, sp),
     }
+    return shapes
+
+
+def write_ceiling(out, stream, reps: int = 5) -> dict:
+    """Write-only HBM ceilings on the same buffer, same run: the best of
+    `reps` timed passes of every probe_shapes() pattern, GB/s."""
+    import torch
+
+    nbytes = out.numel() * out.element_size()
+    shapes = probe_shapes(out, stream)
     res = {}
     for name, fn in shapes.items():
         for _ in range(3):
@@ -491,14 +541,14 @@ def make_step(wl, ens, count, per, world, local):
     else:  # mc_pi: per-rank hits, then the job's one collective, inside the step
         hits = ctx["hits"] = torch.zeros(1, dtype=torch.int64, device=dev)
         total = ctx["total"] = torch.zeros(1, dtype=torch.int64, device=dev)
-        if world > 1:
-            import torch.distributed as dist
+        import torch.distributed as dist
 
+        if dist.is_initialized():
             def fn():
                 hits.zero_()
                 ens.mc_pi(per, hits=hits)
                 total.copy_(hits)
-                dist.all_reduce(total)  # NCCL uint64 sum over the job, every step
+                dist.all_reduce(total)  # NCCL uint64 sum over the job, every step (N = 1: one rank)
         else:
             def fn():
                 hits.zero_()
@@ -580,7 +630,10 @@ def run_workload(wl, steps, warmup, world, rank, local, hbm_peak, peak_src):
                        "pi_estimate": 4.0 * total / samples_last,
                        "abs_err_over_sigma": abs(4.0 * total / samples_last - 3.141592653589793)
                        / (4.0 * (0.7853981633974483 * 0.2146018366025517 / samples_last) ** 0.5),
-                       "allreduce_in_step": world > 1}
+                       "allreduce_in_step": _dist_ready(),
+                       "allreduce": (f"torch.distributed all_reduce (NCCL, {world} rank"
+                                     f"{'s' if world > 1 else ''}) of the uint64 hit count"
+                                     if _dist_ready() else None)}
     return entry, fn, ctx, ens
 
 
@@ -737,7 +790,7 @@ def run_reference_arm(args):
 # --------------------------------------------------------------------------
 
 def sustained(fn, stream, seconds: float, world: int, local: int, words_per_step: int,
-              ms_per_step: float) -> dict:
+              ms_per_step: float, out=None) -> dict:
     """The same step back to back for ~`seconds` (power-capped steady state),
     timed with CUDA events, max over ranks; clocks sampled throughout.  The
     step count comes from the burst timing (max over ranks), so every rank
@@ -758,8 +811,39 @@ def sustained(fn, stream, seconds: float, world: int, local: int, words_per_step
         torch.cuda.synchronize()
         barrier(world)
     ms = max_over_ranks(e0.elapsed_time(e1), world)
-    return {"value": words_per_step * steps / (ms / 1e3), "steps": steps, "ms_per_step": ms / steps,
-            "clocks": clk.summary()}
+    res = {"value": words_per_step * steps / (ms / 1e3), "steps": steps, "ms_per_step": ms / steps,
+           "clocks": clk.summary()}
+    if out is not None:
+        # the write-only ceilings under the same sustained load: memset (copy
+        # engine, no SM work) and the fill's store shape without the generator
+        nbytes = out.numel() * out.element_size()
+        res["write_ceiling_sustained_gbs"] = {}
+        try:
+            shapes = probe_shapes(out, stream)
+        except OSError:
+            shapes = {}
+        for name in ("memset", "rows_stg64_4w_cap4"):
+            if name not in shapes:
+                continue
+            fn_w = shapes[name]
+            with ClockSampler(local) as wclk:
+                torch.cuda.synchronize()
+                w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                w0.record(stream)
+                for i in range(steps):
+                    fn_w()
+                    if i % 1000 == 999:
+                        torch.cuda.synchronize()
+                w1.record(stream)
+                torch.cuda.synchronize()
+            wms = w0.elapsed_time(w1)
+            res["write_ceiling_sustained_gbs"][name] = {
+                "gbs": nbytes * steps / (wms / 1e3) / 1e9, "clocks": wclk.summary()}
+        best = max((v["gbs"] for v in res["write_ceiling_sustained_gbs"].values()), default=None)
+        if best:
+            res["frac_vs_write_ceiling_sustained"] = (
+                words_per_step / max(world, 1) * out.element_size() * steps / (ms / 1e3) / 1e9 / best)
+    return res
 
 
 def host_api_bench(cb: dict) -> dict:
@@ -910,7 +994,7 @@ def main():
             pass
     if wl == "fill_u32" and args.sustained_s > 0:
         result["sustained"] = sustained(fn, stream, args.sustained_s, world, local, job_words,
-                                        result["ms_per_step"])
+                                        result["ms_per_step"], out=ctx.get("out"))
     # e2e through the public host API (generate into pinned host memory)
     if not args.no_e2e and wl == "fill_u32":
         host = torch.empty((count, per), dtype=torch.uint32, pin_memory=True)
@@ -968,12 +1052,13 @@ def main():
         result["extra_workloads"] = extras
         result["gpu_launches_all"] = result["gpu_launches"] + sum(
             e["gpu_launches"] for e in extras.values())
+    import torch.distributed as dist
+
+    if dist.is_initialized():
+        dist.destroy_process_group()
+    forward_nccl_log()
     if rank == 0:
         print(json.dumps(result), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.destroy_process_group()
     return 0
 
 

@@ -136,6 +136,7 @@ def _bench_cmd(*args, env=None):
     r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), *args], capture_output=True,
                        text=True, timeout=900, env=e, cwd="/tmp")
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    _bench_cmd.stdout = r.stdout
     return r.returncode, (json.loads(lines[-1]) if lines else None), r.stderr
 
 
@@ -233,6 +234,11 @@ def test_bench_default_line_contract():
     rc, line, err = _bench_cmd("--gpus", "1", "--steps", "3", "--warmup", "3", "--sustained-s", "0.3",
                                "--no-cpu")
     assert rc == 0, err[-3000:]
+    # stdout is the one JSON line (NCCL's log is forwarded to stderr)
+    assert _bench_cmd.stdout.strip().count("\n") == 0, _bench_cmd.stdout[:2000]
+    # N = 1 runs the job's collective through a one-rank NCCL communicator
+    assert line["comm"]["backend"] == "nccl" and line["comm"]["nranks"] == 1, line["comm"]
+    assert "NCCL INFO" in err and "nRanks 1" in err
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
               "scaling", "vs_baseline", "dtype", "data", "config", "gpu_launches", "clocks", "roofline",
               "e2e", "parity", "sustained", "extra_workloads"):
@@ -247,6 +253,7 @@ def test_bench_default_line_contract():
         assert e["parity"]["checked"] and e["parity"]["ok"], name
         assert e["roofline"]["frac"] and e["roofline"]["frac"] > 0.5, name
     assert abs(line["extra_workloads"]["mc_pi"]["mc"]["pi_estimate"] - 3.14159265) < 1e-4
+    assert line["extra_workloads"]["mc_pi"]["mc"]["allreduce_in_step"]
     for name in ("fill_f32", "fill_f64", "mc_pi"):
         e2e = line["extra_workloads"][name]["e2e"]
         assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] == 0, name
