@@ -762,7 +762,9 @@ def cpu_baseline_for(wl: str) -> dict:
 
 
 def run_reference_arm(args):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    # under torchrun: WORLD_SIZE ranks, rank 0 measures; without it the job
+    # size is --gpus (the host-side reference does not depend on it)
+    world = int(os.environ.get("WORLD_SIZE", str(max(1, args.gpus))))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
