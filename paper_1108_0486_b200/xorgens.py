@@ -417,25 +417,41 @@ class BlockEnsemble:
                    "generate")
         return out
 
+    def _host_ptr(self, host_out, per_block: int, itemsize: int) -> ctypes.c_void_p:
+        """Address of a caller host buffer (torch CPU tensor or numpy array)
+        that must hold num_blocks * per_block contiguous elements of
+        `itemsize` bytes -- the C ABI takes a bare pointer and cannot check."""
+        if hasattr(host_out, "data_ptr"):
+            ok = (not host_out.is_cuda and host_out.is_contiguous()
+                  and host_out.element_size() == itemsize)
+            n, ptr = host_out.numel(), host_out.data_ptr()
+        else:
+            ok = host_out.flags["C_CONTIGUOUS"] and host_out.itemsize == itemsize
+            n, ptr = host_out.size, host_out.ctypes.data
+        if not ok or n < self._n * per_block:
+            raise ValueError(f"host buffer must be contiguous host memory of at least "
+                             f"{self._n * per_block} elements of {itemsize} bytes")
+        return ctypes.c_void_p(ptr)
+
     def generate_into_host(self, per_block: int, host_out, stream=None) -> None:
-        """generate() into a caller buffer (e.g. a pinned torch tensor)."""
-        ptr = host_out.data_ptr() if hasattr(host_out, "data_ptr") else host_out.ctypes.data
-        _raise(lib.xg_generate_host(self._h.ptr, per_block, ctypes.c_void_p(ptr),
-                                    self._stream(stream)), "generate")
+        """generate() into a caller buffer (e.g. a pinned torch tensor) of
+        uint32 words."""
+        ptr = self._host_ptr(host_out, per_block, 4)
+        _raise(lib.xg_generate_host(self._h.ptr, per_block, ptr, self._stream(stream)), "generate")
 
     def generate_f32_into_host(self, per_block: int, host_out, stream=None) -> None:
         """per_block uniform f32 values of every block into a host buffer
         (block-major), converted on the device."""
-        ptr = host_out.data_ptr() if hasattr(host_out, "data_ptr") else host_out.ctypes.data
-        _raise(lib.xg_generate_host_f32(self._h.ptr, per_block, ctypes.c_void_p(ptr),
-                                        self._stream(stream)), "generate_f32")
+        ptr = self._host_ptr(host_out, per_block, 4)
+        _raise(lib.xg_generate_host_f32(self._h.ptr, per_block, ptr, self._stream(stream)),
+               "generate_f32")
 
     def generate_f64_into_host(self, per_block: int, host_out, stream=None) -> None:
         """per_block uniform f64 values (two words each) of every block into a
         host buffer (block-major), converted on the device."""
-        ptr = host_out.data_ptr() if hasattr(host_out, "data_ptr") else host_out.ctypes.data
-        _raise(lib.xg_generate_host_f64(self._h.ptr, per_block, ctypes.c_void_p(ptr),
-                                        self._stream(stream)), "generate_f64")
+        ptr = self._host_ptr(host_out, per_block, 8)
+        _raise(lib.xg_generate_host_f64(self._h.ptr, per_block, ptr, self._stream(stream)),
+               "generate_f64")
 
     def _fill(self, fn, per_block: int, out, torch_dtype, vals_per_block: int, stream):
         torch = _torch()
@@ -446,6 +462,9 @@ class BlockEnsemble:
             raise ValueError("output buffer too small or not contiguous")
         if out.element_size() != torch.empty(0, dtype=torch_dtype).element_size() or not out.is_cuda:
             raise ValueError(f"output buffer must be a CUDA tensor of {torch_dtype} width")
+        if out.device.index != self._h.device:
+            raise ValueError(f"output buffer is on cuda:{out.device.index}, the ensemble on "
+                             f"cuda:{self._h.device}")
         _raise(fn(self._h.ptr, per_block, ctypes.c_void_p(out.data_ptr()), self._stream(stream)))
         return out
 
@@ -479,6 +498,9 @@ class BlockEnsemble:
         torch = _torch()
         if hits is None:
             hits = torch.zeros(1, dtype=torch.int64, device=f"cuda:{self._h.device}")
+        if (hits.numel() < 1 or hits.element_size() != 8 or not hits.is_cuda
+                or hits.device.index != self._h.device):
+            raise ValueError(f"hits must be an int64 tensor on cuda:{self._h.device}")
         _raise(lib.xg_mc_pi(self._h.ptr, samples_per_block, ctypes.c_void_p(hits.data_ptr()),
                             self._stream(stream)))
         return hits

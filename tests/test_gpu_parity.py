@@ -863,3 +863,26 @@ def test_generate_host_f32_f64_equal_device_fills(oracle):
     h = np.empty((5, 777), dtype=np.float64)
     c.generate_f64_into_host(777, h)
     assert np.array_equal(h.view(np.uint64), o.fill_f64(777).view(np.uint64))
+
+
+def test_host_and_device_buffers_are_checked_before_the_call():
+    """The C ABI takes bare pointers; the Python mirror checks every caller
+    buffer (size, element width, host/device placement) before calling it."""
+    e = xg.BlockEnsemble(GP32, 3, 4, 63)
+    with pytest.raises(ValueError):
+        e.generate_into_host(100, np.empty((4, 99), dtype=np.uint32))      # too small
+    with pytest.raises(ValueError):
+        e.generate_into_host(100, np.empty((4, 100), dtype=np.uint64))     # wrong width
+    with pytest.raises(ValueError):
+        e.generate_f64_into_host(10, np.empty((4, 10), dtype=np.float32))  # wrong width
+    with pytest.raises(ValueError):
+        e.generate_into_host(8, torch.empty((4, 8), dtype=torch.uint32, device="cuda"))  # not host
+    with pytest.raises(ValueError):
+        e.fill_u32(8, out=torch.empty((4, 7), dtype=torch.uint32, device="cuda"))
+    with pytest.raises(ValueError):
+        e.mc_pi(32, hits=torch.zeros(1, dtype=torch.int32, device="cuda"))
+    # nothing was consumed by the rejected calls
+    o = xg.BlockEnsemble(GP32, 3, 4, 63)
+    h = torch.empty((4, 100), dtype=torch.uint32).pin_memory()
+    e.generate_into_host(100, h)
+    assert np.array_equal(h.numpy(), np_u32(o.fill_u32(100)))
