@@ -799,15 +799,19 @@ int xg_berlekamp_massey(const uint32_t* dev_seqs, uint64_t nbits, uint32_t count
                         uint64_t stride_words, uint32_t* dev_L, xg_stream_t stream) {
     if (!dev_seqs || !dev_L || nbits == 0 || nbits > kBmMaxBits) return XG_EINVAL;
     if (count == 0) return XG_OK;
-    if (count > 1 && stride_words * 32 < nbits) return XG_EINVAL;
+    uint64_t stride_bits = 0, span = 0;  // one sequence: the stride is never used
+    if (count > 1 && (mul_overflows(stride_words, 32, &stride_bits) ||
+                      mul_overflows(static_cast<uint64_t>(count - 1), stride_words, &span) ||
+                      stride_bits < nbits))
+        return XG_EINVAL;
     int dev;
     int rc = ptr_device(dev_seqs, &dev);
     if (rc) return rc;
     DeviceGuard dg(dev);
     if (!dg.ok) return XG_ECUDA;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const uint64_t data_words = static_cast<uint64_t>(count - 1) * stride_words + (nbits + 31) / 32;
-    return launch_bm_long(dev_seqs, data_words, nbits, stride_words * 32, count, 0, count, nullptr,
+    const uint64_t data_words = span + (nbits + 31) / 32;
+    return launch_bm_long(dev_seqs, data_words, nbits, stride_bits, count, 0, count, nullptr,
                           dev_L, s);
 }
 
@@ -836,7 +840,9 @@ int xg_lc_words(const uint32_t* dev_words, uint64_t nwords, unsigned block_lengt
     if (!dev_words || !dev_hist || (reinterpret_cast<uintptr_t>(dev_hist) % 8) != 0) return XG_EINVAL;
     if (block_length == 0 || block_length > kBmMaxBits || blocks > 0xffffffffull) return XG_EINVAL;
     if (blocks == 0) return XG_OK;
-    if (nwords * 32 < static_cast<uint64_t>(block_length) * blocks) return XG_EINVAL;
+    uint64_t nbits_in;
+    if (mul_overflows(nwords, 32, &nbits_in)) nbits_in = ~0ull;  // more bits than any request
+    if (nbits_in < static_cast<uint64_t>(block_length) * blocks) return XG_EINVAL;
     int dev;
     int rc = ptr_device(dev_words, &dev);
     if (rc) return rc;
@@ -858,12 +864,14 @@ int xg_pack_words(const uint32_t* dev_in, uint64_t n, unsigned w, int left_align
                   xg_stream_t stream) {
     if (!dev_in || !dev_out || (w != 8 && w != 16 && w != 32)) return XG_EINVAL;
     if (n == 0) return XG_OK;
+    uint64_t nbits;
+    if (mul_overflows(n, w, &nbits) || nbits > ~0ull - 31) return XG_EINVAL;
     int dev;
     int rc = ptr_device(dev_in, &dev);
     if (rc) return rc;
     DeviceGuard dg(dev);
     if (!dg.ok) return XG_ECUDA;
-    const uint64_t nout = left_align ? n : (n * w + 31) / 32;
+    const uint64_t nout = left_align ? n : (nbits + 31) / 32;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((nout + 255) / 256, 8ull * sms));

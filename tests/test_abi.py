@@ -123,6 +123,21 @@ def test_create_validation_order_without_gpu():
     assert lib.xg_fill_u32(None, 10, None, None) == _lib.XG_EINVAL
 
 
+def test_size_overflow_rejected_before_device_work():
+    # Sizes whose byte / bit counts overflow 64 bits are XG_EINVAL up front
+    # (std::invalid_argument in the reference), before any pointer query.
+    lib = _lib.lib
+    fake, out = ctypes.c_void_p(0x1000), ctypes.c_void_p(0x2000)
+    big = 1 << 62
+    assert lib.xg_berlekamp_massey(fake, 64, 2, big, out, None) == _lib.XG_EINVAL  # stride bits
+    assert lib.xg_berlekamp_massey(fake, 64, 3, 1 << 61, out, None) == _lib.XG_EINVAL  # span
+    assert lib.xg_berlekamp_massey(fake, 64, 2, 1, out, None) == _lib.XG_EINVAL  # stride < nbits
+    assert lib.xg_pack_words(fake, 1 << 59, 32, 0, out, None) == _lib.XG_EINVAL
+    assert lib.xg_lc_words(fake, 1, 64, 1, out, None) == _lib.XG_EINVAL  # 32 bits < one block
+    assert lib.xg_digest_u32(fake, 1 << 20, big, out, out, out, None) == _lib.XG_EINVAL
+    assert lib.xg_fill_u32(None, big, None, None) == _lib.XG_EINVAL
+
+
 def test_python_mirror_errors_without_gpu():
     p = xg.xorgensgp32_params()
     with pytest.raises(xg.ParamValidationError):
