@@ -116,6 +116,12 @@ int xg_ensemble_info(xg_ensemble_t h, uint32_t* num_streams, uint64_t* base_seed
 
 /* ---- generation (device buffers, asynchronous) --------------------------- */
 
+/* One-stream calls of >= 2^20 words on a register-window set (w = 32, r = 128,
+ * lane_bound >= 32) are generated as up to 2048 segments in parallel, their
+ * start states computed by GF(2) jump-ahead (csrc/xg_jump.cuh): the same
+ * words, at ensemble speed instead of one warp's.  The first such call per
+ * parameter set and segment length also builds the jump tables (tens of ms). */
+
 /* BlockEnsemble::generate(per_block) (proj/src/parallel.cpp:97-135):
  * dev_out[g * per_stream + k] = word k of stream g, continuing each stream
  * from the handle's state (a second call continues where the first stopped).
@@ -226,7 +232,9 @@ int xg_birthday_duplicates(const uint32_t* dev_words, uint32_t n_draws, uint32_t
  * tests/golden/full_size.json. */
 int xg_digest_u32(const uint32_t* dev_words, uint64_t rows, uint64_t per_row, uint32_t* dev_xor,
                   uint64_t* dev_sum, uint64_t* dev_wsum, xg_stream_t stream);
-/* Advance every stream by `words` without storing (discard). */
+/* Advance every stream by `words` without storing (discard).  On a
+ * one-stream handle of a register-window set, words >= 2^20 jump: O(log words)
+ * GF(2) products by cached powers of the transition matrix, no generation. */
 int xg_skip(xg_ensemble_t h, uint64_t words, xg_stream_t stream);
 
 /* ---- host-facing calls (synchronise) -------------------------------------- */

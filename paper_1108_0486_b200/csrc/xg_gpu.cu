@@ -12,6 +12,8 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <new>
 #include <numeric>
 #include <thread>
@@ -21,6 +23,7 @@
 #include "xg_gpu.h"
 #include "xg_digest.cuh"
 #include "xg_generic.cuh"
+#include "xg_jump.cuh"
 #include "xg_kernels.cuh"
 #include "xg_pairs.cuh"
 #include "xg_stattests.cuh"
@@ -104,6 +107,17 @@ struct xg_ensemble {
     // xg_linear_complexity_test word buffer
     uint32_t* d_lc = nullptr;
     size_t lc_bytes = 0;
+    // jump-ahead scratch (one-stream fills, xg_jump.cuh): segment start
+    // windows + Weyl words, GF(2) partial products, a side stream for the
+    // last (short) segment
+    uint32_t* d_jrows = nullptr;
+    uint32_t* d_jweyl = nullptr;
+    uint32_t* d_jpart = nullptr;
+    uint32_t* d_jW = nullptr;    // the 4096 windows W[i] of a raw run (Krylov form)
+    uint32_t* d_jseq = nullptr;  // that run: 128 + 4096 words
+    uint32_t jrows_cap = 0;
+    cudaStream_t jside = nullptr;
+    cudaEvent_t jev[2] = {};
 };
 
 namespace {
@@ -303,8 +317,8 @@ int launch_gen(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t word
 }
 
 template <int MODE>
-int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t words, void* out,
-                unsigned long long* hits, cudaStream_t s) {
+int launch_fill_direct(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t words, void* out,
+                       unsigned long long* hits, cudaStream_t s) {
     if (words == 0 || g_count == 0) return XG_OK;
     if (h->kind == kGeneric) {
         // The conversions (f32/f64/u64 pairs) and the MC predicate are defined
@@ -337,6 +351,491 @@ int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t wor
         default: return launch_word_lane<MODE>(rt_params<2>(h->params), h, g_begin, g_count, words, out, hits, s);
         }
     }
+}
+
+// ---- jump-ahead (xg_jump.cuh) --------------------------------------------
+//
+// One stream of a register-window set cut into segments: the start window
+// of segment k is s0 G^(kJ) (J = 2^j words, G the one-word transition matrix
+// over GF(2)), its Weyl word weyl + kJ omega; K segments are then generated
+// by one launch of the ordinary kernels as a K-stream ensemble whose rows
+// are consecutive pieces of the output.  Powers G^(2^i) are computed once
+// per (device, parameter set) by repeated squaring and kept for the process.
+
+constexpr uint64_t kJumpMin = 1ull << 20;  // words: below this one warp is faster
+constexpr unsigned kJumpMinLog = 16;       // segments of at least 2^16 words
+constexpr uint32_t kJumpMaxSeg = 2048;     // ... and at most ~2048 of them
+constexpr uint32_t kJCoeffRows = kJumpMaxSeg + 1;  // K full segments + a short last one
+constexpr size_t kJRowBytes = kJWords * sizeof(uint32_t);
+constexpr uint32_t kJPartRows = 16 * 4096;  // partial rows of the largest product (see gf2_mul)
+
+struct JumpPowers {
+    xg_params_t p{};
+    int device = 0;
+    std::vector<uint32_t*> pow;  // pow[i] = G^(2^i): 4096 rows of 128 words on `device`
+    std::vector<cudaEvent_t> ready;
+    uint32_t* part = nullptr;    // partials scratch of the squarings
+    // Krylov form: m(x) = the minimal polynomial of G (degree 4096, found by
+    // Berlekamp-Massey), and per segment length 2^j the rows
+    // C[k] = x^(k 2^j) mod m(x), k < kJCoeffRows, so that the window kJ
+    // words ahead of s_0 is C[k] W with W[i] = the window i raw words ahead.
+    int poly = 0;                // 0 not tried, 1 m(x) known, -1 unavailable
+    std::vector<uint64_t> mlow;  // m(x) - x^4096: 64 words, bit k = coefficient of x^k
+    struct Coeffs {
+        unsigned j = 0;
+        uint32_t* rows = nullptr;
+        cudaEvent_t ready = nullptr;
+    };
+    std::vector<Coeffs> coeffs;
+    std::mutex mu;
+};
+
+std::mutex g_jump_mu;
+std::vector<std::unique_ptr<JumpPowers>> g_jump;  // process lifetime
+
+bool same_params(const xg_params_t& a, const xg_params_t& b) {
+    return a.r == b.r && a.s == b.s && a.a == b.a && a.b == b.b && a.c == b.c && a.d == b.d &&
+           a.w == b.w && a.omega == b.omega && a.gamma == b.gamma;
+}
+
+JumpPowers* jump_powers(const xg_ensemble* h) {
+    std::lock_guard<std::mutex> lk(g_jump_mu);
+    for (auto& j : g_jump)
+        if (j->device == h->device && same_params(j->p, h->params)) return j.get();
+    g_jump.push_back(std::make_unique<JumpPowers>());
+    g_jump.back()->p = h->params;
+    g_jump.back()->device = h->device;
+    return g_jump.back().get();
+}
+
+// G on the host: row i = the window after one raw step from the unit window
+// e_i (bit i % 32 of word i / 32): v = T1(W[0]) ^ T2(W[r - s]), W' = W[1..]
+// ++ v (proj/include/xg/xorgens.hpp:13-18,39-47).
+std::vector<uint32_t> transition_matrix(const xg_params_t& p) {
+    auto xs = [](uint32_t x, unsigned l, unsigned r) {
+        const uint32_t t = x ^ (x << l);
+        return t ^ (t >> r);
+    };
+    const unsigned q = p.r - p.s;
+    std::vector<uint32_t> g(static_cast<size_t>(4096) * kJWords, 0u);
+    for (unsigned i = 0; i < 4096; ++i) {
+        const unsigned j = i / 32;
+        const uint32_t e = 1u << (i % 32);
+        uint32_t* row = g.data() + static_cast<size_t>(i) * kJWords;
+        if (j > 0) row[j - 1] ^= e;
+        if (j == 0) row[kJWords - 1] ^= xs(e, p.a, p.b);
+        if (j == q) row[kJWords - 1] ^= xs(e, p.c, p.d);
+    }
+    return g;
+}
+
+// C = A B over GF(2) (A: rows x 4096, B: 4096 x 4096, row-vector convention);
+// `part` holds ksplit * rows partial rows (<= kJPartRows).
+int gf2_mul(const uint32_t* A, uint32_t rows, const uint32_t* B, uint32_t* C, uint32_t* part,
+            cudaStream_t s) {
+    if (rows == 0) return XG_OK;
+    // k-split: as many ranges as the partials buffer holds (64 up to 512
+    // rows, 8 at 4096); rows per warp: 8 for large products, fewer for the
+    // small ones so that their rows spread over more warps.
+    uint32_t ksplit = 64;
+    while (ksplit > 8 && static_cast<uint64_t>(ksplit) * rows > kJPartRows) ksplit >>= 1;
+    const uint32_t kspan = 4096u / ksplit;
+    auto launch = [&](auto kernel, uint32_t rw) {
+        const dim3 grid((rows + 8 * rw - 1) / (8 * rw), ksplit);
+        kernel<<<grid, 256, 0, s>>>(A, B, part, rows, kspan);
+    };
+    if (rows >= 256) {  // many rows: tables pay for themselves
+        ksplit = 4096u / kM4Span;  // the staged span of B; 16 x 4096 partial rows at most
+        const dim3 grid(4, (rows + 8 * 16 - 1) / (8 * 16), ksplit);
+        static std::atomic<uint64_t> done{0};
+        const int rc = raise_smem_once(gf2_mul_m4rm_kernel<16>, kM4Smem, done);
+        if (rc) return rc;
+        gf2_mul_m4rm_kernel<16><<<grid, 256, kM4Smem, s>>>(A, B, part, rows, 4096u / ksplit);
+    } else if (rows >= 64) {
+        launch(gf2_mul_partial_kernel<2>, 2);
+    } else {
+        launch(gf2_mul_partial_kernel<1>, 1);
+    }
+    const uint64_t n16 = static_cast<uint64_t>(rows) * (kJWords / 4);
+    gf2_reduce_kernel<<<static_cast<unsigned>((n16 + 255) / 256), 256, 0, s>>>(part, C, rows, ksplit);
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    return cuda_rc(cudaGetLastError());
+}
+
+// Make G^(2^i) available for i <= upto (squarings on `s`, once per process)
+// and order `s` after their computation.
+int jump_ensure(JumpPowers* jp, unsigned upto, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(jp->mu);
+    int rc = XG_OK;
+    if (jp->pow.empty()) {
+        const std::vector<uint32_t> g = transition_matrix(jp->p);
+        uint32_t* d = nullptr;
+        rc = cuda_rc(cudaMalloc(&d, g.size() * sizeof(uint32_t)));
+        if (!rc) rc = cuda_rc(cudaMemcpy(d, g.data(), g.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+        if (!rc && !jp->part) rc = cuda_rc(cudaMalloc(&jp->part, static_cast<size_t>(kJPartRows) * kJRowBytes));
+        cudaEvent_t ev = nullptr;
+        if (!rc) rc = cuda_rc(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        if (!rc) rc = cuda_rc(cudaEventRecord(ev, s));
+        if (rc) {
+            cudaFree(d);
+            return rc;
+        }
+        jp->pow.push_back(d);
+        jp->ready.push_back(ev);
+    }
+    while (jp->pow.size() <= upto) {
+        uint32_t* d = nullptr;
+        rc = cuda_rc(cudaMalloc(&d, static_cast<size_t>(4096) * kJRowBytes));
+        if (rc) return rc;
+        cudaStreamWaitEvent(s, jp->ready.back(), 0);
+        rc = gf2_mul(jp->pow.back(), 4096, jp->pow.back(), d, jp->part, s);
+        cudaEvent_t ev = nullptr;
+        if (!rc) rc = cuda_rc(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        if (!rc) rc = cuda_rc(cudaEventRecord(ev, s));
+        if (rc) {
+            cudaFree(d);
+            return rc;
+        }
+        jp->pow.push_back(d);
+        jp->ready.push_back(ev);
+    }
+    // squarings share jp->part: order this stream after the newest one
+    return cuda_rc(cudaStreamWaitEvent(s, jp->ready.back(), 0));
+}
+
+int jump_scratch(xg_ensemble* h, uint32_t rows) {
+    int rc = XG_OK;
+    if (h->jrows_cap < rows) {
+        cudaFree(h->d_jrows);
+        cudaFree(h->d_jweyl);
+        h->d_jrows = nullptr;
+        h->d_jweyl = nullptr;
+        h->jrows_cap = 0;
+        rc = cuda_rc(cudaMalloc(&h->d_jrows, static_cast<size_t>(rows) * kJRowBytes));
+        if (!rc) rc = cuda_rc(cudaMalloc(&h->d_jweyl, static_cast<size_t>(rows) * sizeof(uint32_t)));
+        if (rc) return rc;
+        h->jrows_cap = rows;
+    }
+    // partial rows of a product of at most kJCoeffRows rows (16 k-ranges)
+    if (!h->d_jpart) rc = cuda_rc(cudaMalloc(&h->d_jpart, static_cast<size_t>(16) * kJCoeffRows * kJRowBytes));
+    if (!rc && !h->d_jW) rc = cuda_rc(cudaMalloc(&h->d_jW, static_cast<size_t>(4096) * kJRowBytes));
+    if (!rc && !h->d_jseq) rc = cuda_rc(cudaMalloc(&h->d_jseq, (2 * kJWords + 4096) * sizeof(uint32_t)));
+    if (!rc && !h->jside) rc = cuda_rc(cudaStreamCreateWithFlags(&h->jside, cudaStreamNonBlocking));
+    for (int i = 0; i < 2 && !rc; ++i)
+        if (!h->jev[i]) rc = cuda_rc(cudaEventCreateWithFlags(&h->jev[i], cudaEventDisableTiming));
+    return rc;
+}
+
+unsigned ceil_log2(uint64_t x) {
+    unsigned l = 0;
+    while ((1ull << l) < x) ++l;
+    return l;
+}
+
+// Stream g advanced by `words` (skip: no output) in O(log words) products:
+// s G^words over the set bits of `words`, Weyl + words omega.
+int jump_skip(xg_ensemble* h, uint32_t g, uint64_t words, cudaStream_t s) {
+    JumpPowers* jp = jump_powers(h);
+    int rc = jump_ensure(jp, 63 - static_cast<unsigned>(__builtin_clzll(words)), s);
+    if (!rc) rc = jump_scratch(h, 2);
+    if (rc) return rc;
+    uint32_t* win = h->d_win + static_cast<size_t>(g) * kJWords;
+    uint32_t* a = h->d_jrows;
+    uint32_t* b = h->d_jrows + kJWords;
+    rc = cuda_rc(cudaMemcpyAsync(a, win, kJRowBytes, cudaMemcpyDeviceToDevice, s));
+    for (unsigned i = 0; i < 64 && !rc; ++i) {
+        if (!((words >> i) & 1u)) continue;
+        rc = gf2_mul(a, 1, jp->pow[i], b, h->d_jpart, s);
+        std::swap(a, b);
+    }
+    if (!rc) rc = cuda_rc(cudaMemcpyAsync(win, a, kJRowBytes, cudaMemcpyDeviceToDevice, s));
+    if (rc) return rc;
+    // weyl[g] += words * omega (mod 2^32): one-thread kernel, no host round trip
+    const uint32_t step = static_cast<uint32_t>(words * (h->params.omega & kMask32));
+    jump_weyl_kernel<<<1, 32, 0, s>>>(h->d_weyl + g, h->d_jweyl, 2, step);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    rc = cuda_rc(cudaGetLastError());
+    if (!rc) rc = cuda_rc(cudaMemcpyAsync(h->d_weyl + g, h->d_jweyl + 1, sizeof(uint32_t),
+                                          cudaMemcpyDeviceToDevice, s));
+    return rc;
+}
+
+// ---- Krylov form of the jump (one product per call) ----------------------
+
+constexpr unsigned kPolyWords = 64;                // 4096-bit polynomials as uint64
+
+// The raw (Weyl-free) words of a register-window set from `window`, on the
+// host: x_k = T1(W[0]) ^ T2(W[r - s]), W shifts by one (xorgens.hpp:39-47).
+void host_raw_words(const xg_params_t& p, std::vector<uint32_t> window, size_t n, uint32_t* out) {
+    auto xs = [](uint32_t x, unsigned l, unsigned r) {
+        const uint32_t t = x ^ (x << l);
+        return t ^ (t >> r);
+    };
+    const unsigned q = p.r - p.s;
+    std::vector<uint32_t> w(window.begin(), window.end());
+    w.reserve(window.size() + n);
+    for (size_t k = 0; k < n; ++k) {
+        const uint32_t v = xs(w[k], p.a, p.b) ^ xs(w[k + q], p.c, p.d);
+        w.push_back(v);
+        out[k] = v;
+    }
+}
+
+// Berlekamp-Massey over GF(2): the shortest connection polynomial c
+// (c[0] = 1, b_n = XOR_{i=1..L} c_i b_{n-i}) of the bit sequence; returns L.
+unsigned berlekamp_massey_bits(const std::vector<uint8_t>& b, std::vector<uint8_t>& c) {
+    const size_t n = b.size();
+    c.assign(n + 1, 0);
+    std::vector<uint8_t> bb(n + 1, 0), t;
+    c[0] = bb[0] = 1;
+    unsigned L = 0;
+    size_t m = 1;
+    for (size_t i = 0; i < n; ++i) {
+        uint8_t d = b[i];
+        for (unsigned k = 1; k <= L; ++k) d ^= c[k] & b[i - k];
+        if (!d) {
+            ++m;
+        } else if (2 * L <= i) {
+            t = c;
+            for (size_t k = 0; k + m <= n; ++k) c[k + m] ^= bb[k];
+            L = static_cast<unsigned>(i + 1 - L);
+            bb = t;
+            m = 1;
+        } else {
+            for (size_t k = 0; k + m <= n; ++k) c[k + m] ^= bb[k];
+            ++m;
+        }
+    }
+    return L;
+}
+
+// a <- a x mod m (a: 64 words, degree < 4096)
+void poly_mulx(std::vector<uint64_t>& a, const std::vector<uint64_t>& mlow) {
+    const uint64_t top = a[kPolyWords - 1] >> 63;
+    for (unsigned i = kPolyWords - 1; i > 0; --i) a[i] = (a[i] << 1) | (a[i - 1] >> 63);
+    a[0] <<= 1;
+    if (top)
+        for (unsigned i = 0; i < kPolyWords; ++i) a[i] ^= mlow[i];
+}
+
+// a <- a^2 mod m: spread the bits (no cross terms over GF(2)), then fold every
+// x^i, i >= 4096, as x^(i-4096) (m(x) - x^4096), highest first.
+void poly_sqr(std::vector<uint64_t>& a, const std::vector<uint64_t>& mlow) {
+    std::vector<uint64_t> t(2 * kPolyWords, 0);
+    for (unsigned i = 0; i < kPolyWords; ++i)
+        for (unsigned b = 0; b < 64; ++b)
+            if ((a[i] >> b) & 1u) t[(2 * (64 * i + b)) / 64] |= 1ull << ((2 * b) % 64);
+    for (unsigned i = 2 * 4096 - 1; i >= 4096; --i) {
+        if (!((t[i / 64] >> (i % 64)) & 1u)) continue;
+        t[i / 64] ^= 1ull << (i % 64);
+        const unsigned sh = i - 4096, w = sh / 64, o = sh % 64;
+        for (unsigned k = 0; k < kPolyWords; ++k) {
+            t[w + k] ^= mlow[k] << o;
+            if (o) t[w + k + 1] ^= mlow[k] >> (64 - o);
+        }
+    }
+    a.assign(t.begin(), t.begin() + kPolyWords);
+}
+
+// Find m(x) once per parameter set: Berlekamp-Massey on bit 0 of 8192 raw
+// words, degree 4096 required (then m is G's minimal AND characteristic
+// polynomial, so it annihilates every state), checked on two windows.
+bool find_minpoly(JumpPowers* jp) {
+    std::vector<uint32_t> w0(kJWords);
+    for (unsigned i = 0; i < kJWords; ++i) w0[i] = 0x9e3779b9u * (i + 1) ^ (i << 7);
+    std::vector<uint32_t> x(2 * 4096);
+    host_raw_words(jp->p, w0, x.size(), x.data());
+    std::vector<uint8_t> bits(x.size()), c;
+    for (size_t i = 0; i < x.size(); ++i) bits[i] = x[i] & 1u;
+    const unsigned L = berlekamp_massey_bits(bits, c);
+    if (L != 4096) return false;
+    jp->mlow.assign(kPolyWords, 0);
+    for (unsigned k = 0; k < 4096; ++k)  // m_k = c_(L-k)
+        if (c[L - k]) jp->mlow[k / 64] |= 1ull << (k % 64);
+    // check s_4096 = XOR_(k < 4096, m_k = 1) s_k on two windows
+    for (int trial = 0; trial < 2; ++trial) {
+        std::vector<uint32_t> win(kJWords);
+        for (unsigned i = 0; i < kJWords; ++i) win[i] = trial ? (i * 2654435761u + 12345u) : w0[i];
+        std::vector<uint32_t> seq(win), more(4096);
+        host_raw_words(jp->p, win, more.size(), more.data());
+        seq.insert(seq.end(), more.begin(), more.end());  // seq[i .. i + 128) = s_i
+        std::vector<uint32_t> acc(kJWords, 0);
+        for (unsigned k = 0; k < 4096; ++k)
+            if ((jp->mlow[k / 64] >> (k % 64)) & 1u)
+                for (unsigned j = 0; j < kJWords; ++j) acc[j] ^= seq[k + j];
+        for (unsigned j = 0; j < kJWords; ++j)
+            if (acc[j] != seq[4096 + j]) return false;
+    }
+    return true;
+}
+
+// The matrix of "multiply by p(x) mod m": row i = x^i p mod m, as 4096
+// GF(2) rows of 128 u32 words (bit k = coefficient of x^k).
+void mul_matrix(const std::vector<uint64_t>& p, const std::vector<uint64_t>& mlow, std::vector<uint32_t>& rows) {
+    rows.resize(static_cast<size_t>(4096) * kJWords);
+    std::vector<uint64_t> a(p);
+    for (unsigned i = 0; i < 4096; ++i) {
+        std::memcpy(rows.data() + static_cast<size_t>(i) * kJWords, a.data(), kJRowBytes);
+        poly_mulx(a, mlow);
+    }
+}
+
+// C rows for segment length 2^j (once per parameter set and j): C[0] = 1,
+// C[2^l .. 2^(l+1)) = C[0 .. 2^l) (x^(2^(j+l)) mod m) by products with the
+// multiplication matrices, on `s`.  Called with jp->mu held.
+int build_coeffs(JumpPowers* jp, unsigned j, cudaStream_t s, uint32_t** out) {
+    for (auto& c : jp->coeffs)
+        if (c.j == j) {
+            *out = c.rows;
+            return cuda_rc(cudaStreamWaitEvent(s, c.ready, 0));
+        }
+    JumpPowers::Coeffs c;
+    c.j = j;
+    int rc = cuda_rc(cudaMalloc(&c.rows, static_cast<size_t>(kJCoeffRows) * kJRowBytes));
+    uint32_t* dmat = nullptr;
+    if (!rc) rc = cuda_rc(cudaMalloc(&dmat, static_cast<size_t>(4096) * kJRowBytes));
+    uint32_t* part = nullptr;  // own partials: squarings may be running on another stream
+    if (!rc) rc = cuda_rc(cudaMalloc(&part, static_cast<size_t>(kJPartRows) * kJRowBytes));
+    std::vector<uint32_t> one(kJWords, 0);
+    one[0] = 1u;
+    if (!rc) rc = cuda_rc(cudaMemcpyAsync(c.rows, one.data(), kJRowBytes, cudaMemcpyHostToDevice, s));
+    std::vector<uint64_t> p(kPolyWords, 0);
+    p[0] = 2u;  // x
+    for (unsigned i = 0; i < j; ++i) poly_sqr(p, jp->mlow);  // x^(2^j)
+    std::vector<uint32_t> rows;
+    for (unsigned l = 0; !rc && (1u << l) < kJCoeffRows; ++l) {
+        mul_matrix(p, jp->mlow, rows);
+        // synchronous upload: the previous level's product must be done with dmat
+        rc = cuda_rc(cudaStreamSynchronize(s));
+        if (!rc) rc = cuda_rc(cudaMemcpy(dmat, rows.data(), rows.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+        const uint32_t have = 1u << l, n = std::min(have, kJCoeffRows - have);
+        if (!rc) rc = gf2_mul(c.rows, n, dmat, c.rows + static_cast<size_t>(have) * kJWords, part, s);
+        poly_sqr(p, jp->mlow);
+    }
+    if (!rc) rc = cuda_rc(cudaStreamSynchronize(s));
+    cudaFree(dmat);
+    cudaFree(part);
+    if (!rc) rc = cuda_rc(cudaEventCreateWithFlags(&c.ready, cudaEventDisableTiming));
+    if (!rc) rc = cuda_rc(cudaEventRecord(c.ready, s));
+    if (rc) {
+        cudaFree(c.rows);
+        return rc;
+    }
+    jp->coeffs.push_back(c);
+    *out = c.rows;
+    return XG_OK;
+}
+
+// The C rows for 2^j-word segments of this parameter set, or nullptr when
+// the set has no degree-4096 minimal polynomial (the doubling path then).
+int jump_coeffs(JumpPowers* jp, unsigned j, cudaStream_t s, uint32_t** out) {
+    std::lock_guard<std::mutex> lk(jp->mu);
+    *out = nullptr;
+    if (jp->poly == 0) jp->poly = find_minpoly(jp) ? 1 : -1;
+    if (jp->poly < 0) return XG_OK;
+    return build_coeffs(jp, j, s, out);
+}
+
+// Element offset of word `k` of a stream's output for MODE.
+template <int MODE>
+void* out_at(void* out, uint64_t k) {
+    if constexpr (MODE == kU32 || MODE == kRaw || MODE == kF32) return static_cast<uint32_t*>(out) + k;
+    else if constexpr (MODE == kWide) return static_cast<uint64_t*>(out) + k;
+    else if constexpr (MODE == kF64) return static_cast<double*>(out) + k / 2;
+    else return out;
+}
+
+// Stream g, `words` words, generated as K segments of J = 2^j words (plus a
+// shorter last one on a side stream), continuing stream g exactly.
+template <int MODE>
+int jump_fill(xg_ensemble* h, uint32_t g, uint64_t words, void* out, unsigned long long* hits,
+              cudaStream_t s) {
+    if constexpr (MODE == kSkip) {
+        return jump_skip(h, g, words, s);
+    } else {
+        const unsigned j = std::max(kJumpMinLog, ceil_log2((words + kJumpMaxSeg - 1) / kJumpMaxSeg));
+        const uint64_t J = 1ull << j;
+        const uint32_t K = static_cast<uint32_t>(words >> j);
+        const uint64_t rem = words - static_cast<uint64_t>(K) * J;
+        const uint32_t cnt = K + (rem ? 1u : 0u);
+        const unsigned levels = ceil_log2(cnt);
+        JumpPowers* jp = jump_powers(h);
+        uint32_t* coeffs = nullptr;
+        int rc = jump_coeffs(jp, j, s, &coeffs);
+        if (!rc) rc = jump_scratch(h, cnt);
+        if (rc) return rc;
+        uint32_t* win = h->d_win + static_cast<size_t>(g) * kJWords;
+        if (coeffs) {
+            // Krylov form, one product: S[k] = C[k] W, W[i] = the window i raw
+            // words ahead of s_0 = seq[i .. i + 128) of a 4096-word raw run.
+            rc = cuda_rc(cudaMemcpyAsync(h->d_jseq, win, kJRowBytes, cudaMemcpyDeviceToDevice, s));
+            if (!rc) rc = cuda_rc(cudaMemcpyAsync(h->d_jseq + kJWords + 4096, win, kJRowBytes,
+                                                  cudaMemcpyDeviceToDevice, s));
+            xg_ensemble gen = *h;  // a one-stream view over a copy of s_0
+            gen.d_win = h->d_jseq + kJWords + 4096;
+            gen.d_weyl = h->d_jweyl;
+            gen.num_streams = 1;
+            if (!rc) rc = launch_fill_direct<kRaw>(&gen, 0, 1, 4096, h->d_jseq + kJWords, nullptr, s);
+            if (!rc) {
+                jump_windows_kernel<<<4096 * kJWords / 256, 256, 0, s>>>(h->d_jseq, h->d_jW);
+                g_launches.fetch_add(1, std::memory_order_relaxed);
+                rc = cuda_rc(cudaGetLastError());
+            }
+            if (!rc) rc = gf2_mul(coeffs, cnt, h->d_jW, h->d_jrows, h->d_jpart, s);
+        } else {
+            // doubling: rows [2^l, 2^(l+1)) = rows [0, 2^l) G^(J 2^l)
+            rc = jump_ensure(jp, j + (levels ? levels - 1 : 0), s);
+            if (!rc) rc = cuda_rc(cudaMemcpyAsync(h->d_jrows, win, kJRowBytes, cudaMemcpyDeviceToDevice, s));
+            for (unsigned l = 0; l < levels && !rc; ++l) {
+                const uint32_t have = 1u << l;
+                const uint32_t n = std::min(have, cnt - have);
+                rc = gf2_mul(h->d_jrows, n, jp->pow[j + l], h->d_jrows + static_cast<size_t>(have) * kJWords,
+                             h->d_jpart, s);
+            }
+        }
+        if (rc) return rc;
+        // Raw (Weyl-ablated) fills leave the accumulator alone.
+        const uint32_t step = MODE == kRaw ? 0u : static_cast<uint32_t>(J * (h->params.omega & kMask32));
+        jump_weyl_kernel<<<(cnt + 255) / 256, 256, 0, s>>>(h->d_weyl + g, h->d_jweyl, cnt, step);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        rc = cuda_rc(cudaGetLastError());
+        if (rc) return rc;
+        // the segments as an ensemble of cnt streams over the scratch state
+        xg_ensemble view = *h;
+        view.d_win = h->d_jrows;
+        view.d_weyl = h->d_jweyl;
+        view.num_streams = cnt;
+        if (rem) {  // the short last segment concurrently on the side stream
+            rc = cuda_rc(cudaEventRecord(h->jev[0], s));
+            if (!rc) rc = cuda_rc(cudaStreamWaitEvent(h->jside, h->jev[0], 0));
+            if (!rc)
+                rc = launch_fill_direct<MODE>(&view, K, 1, rem, out_at<MODE>(out, static_cast<uint64_t>(K) * J),
+                                              hits, h->jside);
+            if (!rc) rc = cuda_rc(cudaEventRecord(h->jev[1], h->jside));
+        }
+        if (!rc && K) rc = launch_fill_direct<MODE>(&view, 0, K, J, out, hits, s);
+        if (!rc && rem) rc = cuda_rc(cudaStreamWaitEvent(s, h->jev[1], 0));
+        if (rc) return rc;
+        // stream g continues from the end of the last segment
+        rc = cuda_rc(cudaMemcpyAsync(h->d_win + static_cast<size_t>(g) * kJWords,
+                                     h->d_jrows + static_cast<size_t>(cnt - 1) * kJWords, kJRowBytes,
+                                     cudaMemcpyDeviceToDevice, s));
+        if (!rc)
+            rc = cuda_rc(cudaMemcpyAsync(h->d_weyl + g, h->d_jweyl + cnt - 1, sizeof(uint32_t),
+                                         cudaMemcpyDeviceToDevice, s));
+        return rc;
+    }
+}
+
+// Every generation call goes through here: one stream of a register-window
+// set and at least kJumpMin words take the jump-ahead path, everything else
+// the kernels directly.
+template <int MODE>
+int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t words, void* out,
+                unsigned long long* hits, cudaStream_t s) {
+    if (g_count == 1 && words >= kJumpMin && h->kind != kGeneric)
+        return jump_fill<MODE>(h, g_begin, words, out, hits, s);
+    return launch_fill_direct<MODE>(h, g_begin, g_count, words, out, hits, s);
 }
 
 // Raise the dynamic shared-memory limit of the pair kernels once, at
@@ -421,6 +920,14 @@ void free_handle(xg_ensemble* h) {
         cudaFree(h->d_stage);
         cudaFreeHost(h->h_stage);
         cudaFree(h->d_lc);
+        cudaFree(h->d_jrows);
+        cudaFree(h->d_jweyl);
+        cudaFree(h->d_jpart);
+        cudaFree(h->d_jW);
+        cudaFree(h->d_jseq);
+        if (h->jside) cudaStreamDestroy(h->jside);
+        for (int i = 0; i < 2; ++i)
+            if (h->jev[i]) cudaEventDestroy(h->jev[i]);
     }
     delete h;
 }
