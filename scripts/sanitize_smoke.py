@@ -89,3 +89,16 @@ assert xg._lib.lib.xg_lc_words(w2.data_ptr(), w2.numel(), 128, 40, hist.data_ptr
 torch.cuda.synchronize()
 assert int(cnt.sum()) == 17 and int(hist.sum()) == 40
 print("sanitize round-2 host tiles / f32-f64 host / word-buffer tests ok")
+
+# jump-ahead (csrc/xg_jump.cuh): one-stream fills >= 2^20 words (Krylov
+# product, four-Russians and dense GF(2) kernels, side-stream last segment)
+# on two parameter kinds (the 4096-row squarings of a jump skip are left to
+# the parity tests: hours under racecheck)
+for jp in (p, xg.GeneratorParams(128, 33, 11, 7, 9, 19, 32, 0x6A09E667 | 1, 11)):
+    op = o.params(jp.r, jp.s, jp.a, jp.b, jp.c, jp.d, jp.w, jp.omega, jp.gamma)
+    ej = xg.BlockEnsemble(jp, 21, 1, xg.lane_bound(jp))
+    n = (1 << 20) + 4099
+    assert np.array_equal(ej.fill_u32(n).cpu().numpy()[0], o.stream(21, n, op))
+    assert np.array_equal(ej.fill_u32(64).cpu().numpy()[0], o.stream(21, n + 64, op)[-64:])
+torch.cuda.synchronize()
+print("sanitize jump-ahead ok")
