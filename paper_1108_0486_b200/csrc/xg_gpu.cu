@@ -364,7 +364,10 @@ int launch_fill_direct(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint6
 
 constexpr uint64_t kJumpMin = 1ull << 20;  // words: below this one warp is faster
 constexpr unsigned kJumpMinLog = 16;       // segments of at least 2^16 words
-constexpr uint32_t kJumpMaxSeg = 2048;     // ... and at most ~2048 of them
+#ifndef XG_JUMP_MAX_SEG
+#define XG_JUMP_MAX_SEG 1024
+#endif
+constexpr uint32_t kJumpMaxSeg = XG_JUMP_MAX_SEG;  // ... and at most 1024 of them (A/B: 512 / 1024 / 2048)
 constexpr uint32_t kJCoeffRows = kJumpMaxSeg + 1;  // K full segments + a short last one
 constexpr size_t kJRowBytes = kJWords * sizeof(uint32_t);
 constexpr uint32_t kJPartRows = 16 * 4096;  // partial rows of the largest product (see gf2_mul)
@@ -432,8 +435,9 @@ std::vector<uint32_t> transition_matrix(const xg_params_t& p) {
 // C = A B over GF(2) (A: rows x 4096, B: 4096 x 4096, row-vector convention);
 // `part` holds ksplit * rows partial rows (<= kJPartRows).
 int gf2_mul(const uint32_t* A, uint32_t rows, const uint32_t* B, uint32_t* C, uint32_t* part,
-            cudaStream_t s) {
+            cudaStream_t s, uint32_t ldb = kJWords) {
     if (rows == 0) return XG_OK;
+    if (ldb != kJWords && rows < 256) return XG_EINVAL;  // strided B: four-Russians kernel only
     // k-split: as many ranges as the partials buffer holds (64 up to 512
     // rows, 8 at 4096); rows per warp: 8 for large products, fewer for the
     // small ones so that their rows spread over more warps.
@@ -450,7 +454,7 @@ int gf2_mul(const uint32_t* A, uint32_t rows, const uint32_t* B, uint32_t* C, ui
         static std::atomic<uint64_t> done{0};
         const int rc = raise_smem_once(gf2_mul_m4rm_kernel<16>, kM4Smem, done);
         if (rc) return rc;
-        gf2_mul_m4rm_kernel<16><<<grid, 256, kM4Smem, s>>>(A, B, part, rows, 4096u / ksplit);
+        gf2_mul_m4rm_kernel<16><<<grid, 256, kM4Smem, s>>>(A, B, part, rows, 4096u / ksplit, ldb);
     } else if (rows >= 64) {
         launch(gf2_mul_partial_kernel<2>, 2);
     } else {
@@ -776,12 +780,14 @@ int jump_fill(xg_ensemble* h, uint32_t g, uint64_t words, void* out, unsigned lo
             gen.d_weyl = h->d_jweyl;
             gen.num_streams = 1;
             if (!rc) rc = launch_fill_direct<kRaw>(&gen, 0, 1, 4096, h->d_jseq + kJWords, nullptr, s);
-            if (!rc) {
+            if (!rc && cnt >= 256) {  // the four-Russians kernel reads the windows in place
+                rc = gf2_mul(coeffs, cnt, h->d_jseq, h->d_jrows, h->d_jpart, s, 1);
+            } else if (!rc) {
                 jump_windows_kernel<<<4096 * kJWords / 256, 256, 0, s>>>(h->d_jseq, h->d_jW);
                 g_launches.fetch_add(1, std::memory_order_relaxed);
                 rc = cuda_rc(cudaGetLastError());
+                if (!rc) rc = gf2_mul(coeffs, cnt, h->d_jW, h->d_jrows, h->d_jpart, s);
             }
-            if (!rc) rc = gf2_mul(coeffs, cnt, h->d_jW, h->d_jrows, h->d_jpart, s);
         } else {
             // doubling: rows [2^l, 2^(l+1)) = rows [0, 2^l) G^(J 2^l)
             rc = jump_ensure(jp, j + (levels ? levels - 1 : 0), s);
@@ -827,14 +833,22 @@ int jump_fill(xg_ensemble* h, uint32_t g, uint64_t words, void* out, unsigned lo
     }
 }
 
-// Every generation call goes through here: one stream of a register-window
-// set and at least kJumpMin words take the jump-ahead path, everything else
-// the kernels directly.
+// Every generation call goes through here.  Few streams of a register-window
+// set with many words each take the jump-ahead path stream by stream (one
+// warp per stream would run at 2.3e9 RN/s; a jump costs ~0.1 ms): up to 64
+// streams, at least 2^20 words per stream per stream in the call.  Everything
+// else runs the kernels directly.
 template <int MODE>
 int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t words, void* out,
                 unsigned long long* hits, cudaStream_t s) {
-    if (g_count == 1 && words >= kJumpMin && h->kind != kGeneric)
-        return jump_fill<MODE>(h, g_begin, words, out, hits, s);
+    if (h->kind != kGeneric && g_count <= 64 && words >= kJumpMin &&
+        words >= static_cast<uint64_t>(g_count) * kJumpMin) {
+        int rc = XG_OK;
+        for (uint32_t i = 0; i < g_count && !rc; ++i)
+            rc = jump_fill<MODE>(h, g_begin + i, words, out_at<MODE>(out, static_cast<uint64_t>(i) * words), hits,
+                                 s);
+        return rc;
+    }
     return launch_fill_direct<MODE>(h, g_begin, g_count, words, out, hits, s);
 }
 

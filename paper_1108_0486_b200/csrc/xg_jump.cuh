@@ -92,13 +92,15 @@ gf2_mul_partial_kernel(const uint32_t* __restrict__ A, const uint32_t* __restric
 // k-split range of kspan <= 256 rows of B); its slab of B and its rows' bits
 // of A are staged in shared memory first, so the group loop touches no
 // global memory; lane = word of the slab, so a lookup is one conflict-free
-// LDS.32 per warp.  grid (4, ceil(rows / (8 RW)), ksplit).
+// LDS.32 per warp.  Row k of B starts at B + k ldb (ldb = 128 for a matrix,
+// 1 for the overlapping windows of a raw run, which then need no expansion).
+// grid (4, ceil(rows / (8 RW)), ksplit).
 constexpr int kM4Span = 256;  // max kspan of the four-Russians kernel
 constexpr size_t kM4Smem = (256 + kM4Span) * 32 * sizeof(uint32_t);  // table + staged B
 template <int RW>
 __global__ void __launch_bounds__(256)
 gf2_mul_m4rm_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict__ B,
-                    uint32_t* __restrict__ part, uint32_t rows, uint32_t kspan) {
+                    uint32_t* __restrict__ part, uint32_t rows, uint32_t kspan, uint32_t ldb) {
     extern __shared__ uint32_t m4_dyn[];           // kM4Smem bytes (dynamic, > 48 KB)
     uint32_t(*T)[32] = reinterpret_cast<uint32_t(*)[32]>(m4_dyn);                 // [256][32]
     uint32_t(*Bsl)[32] = reinterpret_cast<uint32_t(*)[32]>(m4_dyn + 256 * 32);    // B rows k0.., this slab
@@ -112,11 +114,11 @@ gf2_mul_m4rm_kernel(const uint32_t* __restrict__ A, const uint32_t* __restrict__
     if (kspan == kM4Span) {
         uint32_t v[kM4Span / 8];
 #pragma unroll
-        for (int i = 0; i < kM4Span / 8; ++i) v[i] = B[static_cast<size_t>(k0 + warp + 8 * i) * kJWords + col];
+        for (int i = 0; i < kM4Span / 8; ++i) v[i] = B[static_cast<size_t>(k0 + warp + 8 * i) * ldb + col];
 #pragma unroll
         for (int i = 0; i < kM4Span / 8; ++i) Bsl[warp + 8 * i][lane] = v[i];
     } else {
-        for (unsigned i = warp; i < kspan; i += 8) Bsl[i][lane] = B[static_cast<size_t>(k0 + i) * kJWords + col];
+        for (unsigned i = warp; i < kspan; i += 8) Bsl[i][lane] = B[static_cast<size_t>(k0 + i) * ldb + col];
     }
     {
         constexpr int kAn = (8 * RW * (kM4Span / 32) + 255) / 256;

@@ -98,13 +98,29 @@ def test_jump_skip_far_is_consistent():
 
 
 def test_jump_matches_the_multistream_kernels(oracle):
-    """A 2-stream ensemble takes the direct path: its stream 0 must equal the
-    1-stream (jump) fill of the same seed at 2^25 words."""
-    n = 1 << 25
+    """An ensemble of 65 streams takes the direct path (one warp per stream):
+    its stream 0 must equal the one-stream (jump) fill of the same seed."""
+    n = (1 << 21) + 384
     a = host(one(1234).fill_u32(n))[0]
-    b = host(xg.BlockEnsemble(GP32, 1234, 2, 63).fill_u32(n))[0]
+    b = host(xg.BlockEnsemble(GP32, 1234, 65, 63).fill_u32(n))[0]
     assert np.array_equal(a, b)
     assert np.array_equal(a[:M], oracle.stream(1234, M))
+
+
+def test_jump_few_streams_each_jumped(oracle):
+    """Up to 64 streams with >= 2^20 words each are jumped stream by stream:
+    block-major rows, every mode's row offsets, continuation."""
+    P, n = 3, M + 4099
+    e = xg.BlockEnsemble(GP32, 40, P, 63)
+    o = oracle.ensemble(40, P)
+    assert np.array_equal(host(e.fill_u32(n)), o.fill_u32(n))
+    assert np.array_equal(host(e.fill_f64(M + 1)).view(np.uint64), o.fill_f64(M + 1).view(np.uint64))
+    assert int(e.mc_pi(M).item()) == int(o.mc_hits(M).sum())
+    e.skip(2 * M + 7)
+    o.fill_u32(2 * M + 7)
+    assert np.array_equal(host(e.fill_u32(100)), o.fill_u32(100))
+    g = e.generate(2 * M)
+    assert np.array_equal(g, o.fill_u32(2 * M))
 
 
 @pytest.mark.parametrize("ps", [
