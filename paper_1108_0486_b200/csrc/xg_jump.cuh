@@ -204,4 +204,10 @@ __global__ void jump_weyl_kernel(const uint32_t* __restrict__ w0, uint32_t* __re
     if (k < n) out[k] = w0[0] + k * step;
 }
 
+// w[k] += step (mod 2^32), k < n: the Weyl words of skipped streams.
+__global__ void jump_weyl_add_kernel(uint32_t* __restrict__ w, uint32_t n, uint32_t step) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) w[k] += step;
+}
+
 }  // namespace xgk

@@ -41,13 +41,18 @@ for n in [1 << 20, 1 << 22, 10**8, 1 << 28, 1 << 30]:
     ms = timed(lambda: e.fill_u32(n, out=out), reps)
     res[f"jump_fill_u32 n={n}"] = {"ms": ms, "rn_per_s": n / (ms / 1e3)}
     del out
-# one warp (direct path): a 2-stream ensemble, per-stream rate
-d = xg.BlockEnsemble(p, 1, 2, 63)
+# one warp (direct path): a 65-stream ensemble (more than the 64 streams the
+# jump takes), per-stream rate
+d = xg.BlockEnsemble(p, 1, 65, 63)
 n = 1 << 22
-out = torch.empty((2, n), dtype=torch.uint32, device="cuda")
+out = torch.empty((65, n), dtype=torch.uint32, device="cuda")
 d.fill_u32(n, out=out)
 ms = timed(lambda: d.fill_u32(n, out=out), 5)
-res["direct one warp (2-stream ensemble / 2), n=2^22"] = {"ms": ms, "rn_per_s": n / (ms / 1e3)}
+res["direct one warp (65-stream ensemble / 65), n=2^22"] = {"ms": ms, "rn_per_s": n / (ms / 1e3)}
+# a batch skip: 2^14 streams jump 2^22 words (generating them: ~25 ms)
+b = xg.BlockEnsemble(p, 1, 1 << 14, 63)
+b.skip(1 << 22)
+res["skip(2^22) of 2^14 streams (batch jump), ms"] = timed(lambda: b.skip(1 << 22), 5)
 del out
 f = xg.BlockEnsemble(p, 1, 1, 63)
 t0 = time.perf_counter()

@@ -175,3 +175,25 @@ def test_bench_stream1_parity_and_rate():
 
     res = bench.parity_check("stream1", 1, 0, 0)
     assert res["checked"] and res["ok"], res
+
+
+def test_jump_skip_many_streams(oracle):
+    """More than 64 streams skipping >= 2^22 words jump as a batch (rows times
+    G^(2^i) in chunks of 1024): sampled streams against the oracle, and a
+    2^30 skip of 2000 streams against one-stream skips (other kernels:
+    four-Russians rows vs the dense single-row product)."""
+    P, n = 100, (1 << 22) + 3
+    e = xg.BlockEnsemble(GP32, 600, P, 63)
+    e.skip(n)
+    got = host(e.fill_u32(1000))
+    for g in (0, 50, P - 1):
+        assert np.array_equal(got[g], oracle.stream(600 + g, n + 1000)[n:]), g
+    P, n = 2000, 1 << 30
+    e = xg.BlockEnsemble(GP32, 9000, P, 63)
+    e.skip(n)
+    got = host(e.fill_u32(256))
+    for g in (0, 1023, 1024, P - 1):
+        s = one(9000 + g)
+        s.skip(n)
+        assert np.array_equal(got[g], host(s.fill_u32(256))[0]), g
+    assert e.block_state(P - 1)[1] == (one(9000 + P - 1).block_state(0)[1] + (n + 256) * GP32.omega) % (1 << 32)
