@@ -1021,7 +1021,9 @@ def main():
         result["sustained"] = sustained(fn, stream, args.sustained_s, world, local, job_words,
                                         result["ms_per_step"], out=ctx.get("out"))
     # e2e through the public host API (generate into pinned host memory)
-    if not args.no_e2e and wl == "fill_u32":
+    if not args.no_e2e and wl in ("fill_u32", "stream1"):
+        # (stream1: ONE generator's 10^8 words into host memory -- the
+        # reference's XorgensSource loop, served by the jump-ahead path)
         host = torch.empty((count, per), dtype=torch.uint32, pin_memory=True)
         e2e_steps = max(3, min(args.steps, 5))
         ens.generate_into_host(per, host)

@@ -306,6 +306,17 @@ int xg_state_import(xg_ensemble_t h, uint32_t index, const uint64_t* buffer, uin
 int xg_state_export_all(xg_ensemble_t h, uint32_t* host_window, uint32_t* host_weyl);
 int xg_state_import_all(xg_ensemble_t h, const uint32_t* host_window, const uint32_t* host_weyl);
 
+/* ---- jump-ahead support (host only, no GPU) ------------------------------ */
+
+/* The minimal polynomial m(x) of a register-window set's one-word transition
+ * over GF(2) -- the polynomial the jump-ahead path reduces x^n by
+ * (csrc/xg_jump.cuh): Berlekamp-Massey over the raw stream, degree 4096
+ * required and checked.  coeffs64[k / 64] bit k % 64 = coefficient of x^k for
+ * k < 4096 (64 words; the x^4096 term is implied).  XG_EUNSUPPORTED for the
+ * general-parameter sets or a degree below 4096 (jumps then use powers of
+ * the transition matrix). */
+int xg_jump_minpoly(const xg_params_t* p, uint64_t* coeffs64);
+
 /* ---- multi-GPU partitioner (host only) ----------------------------------- */
 
 /* Contiguous, balanced split of global streams [0, total) over `world`

@@ -89,6 +89,7 @@ SIGNATURES = {
     "xg_state_import": (_int, [_vp, _u32, _P(_u64), _u64]),
     "xg_state_export_all": (_int, [_vp, _vp, _vp]),
     "xg_state_import_all": (_int, [_vp, _vp, _vp]),
+    "xg_jump_minpoly": (_int, [_P(xg_params_t), _P(_u64)]),
     "xg_partition": (_int, [_u64, _u32, _u32, _P(_u64), _P(_u32)]),
     "xg_kernel_launches": (_u64, []),
     "xg_build_info": (ctypes.c_char_p, []),

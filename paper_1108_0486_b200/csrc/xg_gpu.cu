@@ -645,34 +645,36 @@ void poly_sqr(std::vector<uint64_t>& a, const std::vector<uint64_t>& mlow) {
 // Find m(x) once per parameter set: Berlekamp-Massey on bit 0 of 8192 raw
 // words, degree 4096 required (then m is G's minimal AND characteristic
 // polynomial, so it annihilates every state), checked on two windows.
-bool find_minpoly(JumpPowers* jp) {
+bool minpoly_of(const xg_params_t& p, std::vector<uint64_t>& mlow) {
     std::vector<uint32_t> w0(kJWords);
     for (unsigned i = 0; i < kJWords; ++i) w0[i] = 0x9e3779b9u * (i + 1) ^ (i << 7);
     std::vector<uint32_t> x(2 * 4096);
-    host_raw_words(jp->p, w0, x.size(), x.data());
+    host_raw_words(p, w0, x.size(), x.data());
     std::vector<uint8_t> bits(x.size()), c;
     for (size_t i = 0; i < x.size(); ++i) bits[i] = x[i] & 1u;
     const unsigned L = berlekamp_massey_bits(bits, c);
     if (L != 4096) return false;
-    jp->mlow.assign(kPolyWords, 0);
+    mlow.assign(kPolyWords, 0);
     for (unsigned k = 0; k < 4096; ++k)  // m_k = c_(L-k)
-        if (c[L - k]) jp->mlow[k / 64] |= 1ull << (k % 64);
+        if (c[L - k]) mlow[k / 64] |= 1ull << (k % 64);
     // check s_4096 = XOR_(k < 4096, m_k = 1) s_k on two windows
     for (int trial = 0; trial < 2; ++trial) {
         std::vector<uint32_t> win(kJWords);
         for (unsigned i = 0; i < kJWords; ++i) win[i] = trial ? (i * 2654435761u + 12345u) : w0[i];
         std::vector<uint32_t> seq(win), more(4096);
-        host_raw_words(jp->p, win, more.size(), more.data());
+        host_raw_words(p, win, more.size(), more.data());
         seq.insert(seq.end(), more.begin(), more.end());  // seq[i .. i + 128) = s_i
         std::vector<uint32_t> acc(kJWords, 0);
         for (unsigned k = 0; k < 4096; ++k)
-            if ((jp->mlow[k / 64] >> (k % 64)) & 1u)
+            if ((mlow[k / 64] >> (k % 64)) & 1u)
                 for (unsigned j = 0; j < kJWords; ++j) acc[j] ^= seq[k + j];
         for (unsigned j = 0; j < kJWords; ++j)
             if (acc[j] != seq[4096 + j]) return false;
     }
     return true;
 }
+
+bool find_minpoly(JumpPowers* jp) { return minpoly_of(jp->p, jp->mlow); }
 
 // The matrix of "multiply by p(x) mod m": row i = x^i p mod m, as 4096
 // GF(2) rows of 128 u32 words (bit k = coefficient of x^k).
@@ -1942,6 +1944,18 @@ int xg_state_import_all(xg_ensemble_t h, const uint32_t* host_window, const uint
     if (!rc) rc = cuda_rc(cudaMemcpy(h->d_win, host_window, n * kR * 4, cudaMemcpyHostToDevice));
     if (!rc) rc = cuda_rc(cudaMemcpy(h->d_weyl, host_weyl, n * 4, cudaMemcpyHostToDevice));
     return rc;
+}
+
+int xg_jump_minpoly(const xg_params_t* p, uint64_t* coeffs64) {
+    if (!p || !coeffs64) return XG_EINVAL;
+    Kind kind;
+    int e = classify(p, &kind);
+    if (e) return e;
+    if (kind == kGeneric) return XG_EUNSUPPORTED;
+    std::vector<uint64_t> m;
+    if (!minpoly_of(*p, m)) return XG_EUNSUPPORTED;
+    std::memcpy(coeffs64, m.data(), kPolyWords * sizeof(uint64_t));
+    return XG_OK;
 }
 
 int xg_partition(uint64_t total_streams, uint32_t world, uint32_t rank, uint64_t* first,
