@@ -44,7 +44,7 @@ METRIC = "RN/s (32-bit, device-timed) at 1/2/4/8 B200; % of HBM write BW"
 FULL_SIZE = os.path.join(ROOT, "tests", "golden", "full_size.json")
 CHUNK = 1 << 14  # streams per golden chunk
 WORKLOADS = ["fill_u32", "fill_f32", "fill_f64", "fill_2p34", "mc_pi", "skip", "stream1", "rank", "lc"]
-EXTRA = ("fill_f32", "fill_f64", "fill_2p34", "mc_pi")
+EXTRA = ("fill_f32", "fill_f64", "fill_2p34", "mc_pi", "stream1")
 
 
 def load_peaks():
@@ -930,6 +930,22 @@ def extra_e2e(wl: str, ens, fn, ctx, world: int, rank: int) -> dict:
         return {"value": job_words * steps / dt, "unit": "RN/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 8, "steps": steps,
                 "api": "BlockEnsemble.mc_pi (+ NCCL all-reduce at N > 1) -> hit count read back"}
+    if wl == "stream1":
+        # ONE generator's 10^8 words into pinned host memory (what a user of
+        # the reference's XorgensState loop gets), jump-ahead on the device
+        host = torch.empty((count, per), dtype=torch.uint32, pin_memory=True)
+        ens.generate_into_host(per, host)
+        barrier(world)
+        t = time.perf_counter()
+        steps = 3
+        for _ in range(steps):
+            ens.generate_into_host(per, host)
+        dt = max_over_ranks(time.perf_counter() - t, world)
+        del host
+        return {"value": job_words * steps / dt, "unit": "RN/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": count * per * 4, "steps": steps,
+                "api": "XorgensState stream -> BlockEnsemble.generate -> xg_generate_host (pinned host "
+                       "buffer; one stream, jump-ahead segments)"}
     return {"value": None, "why": "the 2^34-word output (64 GiB per job) is not copied to the host"}
 
 

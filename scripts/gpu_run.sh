@@ -25,5 +25,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"pai
   -o $OUT/prof_mc_pi python bench.py --workload mc_pi --steps 1 --warmup 3 --no-cpu > /dev/null 2>> $OUT/ncu.err
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"digest_kernel" -c 1 \
   -o $OUT/prof_digest python bench.py --workload fill_u32 --steps 1 --warmup 3 --no-cpu --no-e2e --sustained-s 0 > /dev/null 2>> $OUT/ncu.err
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gf2_mul_m4rm" -s 2 -c 1 \
+  -o $OUT/prof_jump_m4rm python bench.py --workload stream1 --steps 2 --warmup 3 --no-cpu --no-e2e > /dev/null 2>> $OUT/ncu.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_stream1.csv \
+  python scripts/jump_profile.py 100000000 > /dev/null 2>> $OUT/ncu.err
 for f in $OUT/prof_*.ncu-rep; do python scripts/ncu_summary.py $f > ${f%.ncu-rep}.json 2>> $OUT/ncu.err; done
 echo done > $OUT/DONE
