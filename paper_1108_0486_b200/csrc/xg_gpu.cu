@@ -389,6 +389,7 @@ struct JumpPowers {
         unsigned j = 0;
         uint32_t* rows = nullptr;
         cudaEvent_t ready = nullptr;
+        bool done = false;  // `ready` seen complete: later calls need no wait
     };
     std::vector<Coeffs> coeffs;
     std::mutex mu;
@@ -694,7 +695,11 @@ int build_coeffs(JumpPowers* jp, unsigned j, cudaStream_t s, uint32_t** out) {
     for (auto& c : jp->coeffs)
         if (c.j == j) {
             *out = c.rows;
-            return cuda_rc(cudaStreamWaitEvent(s, c.ready, 0));
+            if (!c.done) {
+                c.done = cudaEventQuery(c.ready) == cudaSuccess;
+                if (!c.done) cudaGetLastError();  // cudaErrorNotReady is not a failure
+            }
+            return c.done ? XG_OK : cuda_rc(cudaStreamWaitEvent(s, c.ready, 0));
         }
     JumpPowers::Coeffs c;
     c.j = j;
@@ -772,15 +777,20 @@ int jump_fill(xg_ensemble* h, uint32_t g, uint64_t words, void* out, unsigned lo
         if (!rc) rc = jump_scratch(h, cnt);
         if (rc) return rc;
         uint32_t* win = h->d_win + static_cast<size_t>(g) * kJWords;
+        // Raw (Weyl-ablated) fills leave the accumulator alone.
+        const uint32_t step = MODE == kRaw ? 0u : static_cast<uint32_t>(J * (h->params.omega & kMask32));
+        const uint32_t nb = (std::max<uint32_t>(cnt, kJWords) + 255) / 256;
         if (coeffs) {
             // Krylov form, one product: S[k] = C[k] W, W[i] = the window i raw
-            // words ahead of s_0 = seq[i .. i + 128) of a 4096-word raw run.
-            rc = cuda_rc(cudaMemcpyAsync(h->d_jseq, win, kJRowBytes, cudaMemcpyDeviceToDevice, s));
-            if (!rc) rc = cuda_rc(cudaMemcpyAsync(h->d_jseq + kJWords + 4096, win, kJRowBytes,
-                                                  cudaMemcpyDeviceToDevice, s));
-            xg_ensemble gen = *h;  // a one-stream view over a copy of s_0
+            // words ahead of s_0 = seq[i .. i + 128) of a 4096-word raw run
+            // (s_0 also seeds the raw run's own state slot, seq + 128 + 4096).
+            jump_begin_kernel<<<nb, 256, 0, s>>>(win, h->d_weyl + g, h->d_jseq, h->d_jseq + kJWords + 4096,
+                                                 h->d_jweyl, cnt, step);
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            rc = cuda_rc(cudaGetLastError());
+            xg_ensemble gen = *h;  // a one-stream view over the copy of s_0
             gen.d_win = h->d_jseq + kJWords + 4096;
-            gen.d_weyl = h->d_jweyl;
+            gen.d_weyl = h->d_jweyl;  // read, not advanced, by a raw fill
             gen.num_streams = 1;
             if (!rc) rc = launch_fill_direct<kRaw>(&gen, 0, 1, 4096, h->d_jseq + kJWords, nullptr, s);
             if (!rc && cnt >= 256) {  // the four-Russians kernel reads the windows in place
@@ -794,7 +804,12 @@ int jump_fill(xg_ensemble* h, uint32_t g, uint64_t words, void* out, unsigned lo
         } else {
             // doubling: rows [2^l, 2^(l+1)) = rows [0, 2^l) G^(J 2^l)
             rc = jump_ensure(jp, j + (levels ? levels - 1 : 0), s);
-            if (!rc) rc = cuda_rc(cudaMemcpyAsync(h->d_jrows, win, kJRowBytes, cudaMemcpyDeviceToDevice, s));
+            if (!rc) {
+                jump_begin_kernel<<<nb, 256, 0, s>>>(win, h->d_weyl + g, h->d_jrows, nullptr, h->d_jweyl, cnt,
+                                                     step);
+                g_launches.fetch_add(1, std::memory_order_relaxed);
+                rc = cuda_rc(cudaGetLastError());
+            }
             for (unsigned l = 0; l < levels && !rc; ++l) {
                 const uint32_t have = 1u << l;
                 const uint32_t n = std::min(have, cnt - have);
@@ -802,12 +817,6 @@ int jump_fill(xg_ensemble* h, uint32_t g, uint64_t words, void* out, unsigned lo
                              h->d_jpart, s);
             }
         }
-        if (rc) return rc;
-        // Raw (Weyl-ablated) fills leave the accumulator alone.
-        const uint32_t step = MODE == kRaw ? 0u : static_cast<uint32_t>(J * (h->params.omega & kMask32));
-        jump_weyl_kernel<<<(cnt + 255) / 256, 256, 0, s>>>(h->d_weyl + g, h->d_jweyl, cnt, step);
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        rc = cuda_rc(cudaGetLastError());
         if (rc) return rc;
         // the segments as an ensemble of cnt streams over the scratch state
         xg_ensemble view = *h;
@@ -826,13 +835,10 @@ int jump_fill(xg_ensemble* h, uint32_t g, uint64_t words, void* out, unsigned lo
         if (!rc && rem) rc = cuda_rc(cudaStreamWaitEvent(s, h->jev[1], 0));
         if (rc) return rc;
         // stream g continues from the end of the last segment
-        rc = cuda_rc(cudaMemcpyAsync(h->d_win + static_cast<size_t>(g) * kJWords,
-                                     h->d_jrows + static_cast<size_t>(cnt - 1) * kJWords, kJRowBytes,
-                                     cudaMemcpyDeviceToDevice, s));
-        if (!rc)
-            rc = cuda_rc(cudaMemcpyAsync(h->d_weyl + g, h->d_jweyl + cnt - 1, sizeof(uint32_t),
-                                         cudaMemcpyDeviceToDevice, s));
-        return rc;
+        jump_end_kernel<<<1, kJWords, 0, s>>>(h->d_jrows + static_cast<size_t>(cnt - 1) * kJWords,
+                                              h->d_jweyl + cnt - 1, win, h->d_weyl + g);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return cuda_rc(cudaGetLastError());
     }
 }
 

@@ -197,11 +197,27 @@ jump_windows_kernel(const uint32_t* __restrict__ seq, uint32_t* __restrict__ W) 
     W[t] = seq[(t >> 7) + (t & 127u)];
 }
 
-// Segment Weyl words: out[k] = w0[0] + k * step (mod 2^32), k < n.
-__global__ void jump_weyl_kernel(const uint32_t* __restrict__ w0, uint32_t* __restrict__ out, uint32_t n,
-                                 uint32_t step) {
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < n) out[k] = w0[0] + k * step;
+// Start of a jump fill, one launch: the source window (128 words) copied to
+// dst_a and, if given, dst_b; the segment Weyl words wout[k] = w0[0] + k step
+// (mod 2^32), k < n.
+__global__ void __launch_bounds__(256)
+jump_begin_kernel(const uint32_t* __restrict__ win, const uint32_t* __restrict__ w0, uint32_t* __restrict__ dst_a,
+                  uint32_t* __restrict__ dst_b, uint32_t* __restrict__ wout, uint32_t n, uint32_t step) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < kJWords) {
+        const uint32_t v = win[t];
+        dst_a[t] = v;
+        if (dst_b) dst_b[t] = v;
+    }
+    if (t < n) wout[t] = w0[0] + t * step;
+}
+
+// End of a jump fill: the stream continues from the last segment's state.
+__global__ void jump_end_kernel(const uint32_t* __restrict__ win, const uint32_t* __restrict__ w,
+                                uint32_t* __restrict__ dst_win, uint32_t* __restrict__ dst_w) {
+    const uint32_t t = threadIdx.x;  // 128 threads
+    dst_win[t] = win[t];
+    if (t == 0) dst_w[0] = w[0];
 }
 
 // w[k] += step (mod 2^32), k < n: the Weyl words of skipped streams.
