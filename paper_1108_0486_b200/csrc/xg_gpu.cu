@@ -410,6 +410,10 @@ JumpPowers* jump_powers(const xg_ensemble* h) {
     g_jump.push_back(std::make_unique<JumpPowers>());
     g_jump.back()->p = h->params;
     g_jump.back()->device = h->device;
+    // pow[i] is read without the lock once jump_ensure has returned: never
+    // reallocate (i < 64 always)
+    g_jump.back()->pow.reserve(64);
+    g_jump.back()->ready.reserve(64);
     return g_jump.back().get();
 }
 

@@ -197,3 +197,38 @@ def test_jump_skip_many_streams(oracle):
         s.skip(n)
         assert np.array_equal(got[g], host(s.fill_u32(256))[0]), g
     assert e.block_state(P - 1)[1] == (one(9000 + P - 1).block_state(0)[1] + (n + 256) * GP32.omega) % (1 << 32)
+
+
+def test_jump_from_two_host_threads(oracle):
+    """Two one-stream handles of the same parameter set on two host threads
+    and two CUDA streams share the process-wide jump tables: each gets the
+    reference's words (fills and long skips, so the powers grow meanwhile)."""
+    import threading
+
+    out, errs = {}, []
+
+    def work(seed):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                e = one(seed)
+                a = e.fill_u32(3 * M + 11, stream=st)
+                e.skip((1 << 33) + seed, stream=st)
+                b = e.fill_u32(512, stream=st)
+                st.synchronize()
+                out[seed] = (a.cpu().numpy()[0], b.cpu().numpy()[0])
+        except Exception as ex:  # noqa: BLE001
+            errs.append(ex)
+
+    th = [threading.Thread(target=work, args=(s,)) for s in (70, 71)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for seed in (70, 71):
+        assert np.array_equal(out[seed][0], oracle.stream(seed, 3 * M + 11))
+        ref = one(seed)
+        ref.skip(3 * M + 11)
+        ref.skip((1 << 33) + seed)
+        assert np.array_equal(out[seed][1], host(ref.fill_u32(512))[0])
