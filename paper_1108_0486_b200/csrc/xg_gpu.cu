@@ -846,25 +846,74 @@ int jump_fill(xg_ensemble* h, uint32_t g, uint64_t words, void* out, unsigned lo
     }
 }
 
-// Every generation call goes through here.  Few streams of a register-window
-// set with many words each take the jump-ahead path stream by stream (one
-// warp per stream would run at 2.3e9 RN/s; a jump costs ~0.1 ms): up to 64
-// streams, at least 2^20 words per stream per stream in the call.  Everything
-// else runs the kernels directly.
+// More streams than the per-stream path takes (65 .. 512) with a power-of-two
+// length: every stream cut into Q = 2^q segments of J = words / Q >= 2^16
+// (P Q <= kJumpMaxSeg), the P Q start windows by doubling over q with the
+// cached powers -- all streams of a level in one product -- then ONE fill of
+// the P Q segments as an ensemble whose rows are the output rows' pieces.
+template <int MODE>
+int jump_fill_many(xg_ensemble* h, uint32_t g0, uint32_t P, uint64_t words, void* out,
+                   unsigned long long* hits, cudaStream_t s) {
+    uint32_t Q = 1;
+    while (2 * Q * P <= kJumpMaxSeg && (words / (2 * Q)) >= (1ull << kJumpMinLog)) Q *= 2;
+    if (Q < 2) return launch_fill_direct<MODE>(h, g0, P, words, out, hits, s);
+    const uint64_t J = words / Q;
+    const unsigned j = 63 - static_cast<unsigned>(__builtin_clzll(J)), lq = ceil_log2(Q);
+    JumpPowers* jp = jump_powers(h);
+    int rc = jump_ensure(jp, j + lq - 1, s);
+    if (!rc) rc = jump_scratch(h, P * Q);
+    if (rc) return rc;
+    rc = cuda_rc(cudaMemcpyAsync(h->d_jrows, h->d_win + static_cast<size_t>(g0) * kJWords,
+                                 static_cast<size_t>(P) * kJRowBytes, cudaMemcpyDeviceToDevice, s));
+    for (unsigned l = 0; l < lq && !rc; ++l) {  // rows [P 2^l, P 2^(l+1)) = rows [0, P 2^l) G^(J 2^l)
+        const uint32_t have = P << l;
+        rc = gf2_mul(h->d_jrows, have, jp->pow[j + l], h->d_jrows + static_cast<size_t>(have) * kJWords,
+                     h->d_jpart, s);
+    }
+    if (rc) return rc;
+    const uint32_t step = MODE == kRaw ? 0u : static_cast<uint32_t>(J * (h->params.omega & kMask32));
+    jump_permute_kernel<<<(P * Q * 32 + 255) / 256, 256, 0, s>>>(h->d_jrows, h->d_jW, h->d_weyl + g0,
+                                                               h->d_jweyl, P, Q, step);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    rc = cuda_rc(cudaGetLastError());
+    xg_ensemble view = *h;
+    view.d_win = h->d_jW;
+    view.d_weyl = h->d_jweyl;
+    view.num_streams = P * Q;
+    if (!rc) rc = launch_fill_direct<MODE>(&view, 0, P * Q, J, out, hits, s);
+    if (rc) return rc;
+    jump_finish_many_kernel<<<(P * 32 + 255) / 256, 256, 0, s>>>(h->d_jW, h->d_jweyl,
+                                                                 h->d_win + static_cast<size_t>(g0) * kJWords,
+                                                                 h->d_weyl + g0, P, Q);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cuda_rc(cudaGetLastError());
+}
+
+// Every generation call goes through here; the jump-ahead paths where one
+// warp per stream would leave the GPU idle (xg_jump.cuh), else the kernels
+// directly:
+//   skip of >= 2^20 words (more than 64 streams: >= 2^22)     -> jump_skip, O(log n)
+//   one stream, >= 2^20 words                                  -> jump_fill (Krylov)
+//   2 .. 512 streams, a power-of-two length >= 2^20            -> jump_fill_many
+//   <= 64 streams, >= 2^20 words each per stream in the call    -> jump_fill per stream
 template <int MODE>
 int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t words, void* out,
                 unsigned long long* hits, cudaStream_t s) {
-    // A long skip of many streams: one batch of products per chunk of rows
-    // (skip of 2^22 words: ~0.3 ms for 2^14 streams against ~25 ms generated).
-    if (MODE == kSkip && h->kind != kGeneric && g_count > 64 && words >= kJumpSkipMany)
-        return jump_skip(h, g_begin, g_count, words, s);
-    if (h->kind != kGeneric && g_count <= 64 && words >= kJumpMin &&
-        words >= static_cast<uint64_t>(g_count) * kJumpMin) {
-        int rc = XG_OK;
-        for (uint32_t i = 0; i < g_count && !rc; ++i)
-            rc = jump_fill<MODE>(h, g_begin + i, words, out_at<MODE>(out, static_cast<uint64_t>(i) * words), hits,
-                                 s);
-        return rc;
+    if (h->kind == kGeneric || words < kJumpMin || g_count == 0)
+        return launch_fill_direct<MODE>(h, g_begin, g_count, words, out, hits, s);
+    if constexpr (MODE == kSkip) {
+        if (g_count <= 64 || words >= kJumpSkipMany) return jump_skip(h, g_begin, g_count, words, s);
+    } else {
+        if (g_count == 1) return jump_fill<MODE>(h, g_begin, words, out, hits, s);
+        if (2 * g_count <= kJumpMaxSeg && (words & (words - 1)) == 0)
+            return jump_fill_many<MODE>(h, g_begin, g_count, words, out, hits, s);
+        if (g_count <= 64 && words >= static_cast<uint64_t>(g_count) * kJumpMin) {
+            int rc = XG_OK;
+            for (uint32_t i = 0; i < g_count && !rc; ++i)
+                rc = jump_fill<MODE>(h, g_begin + i, words, out_at<MODE>(out, static_cast<uint64_t>(i) * words),
+                                     hits, s);
+            return rc;
+        }
     }
     return launch_fill_direct<MODE>(h, g_begin, g_count, words, out, hits, s);
 }

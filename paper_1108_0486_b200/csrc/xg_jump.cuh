@@ -220,6 +220,35 @@ __global__ void jump_end_kernel(const uint32_t* __restrict__ win, const uint32_t
     if (t == 0) dst_w[0] = w[0];
 }
 
+// Many streams, Q segments each (jump_fill_many): the jumped windows come
+// q-major (row q P + g, so each doubling level is one contiguous product);
+// the fill wants them g-major (row g Q + q: segment q of stream g, output at
+// g words + q J).  dst[g Q + q] = src[q P + g], wout[g Q + q] = w[g] + q step.
+// One warp per row, 16 bytes per lane.
+__global__ void __launch_bounds__(256)
+jump_permute_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, const uint32_t* __restrict__ w,
+                    uint32_t* __restrict__ wout, uint32_t P, uint32_t Q, uint32_t step) {
+    const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
+    if (row >= P * Q) return;
+    const uint32_t g = row / Q, q = row % Q;
+    reinterpret_cast<uint4*>(dst + static_cast<size_t>(row) * kJWords)[lane] =
+        reinterpret_cast<const uint4*>(src + (static_cast<size_t>(q) * P + g) * kJWords)[lane];
+    if (lane == 0) wout[row] = w[g] + q * step;
+}
+
+// ... and after the fill every stream continues from its last segment:
+// win[g] = rows[g Q + Q - 1], weyl[g] = wrows[g Q + Q - 1].
+__global__ void __launch_bounds__(256)
+jump_finish_many_kernel(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ wrows,
+                        uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32_t P, uint32_t Q) {
+    const uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
+    if (g >= P) return;
+    const size_t last = static_cast<size_t>(g) * Q + Q - 1;
+    reinterpret_cast<uint4*>(win + static_cast<size_t>(g) * kJWords)[lane] =
+        reinterpret_cast<const uint4*>(rows + last * kJWords)[lane];
+    if (lane == 0) weyl[g] = wrows[last];
+}
+
 // w[k] += step (mod 2^32), k < n: the Weyl words of skipped streams.
 __global__ void jump_weyl_add_kernel(uint32_t* __restrict__ w, uint32_t n, uint32_t step) {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;

@@ -232,3 +232,21 @@ def test_jump_from_two_host_threads(oracle):
         ref.skip(3 * M + 11)
         ref.skip((1 << 33) + seed)
         assert np.array_equal(out[seed][1], host(ref.fill_u32(512))[0])
+
+
+@pytest.mark.parametrize("P,n", [(100, 1 << 21), (512, 1 << 20), (65, 1 << 22)])
+def test_jump_many_streams_power_of_two(oracle, P, n):
+    """65 .. 512 streams with a power-of-two length: every stream cut into Q
+    segments (doubling over q for all streams at once), one fill of P Q
+    segments -- block-major rows, continuation, f64 and MC modes."""
+    e = xg.BlockEnsemble(GP32, 300, P, 63)
+    o = oracle.ensemble(300, P)
+    assert np.array_equal(host(e.fill_u32(n)), o.fill_u32(n))
+    assert np.array_equal(host(e.fill_u32(1000)), o.fill_u32(1000))  # state continued
+    if P == 100:
+        assert np.array_equal(host(e.fill_f64(n // 2)).view(np.uint64), o.fill_f64(n // 2).view(np.uint64))
+        assert int(e.mc_pi(n // 2).item()) == int(o.mc_hits(n // 2).sum())
+        assert np.array_equal(host(e.fill_raw_u32(n)), o.fill_raw_u32(n))
+    for g in (0, P - 1):
+        buf, wy = e.block_state(g)
+        assert wy == o.weyl(g) and np.array_equal(np.array(buf, dtype=np.uint64), o.logical_buffer(g))
