@@ -116,11 +116,15 @@ int xg_ensemble_info(xg_ensemble_t h, uint32_t* num_streams, uint64_t* base_seed
 
 /* ---- generation (device buffers, asynchronous) --------------------------- */
 
-/* One-stream calls of >= 2^20 words on a register-window set (w = 32, r = 128,
- * lane_bound >= 32) are generated as up to 2048 segments in parallel, their
- * start states computed by GF(2) jump-ahead (csrc/xg_jump.cuh): the same
- * words, at ensemble speed instead of one warp's.  The first such call per
- * parameter set and segment length also builds the jump tables (tens of ms). */
+/* Calls of >= 2^20 words on few streams of a register-window set (w = 32,
+ * r = 128, lane_bound >= 32) -- one stream; 2 .. 512 streams of a
+ * power-of-two length; up to 64 streams of any length -- are generated as up
+ * to 1024 segments in parallel, their start states computed by GF(2)
+ * jump-ahead (csrc/xg_jump.cuh): the same words, at ensemble speed instead of
+ * one warp per stream.  The first such call per parameter set and segment
+ * length builds the jump tables on the calling stream and synchronises it
+ * (tens of ms); capture such calls into CUDA graphs only after a first
+ * eager call. */
 
 /* BlockEnsemble::generate(per_block) (proj/src/parallel.cpp:97-135):
  * dev_out[g * per_stream + k] = word k of stream g, continuing each stream
