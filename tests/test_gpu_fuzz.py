@@ -170,3 +170,49 @@ def test_random_single_stream_sequence(oracle, name):
             assert np.array_equal(np.array(st.logical_buffer(), dtype=np.uint64), o.logical_buffer(0)), tag
             assert st.weyl_value() == o.weyl(0), tag
         assert pos < 2600000 - 80000
+
+
+@pytest.mark.parametrize("name", list(SETS))
+def test_random_sequence_with_jumps(oracle, name):
+    """The same walk with long calls mixed in: >= 2^20-word calls on 1, 2, 3
+    or 8 streams take the jump-ahead paths (one stream: Krylov product;
+    power-of-two lengths: Q segments per stream; other lengths on <= 64
+    streams: stream by stream; skips: batch products), interleaved with the
+    direct kernels, into aligned and misaligned views -- bit-exact after
+    every call and in the final states."""
+    rng = np.random.default_rng(99 + len(name))
+    r, s, a, b, c, d, w, omega, gamma = SETS[name]
+    p = xg.GeneratorParams(r, s, a, b, c, d, w, omega, gamma)
+    streams = int(rng.choice([1, 2, 3, 8]))
+    base = int(rng.integers(0, 2**63))
+    e = xg.BlockEnsemble(p, base, streams, 32)
+    o = oracle.ensemble(base, streams, oracle.params(r, s, a, b, c, d, w, omega, gamma))
+    M = 1 << 20
+    for step in range(16):
+        kind = int(rng.integers(3))
+        n = (int(rng.integers(1, 700)) if kind == 0 else
+             (M << int(rng.integers(2))) if kind == 1 else M + int(rng.integers(1, 5000)))
+        op = ["u32", "f32", "f64", "mc", "skip", "host"][int(rng.integers(6))]
+        mis = bool(rng.integers(2))
+        tag = f"{name} streams {streams} step {step}: {op}({n}, misaligned={mis})"
+        if op == "u32":
+            got = _host(e.fill_u32(n, out=_view(streams, n, torch.uint32, mis)))
+            assert np.array_equal(got, o.fill_u32(n)), tag
+        elif op == "f32":
+            got = _host(e.fill_f32(n, out=_view(streams, n, torch.float32, mis)))
+            assert np.array_equal(got.view(np.uint32), o.fill_f32(n).view(np.uint32)), tag
+        elif op == "f64":
+            got = _host(e.fill_f64(n, out=_view(streams, n, torch.float64, mis)))
+            assert np.array_equal(got.view(np.uint64), o.fill_f64(n).view(np.uint64)), tag
+        elif op == "mc":
+            k = 32 * max(1, n // 64)
+            assert int(_host(e.mc_pi(k))[0]) == int(o.mc_hits(k).sum()), tag
+        elif op == "skip":
+            e.skip(n)
+            o.fill_u32(n)
+        else:
+            assert np.array_equal(e.generate(n), o.fill_u32(n)), tag
+    for g in range(streams):
+        buf, wy = e.block_state(g)
+        assert np.array_equal(np.array(buf, dtype=np.uint32), o.logical_buffer(g).astype(np.uint32))
+        assert wy == o.weyl(g)
