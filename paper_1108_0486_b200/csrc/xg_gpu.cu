@@ -1,10 +1,14 @@
 // xg_gpu.cu -- host side of libxg_gpu.so: the C ABI declared in
-// include/xg_gpu.h over the sm_100a kernels in xg_kernels.cuh.
+// include/xg_gpu.h over the sm_100a kernels (xg_pairs.cuh, xg_kernels.cuh,
+// xg_generic.cuh, xg_jump.cuh, xg_stattests.cuh, xg_digest.cuh).
 //
 // Host validation mirrors the reference exactly (check order and error
 // classes of proj/src/params.cpp:22-37 and proj/src/parallel.cpp:84-95); all
 // generator arithmetic runs on the device.  There is no CPU fallback: a call
-// without a usable CUDA device returns XG_ECUDA.
+// without a usable CUDA device returns XG_ECUDA.  (The host computes only the
+// jump-ahead tables' polynomial algebra -- Berlekamp-Massey over 8192 bits of
+// a 4096-bit recurrence and squarings mod m(x), once per parameter set; every
+// output word is generated on the device.)
 #include <cuda_runtime.h>
 
 #include <algorithm>
