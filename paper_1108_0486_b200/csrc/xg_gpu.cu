@@ -6,9 +6,9 @@
 // classes of proj/src/params.cpp:22-37 and proj/src/parallel.cpp:84-95); all
 // generator arithmetic runs on the device.  There is no CPU fallback: a call
 // without a usable CUDA device returns XG_ECUDA.  (The host computes only the
-// jump-ahead tables' polynomial algebra -- Berlekamp-Massey over 8192 bits of
-// a 4096-bit recurrence and squarings mod m(x), once per parameter set; every
-// output word is generated on the device.)
+// jump-ahead tables' polynomial algebra -- Berlekamp-Massey over 8192 bits the
+// device generated, squarings mod m(x) -- once per parameter set; every word
+// is generated on the device.)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -580,6 +580,8 @@ constexpr unsigned kPolyWords = 64;                // 4096-bit polynomials as ui
 
 // The raw (Weyl-free) words of a register-window set from `window`, on the
 // host: x_k = T1(W[0]) ^ T2(W[r - s]), W shifts by one (xorgens.hpp:39-47).
+// Only the host-only analysis call xg_jump_minpoly uses it; the jump path
+// takes the same words from the device (find_minpoly).
 void host_raw_words(const xg_params_t& p, std::vector<uint32_t> window, size_t n, uint32_t* out) {
     auto xs = [](uint32_t x, unsigned l, unsigned r) {
         const uint32_t t = x ^ (x << l);
@@ -654,15 +656,21 @@ void poly_sqr(std::vector<uint64_t>& a, const std::vector<uint64_t>& mlow) {
 // Find m(x) once per parameter set: Berlekamp-Massey on bit 0 of 8192 raw
 // words, degree 4096 required (then m is G's minimal AND characteristic
 // polynomial, so it annihilates every state), checked on two windows.
-bool minpoly_of(const xg_params_t& p, std::vector<uint64_t>& mlow) {
+// `raw(window, n, out)` produces the n raw (Weyl-free) words that follow a
+// 128-word window: on the device for the jump path (find_minpoly), on the
+// host only for the xg_jump_minpoly analysis call.
+template <class Raw>
+int minpoly_of(Raw raw, std::vector<uint64_t>& mlow, bool* ok) {
+    *ok = false;
     std::vector<uint32_t> w0(kJWords);
     for (unsigned i = 0; i < kJWords; ++i) w0[i] = 0x9e3779b9u * (i + 1) ^ (i << 7);
     std::vector<uint32_t> x(2 * 4096);
-    host_raw_words(p, w0, x.size(), x.data());
+    int rc = raw(w0, x.size(), x.data());
+    if (rc) return rc;
     std::vector<uint8_t> bits(x.size()), c;
     for (size_t i = 0; i < x.size(); ++i) bits[i] = x[i] & 1u;
     const unsigned L = berlekamp_massey_bits(bits, c);
-    if (L != 4096) return false;
+    if (L != 4096) return XG_OK;
     mlow.assign(kPolyWords, 0);
     for (unsigned k = 0; k < 4096; ++k)  // m_k = c_(L-k)
         if (c[L - k]) mlow[k / 64] |= 1ull << (k % 64);
@@ -671,19 +679,41 @@ bool minpoly_of(const xg_params_t& p, std::vector<uint64_t>& mlow) {
         std::vector<uint32_t> win(kJWords);
         for (unsigned i = 0; i < kJWords; ++i) win[i] = trial ? (i * 2654435761u + 12345u) : w0[i];
         std::vector<uint32_t> seq(win), more(4096);
-        host_raw_words(p, win, more.size(), more.data());
+        rc = raw(win, more.size(), more.data());
+        if (rc) return rc;
         seq.insert(seq.end(), more.begin(), more.end());  // seq[i .. i + 128) = s_i
         std::vector<uint32_t> acc(kJWords, 0);
         for (unsigned k = 0; k < 4096; ++k)
             if ((mlow[k / 64] >> (k % 64)) & 1u)
                 for (unsigned j = 0; j < kJWords; ++j) acc[j] ^= seq[k + j];
         for (unsigned j = 0; j < kJWords; ++j)
-            if (acc[j] != seq[4096 + j]) return false;
+            if (acc[j] != seq[4096 + j]) return XG_OK;
     }
-    return true;
+    *ok = true;
+    return XG_OK;
 }
 
-bool find_minpoly(JumpPowers* jp) { return minpoly_of(jp->p, jp->mlow); }
+// m(x) of the handle's parameter set from raw words generated on the device
+// (a one-stream view over scratch: 128-word state slot + output), on `s`.
+int find_minpoly(JumpPowers* jp, xg_ensemble* h, cudaStream_t s, bool* ok) {
+    uint32_t* d = nullptr;  // [128 state][8192 output][1 weyl]
+    int rc = cuda_rc(cudaMalloc(&d, (kJWords + 2 * 4096 + 1) * sizeof(uint32_t)));
+    if (rc) return rc;
+    auto raw = [&](const std::vector<uint32_t>& window, size_t n, uint32_t* out) {
+        xg_ensemble gen = *h;
+        gen.d_win = d;
+        gen.d_weyl = d + kJWords + 2 * 4096;  // read, not advanced, by a raw fill
+        gen.num_streams = 1;
+        int e = cuda_rc(cudaMemcpyAsync(d, window.data(), kJRowBytes, cudaMemcpyHostToDevice, s));
+        if (!e) e = launch_fill_direct<kRaw>(&gen, 0, 1, n, d + kJWords, nullptr, s);
+        if (!e) e = cuda_rc(cudaMemcpyAsync(out, d + kJWords, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        if (!e) e = cuda_rc(cudaStreamSynchronize(s));
+        return e;
+    };
+    rc = minpoly_of(raw, jp->mlow, ok);
+    cudaFree(d);
+    return rc;
+}
 
 // The matrix of "multiply by p(x) mod m": row i = x^i p mod m, as 4096
 // GF(2) rows of 128 u32 words (bit k = coefficient of x^k).
@@ -748,10 +778,15 @@ int build_coeffs(JumpPowers* jp, unsigned j, cudaStream_t s, uint32_t** out) {
 
 // The C rows for 2^j-word segments of this parameter set, or nullptr when
 // the set has no degree-4096 minimal polynomial (the doubling path then).
-int jump_coeffs(JumpPowers* jp, unsigned j, cudaStream_t s, uint32_t** out) {
+int jump_coeffs(JumpPowers* jp, xg_ensemble* h, unsigned j, cudaStream_t s, uint32_t** out) {
     std::lock_guard<std::mutex> lk(jp->mu);
     *out = nullptr;
-    if (jp->poly == 0) jp->poly = find_minpoly(jp) ? 1 : -1;
+    if (jp->poly == 0) {
+        bool ok = false;
+        const int rc = find_minpoly(jp, h, s, &ok);
+        if (rc) return rc;
+        jp->poly = ok ? 1 : -1;
+    }
     if (jp->poly < 0) return XG_OK;
     return build_coeffs(jp, j, s, out);
 }
@@ -781,7 +816,7 @@ int jump_fill(xg_ensemble* h, uint32_t g, uint64_t words, void* out, unsigned lo
         const unsigned levels = ceil_log2(cnt);
         JumpPowers* jp = jump_powers(h);
         uint32_t* coeffs = nullptr;
-        int rc = jump_coeffs(jp, j, s, &coeffs);
+        int rc = jump_coeffs(jp, h, j, s, &coeffs);
         if (!rc) rc = jump_scratch(h, cnt);
         if (rc) return rc;
         uint32_t* win = h->d_win + static_cast<size_t>(g) * kJWords;
@@ -2016,7 +2051,14 @@ int xg_jump_minpoly(const xg_params_t* p, uint64_t* coeffs64) {
     if (e) return e;
     if (kind == kGeneric) return XG_EUNSUPPORTED;
     std::vector<uint64_t> m;
-    if (!minpoly_of(*p, m)) return XG_EUNSUPPORTED;
+    bool ok = false;
+    auto raw = [p](const std::vector<uint32_t>& window, size_t n, uint32_t* out) {
+        host_raw_words(*p, window, n, out);
+        return XG_OK;
+    };
+    e = minpoly_of(raw, m, &ok);
+    if (e) return e;
+    if (!ok) return XG_EUNSUPPORTED;
     std::memcpy(coeffs64, m.data(), kPolyWords * sizeof(uint64_t));
     return XG_OK;
 }
