@@ -250,3 +250,19 @@ def test_jump_many_streams_power_of_two(oracle, P, n):
     for g in (0, P - 1):
         buf, wy = e.block_state(g)
         assert wy == o.weyl(g) and np.array_equal(np.array(buf, dtype=np.uint64), o.logical_buffer(g))
+
+
+def test_jump_host_generate_across_staging_tiles(oracle):
+    """One stream longer than a 2^26-word staging slot: generate() tiles it
+    (each tile a jump fill continuing the previous one, copies overlapping
+    generation) -- the whole stream is the reference's."""
+    n = (1 << 26) + 1000
+    e = one(4242)
+    g = e.generate(n)
+    assert np.array_equal(g[0], oracle.stream(4242, n))
+    host_rows = [np.zeros(3 * M + 7, dtype=np.uint64)]
+    import ctypes
+
+    arr = (ctypes.c_void_p * 1)(host_rows[0].ctypes.data)
+    assert xg._lib.lib.xg_generate_host_rows(e.handle, 3 * M + 7, arr, None) == 0
+    assert np.array_equal(host_rows[0], oracle.stream(4242, n + 3 * M + 7)[n:].astype(np.uint64))
