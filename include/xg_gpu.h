@@ -116,9 +116,9 @@ int xg_ensemble_info(xg_ensemble_t h, uint32_t* num_streams, uint64_t* base_seed
 
 /* ---- generation (device buffers, asynchronous) --------------------------- */
 
-/* Calls of >= 2^20 words on few streams of a register-window set (w = 32,
- * r = 128, lane_bound >= 32) -- one stream; 2 .. 512 streams of a
- * power-of-two length; up to 64 streams of any length -- are generated as up
+/* Calls on one stream of >= 2^20 words, or on 2 .. 512 streams of >= 2^18
+ * words each, of a register-window set (w = 32, r = 128, lane_bound >= 32) are
+ * generated as up
  * to 1024 segments in parallel, their start states computed by GF(2)
  * jump-ahead (csrc/xg_jump.cuh): the same words, at ensemble speed instead of
  * one warp per stream.  The first such call per parameter set and segment

@@ -203,9 +203,17 @@ bool pair_aligned(const void* out, uint64_t words) {
     else return true;  // f64 (8-byte values, words even), MC, skip
 }
 
+// Output row geometry of a fill: rows come in groups of rg contiguous rows
+// (each row `words` words long), the groups ld output elements apart;
+// ld = 0 means plain block-major rows (ld = the row length, rg = 1).
+template <int MODE>
+uint64_t row_ld(uint64_t words, uint64_t ld) {
+    return ld ? ld : (MODE == kF64 ? words >> 1 : words);
+}
+
 template <int MODE, class P>
 int launch_pair(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t words,
-                void* out, unsigned long long* hits, cudaStream_t s) {
+                void* out, unsigned long long* hits, cudaStream_t s, uint64_t ld = 0, uint32_t rg = 1) {
     // Streams (warps) per CTA.  Every stream is the same amount of work, so
     // what matters is how evenly the warps land on the SMs.  Up to 32 streams
     // per SM, launch one CTA per SM holding ceil(P / SMs) streams: the
@@ -248,16 +256,18 @@ int launch_pair(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count, 
     }
     const unsigned grid = static_cast<unsigned>((static_cast<uint64_t>(g_count) + wpb - 1) / wpb);
     pair_kernel<P, MODE><<<grid, 32 * wpb, smem, s>>>(p, h->d_win, h->d_weyl, g_begin, g_count,
-                                                      words, out, hits);
+                                                      words, out, hits, row_ld<MODE>(words, ld), rg);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cuda_rc(cudaGetLastError());
 }
 
 template <int MODE, class P>
 int launch_word_lane(const P& p, xg_ensemble* h, uint32_t g_begin, uint32_t g_count,
-                     uint64_t words, void* out, unsigned long long* hits, cudaStream_t s) {
+                     uint64_t words, void* out, unsigned long long* hits, cudaStream_t s,
+                     uint64_t ld = 0, uint32_t rg = 1) {
     fill_kernel<P, MODE><<<grid_for(g_count), kThreads, 0, s>>>(p, h->d_win, h->d_weyl, g_begin,
-                                                                g_count, words, out, hits);
+                                                                g_count, words, out, hits,
+                                                                row_ld<MODE>(words, ld), rg);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cuda_rc(cudaGetLastError());
 }
@@ -322,7 +332,7 @@ int launch_gen(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t word
 
 template <int MODE>
 int launch_fill_direct(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t words, void* out,
-                       unsigned long long* hits, cudaStream_t s) {
+                       unsigned long long* hits, cudaStream_t s, uint64_t ld = 0, uint32_t rg = 1) {
     if (words == 0 || g_count == 0) return XG_OK;
     if (h->kind == kGeneric) {
         // The conversions (f32/f64/u64 pairs) and the MC predicate are defined
@@ -340,19 +350,22 @@ int launch_fill_direct(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint6
         return XG_EUNSUPPORTED;
     }
     if constexpr (MODE == kRank) {  // pair-lane kernel only (needs r - s < 64)
-        if (h->kind == kGP32) return launch_pair<MODE>(GP32{}, h, g_begin, g_count, words, out, hits, s);
+        if (h->kind == kGP32) return launch_pair<MODE>(GP32{}, h, g_begin, g_count, words, out, hits, s, ld, rg);
         if (h->kind == kRtJ1)
-            return launch_pair<MODE>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s);
+            return launch_pair<MODE>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s, ld, rg);
         return XG_EUNSUPPORTED;
     } else {
-        if (h->kind != kRtJ2 && pair_aligned<MODE>(out, words)) {
-            if (h->kind == kGP32) return launch_pair<MODE>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-            return launch_pair<MODE>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s);
+        // pair stores need every row start aligned: an odd group stride ld
+        // (rows of u32 / u64 words) sends the call to the word-lane kernel
+        const bool ld_ok = ld == 0 || MODE == kF64 || (ld & 1u) == 0;
+        if (h->kind != kRtJ2 && pair_aligned<MODE>(out, words) && ld_ok) {
+            if (h->kind == kGP32) return launch_pair<MODE>(GP32{}, h, g_begin, g_count, words, out, hits, s, ld, rg);
+            return launch_pair<MODE>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s, ld, rg);
         }
         switch (h->kind) {
-        case kGP32: return launch_word_lane<MODE>(GP32{}, h, g_begin, g_count, words, out, hits, s);
-        case kRtJ1: return launch_word_lane<MODE>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s);
-        default: return launch_word_lane<MODE>(rt_params<2>(h->params), h, g_begin, g_count, words, out, hits, s);
+        case kGP32: return launch_word_lane<MODE>(GP32{}, h, g_begin, g_count, words, out, hits, s, ld, rg);
+        case kRtJ1: return launch_word_lane<MODE>(rt_params<1>(h->params), h, g_begin, g_count, words, out, hits, s, ld, rg);
+        default: return launch_word_lane<MODE>(rt_params<2>(h->params), h, g_begin, g_count, words, out, hits, s, ld, rg);
         }
     }
 }
@@ -368,6 +381,7 @@ int launch_fill_direct(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint6
 
 constexpr uint64_t kJumpMin = 1ull << 20;  // words: below this one warp is faster
 constexpr uint64_t kJumpSkipMany = 1ull << 22;  // skips of more streams than 64: jump from here
+constexpr uint64_t kJumpManyMin = 1ull << 18;   // 2 .. 512 streams: segments of >= 2^16 words, >= 2 each
 constexpr unsigned kJumpMinLog = 16;       // segments of at least 2^16 words
 #ifndef XG_JUMP_MAX_SEG
 #define XG_JUMP_MAX_SEG 1024
@@ -885,45 +899,62 @@ int jump_fill(xg_ensemble* h, uint32_t g, uint64_t words, void* out, unsigned lo
     }
 }
 
-// More streams than the per-stream path takes (65 .. 512) with a power-of-two
-// length: every stream cut into Q = 2^q segments of J = words / Q >= 2^16
-// (P Q <= kJumpMaxSeg), the P Q start windows by doubling over q with the
-// cached powers -- all streams of a level in one product -- then ONE fill of
-// the P Q segments as an ensemble whose rows are the output rows' pieces.
+// 2 .. 512 streams, any length >= 2^20: every stream cut into Q segments of
+// J = 2^j words (P Q <= kJumpMaxSeg; Q = words / J, so the remainder
+// rem = words - Q J < J), the start windows of all P (Q + 1) segments by
+// doubling over q with the cached powers -- every stream of a level in one
+// product, rows q-major -- then ONE fill of the P Q full segments (rows
+// g-major; output row (g, q) at g ld + q J: groups of Q rows, ld apart) and,
+// concurrently on the side stream, one of the P remainders.
 template <int MODE>
 int jump_fill_many(xg_ensemble* h, uint32_t g0, uint32_t P, uint64_t words, void* out,
                    unsigned long long* hits, cudaStream_t s) {
-    uint32_t Q = 1;
-    while (2 * Q * P <= kJumpMaxSeg && (words / (2 * Q)) >= (1ull << kJumpMinLog)) Q *= 2;
+    const uint64_t qmax = kJumpMaxSeg / P;  // >= 2
+    unsigned j = kJumpMinLog;
+    while ((words >> j) > qmax) ++j;
+    const uint64_t J = 1ull << j;
+    const uint32_t Q = static_cast<uint32_t>(words >> j);
+    const uint64_t rem = words - static_cast<uint64_t>(Q) * J;
     if (Q < 2) return launch_fill_direct<MODE>(h, g0, P, words, out, hits, s);
-    const uint64_t J = words / Q;
-    const unsigned j = 63 - static_cast<unsigned>(__builtin_clzll(J)), lq = ceil_log2(Q);
+    const uint32_t cq = Q + (rem ? 1u : 0u);  // segment starts per stream
+    const unsigned lq = ceil_log2(cq);
     JumpPowers* jp = jump_powers(h);
     int rc = jump_ensure(jp, j + lq - 1, s);
-    if (!rc) rc = jump_scratch(h, P * Q);
+    if (!rc) rc = jump_scratch(h, P * cq);
     if (rc) return rc;
     rc = cuda_rc(cudaMemcpyAsync(h->d_jrows, h->d_win + static_cast<size_t>(g0) * kJWords,
                                  static_cast<size_t>(P) * kJRowBytes, cudaMemcpyDeviceToDevice, s));
-    for (unsigned l = 0; l < lq && !rc; ++l) {  // rows [P 2^l, P 2^(l+1)) = rows [0, P 2^l) G^(J 2^l)
+    for (unsigned l = 0; l < lq && !rc; ++l) {  // rows [P 2^l, ..) = rows [0, ..) G^(J 2^l), q-major
         const uint32_t have = P << l;
-        rc = gf2_mul(h->d_jrows, have, jp->pow[j + l], h->d_jrows + static_cast<size_t>(have) * kJWords,
+        const uint32_t n = std::min(have, P * cq - have);
+        rc = gf2_mul(h->d_jrows, n, jp->pow[j + l], h->d_jrows + static_cast<size_t>(have) * kJWords,
                      h->d_jpart, s);
     }
     if (rc) return rc;
     const uint32_t step = MODE == kRaw ? 0u : static_cast<uint32_t>(J * (h->params.omega & kMask32));
-    jump_permute_kernel<<<(P * Q * 32 + 255) / 256, 256, 0, s>>>(h->d_jrows, h->d_jW, h->d_weyl + g0,
-                                                               h->d_jweyl, P, Q, step);
+    jump_permute_kernel<<<(P * cq * 32 + 255) / 256, 256, 0, s>>>(h->d_jrows, h->d_jW, h->d_weyl + g0,
+                                                                h->d_jweyl, P, Q, cq, step);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     rc = cuda_rc(cudaGetLastError());
     xg_ensemble view = *h;
     view.d_win = h->d_jW;
     view.d_weyl = h->d_jweyl;
-    view.num_streams = P * Q;
-    if (!rc) rc = launch_fill_direct<MODE>(&view, 0, P * Q, J, out, hits, s);
+    view.num_streams = P * cq;
+    const uint64_t ld = row_ld<MODE>(words, 0);  // output elements per stream row
+    if (!rc && rem) {  // the P remainders (rows P Q + g) concurrently on the side stream
+        rc = cuda_rc(cudaEventRecord(h->jev[0], s));
+        if (!rc) rc = cuda_rc(cudaStreamWaitEvent(h->jside, h->jev[0], 0));
+        if (!rc)
+            rc = launch_fill_direct<MODE>(&view, P * Q, P, rem, out_at<MODE>(out, static_cast<uint64_t>(Q) * J),
+                                          hits, h->jside, ld, 1);
+        if (!rc) rc = cuda_rc(cudaEventRecord(h->jev[1], h->jside));
+    }
+    if (!rc) rc = launch_fill_direct<MODE>(&view, 0, P * Q, J, out, hits, s, ld, Q);
+    if (!rc && rem) rc = cuda_rc(cudaStreamWaitEvent(s, h->jev[1], 0));
     if (rc) return rc;
     jump_finish_many_kernel<<<(P * 32 + 255) / 256, 256, 0, s>>>(h->d_jW, h->d_jweyl,
                                                                  h->d_win + static_cast<size_t>(g0) * kJWords,
-                                                                 h->d_weyl + g0, P, Q);
+                                                                 h->d_weyl + g0, P, Q, rem != 0);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cuda_rc(cudaGetLastError());
 }
@@ -933,25 +964,20 @@ int jump_fill_many(xg_ensemble* h, uint32_t g0, uint32_t P, uint64_t words, void
 // directly:
 //   skip of >= 2^20 words (more than 64 streams: >= 2^22)     -> jump_skip, O(log n)
 //   one stream, >= 2^20 words                                  -> jump_fill (Krylov)
-//   2 .. 512 streams, a power-of-two length >= 2^20            -> jump_fill_many
-//   <= 64 streams, >= 2^20 words each per stream in the call    -> jump_fill per stream
+//   2 .. 512 streams, >= 2^18 words                            -> jump_fill_many
 template <int MODE>
 int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t words, void* out,
                 unsigned long long* hits, cudaStream_t s) {
-    if (h->kind == kGeneric || words < kJumpMin || g_count == 0)
+    if (h->kind == kGeneric || words < kJumpManyMin || g_count == 0)
         return launch_fill_direct<MODE>(h, g_begin, g_count, words, out, hits, s);
     if constexpr (MODE == kSkip) {
-        if (g_count <= 64 || words >= kJumpSkipMany) return jump_skip(h, g_begin, g_count, words, s);
+        if (words >= kJumpMin && (g_count <= 64 || words >= kJumpSkipMany))
+            return jump_skip(h, g_begin, g_count, words, s);
     } else {
-        if (g_count == 1) return jump_fill<MODE>(h, g_begin, words, out, hits, s);
-        if (2 * g_count <= kJumpMaxSeg && (words & (words - 1)) == 0)
+        if (g_count == 1) {
+            if (words >= kJumpMin) return jump_fill<MODE>(h, g_begin, words, out, hits, s);
+        } else if (2 * g_count <= kJumpMaxSeg) {
             return jump_fill_many<MODE>(h, g_begin, g_count, words, out, hits, s);
-        if (g_count <= 64 && words >= static_cast<uint64_t>(g_count) * kJumpMin) {
-            int rc = XG_OK;
-            for (uint32_t i = 0; i < g_count && !rc; ++i)
-                rc = jump_fill<MODE>(h, g_begin + i, words, out_at<MODE>(out, static_cast<uint64_t>(i) * words),
-                                     hits, s);
-            return rc;
         }
     }
     return launch_fill_direct<MODE>(h, g_begin, g_count, words, out, hits, s);

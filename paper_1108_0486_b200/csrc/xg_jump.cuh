@@ -220,30 +220,40 @@ __global__ void jump_end_kernel(const uint32_t* __restrict__ win, const uint32_t
     if (t == 0) dst_w[0] = w[0];
 }
 
-// Many streams, Q segments each (jump_fill_many): the jumped windows come
-// q-major (row q P + g, so each doubling level is one contiguous product);
-// the fill wants them g-major (row g Q + q: segment q of stream g, output at
-// g words + q J).  dst[g Q + q] = src[q P + g], wout[g Q + q] = w[g] + q step.
-// One warp per row, 16 bytes per lane.
+// Many streams, Q full segments (+ one remainder if cq = Q + 1) each
+// (jump_fill_many): the jumped windows come q-major (row q P + g, so each
+// doubling level is one contiguous product); the fill wants the full
+// segments g-major (row g Q + q: segment q of stream g, output at g ld + q J)
+// followed by the P remainders (row P Q + g, already contiguous).
+// dst[g Q + q] = src[q P + g], dst[P Q + g] = src[Q P + g];
+// Weyl words w[g] + q step alike.  One warp per row, 16 bytes per lane.
 __global__ void __launch_bounds__(256)
 jump_permute_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, const uint32_t* __restrict__ w,
-                    uint32_t* __restrict__ wout, uint32_t P, uint32_t Q, uint32_t step) {
+                    uint32_t* __restrict__ wout, uint32_t P, uint32_t Q, uint32_t cq, uint32_t step) {
     const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
-    if (row >= P * Q) return;
-    const uint32_t g = row / Q, q = row % Q;
+    if (row >= P * cq) return;
+    uint32_t g, q;
+    if (row < P * Q) {
+        g = row / Q;
+        q = row % Q;
+    } else {
+        g = row - P * Q;
+        q = Q;
+    }
     reinterpret_cast<uint4*>(dst + static_cast<size_t>(row) * kJWords)[lane] =
         reinterpret_cast<const uint4*>(src + (static_cast<size_t>(q) * P + g) * kJWords)[lane];
     if (lane == 0) wout[row] = w[g] + q * step;
 }
 
 // ... and after the fill every stream continues from its last segment:
-// win[g] = rows[g Q + Q - 1], weyl[g] = wrows[g Q + Q - 1].
+// the remainder (row P Q + g) if there is one, else row g Q + Q - 1.
 __global__ void __launch_bounds__(256)
 jump_finish_many_kernel(const uint32_t* __restrict__ rows, const uint32_t* __restrict__ wrows,
-                        uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32_t P, uint32_t Q) {
+                        uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32_t P, uint32_t Q,
+                        bool has_rem) {
     const uint32_t g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31u;
     if (g >= P) return;
-    const size_t last = static_cast<size_t>(g) * Q + Q - 1;
+    const size_t last = has_rem ? static_cast<size_t>(P) * Q + g : static_cast<size_t>(g) * Q + Q - 1;
     reinterpret_cast<uint4*>(win + static_cast<size_t>(g) * kJWords)[lane] =
         reinterpret_cast<const uint4*>(rows + last * kJWords)[lane];
     if (lane == 0) weyl[g] = wrows[last];

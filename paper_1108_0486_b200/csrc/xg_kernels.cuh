@@ -294,7 +294,7 @@ template <class P, int MODE>
 __global__ void __launch_bounds__(kThreads)
 fill_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32_t g_begin,
             uint32_t g_count, uint64_t words, void* __restrict__ out,
-            unsigned long long* __restrict__ hits_out) {
+            unsigned long long* __restrict__ hits_out, uint64_t ld, uint32_t rg) {
     const unsigned lane = threadIdx.x & 31;
     const uint32_t gl = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
     if (gl >= g_count) return;
@@ -325,7 +325,9 @@ fill_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32
     const uint64_t per_stream_vals = kPairs ? (words >> 1) : words;
     void* o = out;
     if constexpr (MODE == kU32 || MODE == kF32 || MODE == kF64 || MODE == kRaw || MODE == kWide) {
-        const uint64_t first = static_cast<uint64_t>(gl) * per_stream_vals + lane;
+        // row gl: groups of rg contiguous rows, ld elements apart (pair_kernel)
+        const uint64_t first = static_cast<uint64_t>(gl / rg) * ld +
+                               static_cast<uint64_t>(gl % rg) * per_stream_vals + lane;
         if constexpr (MODE == kF64) o = static_cast<double*>(out) + first;
         else if constexpr (MODE == kWide) o = static_cast<unsigned long long*>(out) + first;
         else o = static_cast<uint32_t*>(out) + first;

@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(std::is_same_v<P, GP32> ? 1024 : 256,
                                   std::is_same_v<P, GP32> ? (MODE == kMC ? 1 : 2) : 5)
 pair_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32_t g_begin,
             uint32_t g_count, uint64_t words, void* __restrict__ out,
-            unsigned long long* __restrict__ hits_out) {
+            unsigned long long* __restrict__ hits_out, uint64_t ld, uint32_t rg) {
     const unsigned lane = threadIdx.x & 31u;
     // CTAs hold 1..8 streams (the host spreads small ensembles over the SMs)
     const uint32_t gl = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -300,13 +300,18 @@ pair_kernel(P p, uint32_t* __restrict__ win, uint32_t* __restrict__ weyl, uint32
     uint32_t wl = weyl0 + (2u * lane + 1u) * p.omega;  // Weyl term of word 2l (parallel.cpp:33-39)
     const uint32_t w64 = 64u * p.omega;
 
+    // Row gl of the output: rows come in groups of rg contiguous rows, the
+    // groups ld elements apart (rg = 1, ld = the row length: plain block-major
+    // rows; jump-ahead segments of several streams: rg > 1).
+    const uint64_t seg = MODE == kF64 ? (words >> 1) : words;  // output elements per row
+    const uint64_t row0 = static_cast<uint64_t>(gl / rg) * ld + static_cast<uint64_t>(gl % rg) * seg;
     void* o = out;
     if constexpr (MODE == kU32 || MODE == kRaw || MODE == kF32)
-        o = static_cast<uint32_t*>(out) + static_cast<uint64_t>(gl) * words + 2u * lane;
+        o = static_cast<uint32_t*>(out) + row0 + 2u * lane;
     else if constexpr (MODE == kWide)
-        o = static_cast<unsigned long long*>(out) + static_cast<uint64_t>(gl) * words + 2u * lane;
+        o = static_cast<unsigned long long*>(out) + row0 + 2u * lane;
     else if constexpr (MODE == kF64)
-        o = static_cast<double*>(out) + static_cast<uint64_t>(gl) * (words >> 1) + lane;
+        o = static_cast<double*>(out) + row0 + lane;
     AccT<MODE> hits{};
 
     uint64_t left = words >> 7;  // bodies of 128 words

@@ -41,14 +41,14 @@ for n in [1 << 20, 1 << 22, 10**8, 1 << 28, 1 << 30]:
     ms = timed(lambda: e.fill_u32(n, out=out), reps)
     res[f"jump_fill_u32 n={n}"] = {"ms": ms, "rn_per_s": n / (ms / 1e3)}
     del out
-# one warp (direct path): 65 streams of a length that is not a power of two
-# (more streams than the per-stream jump takes), per-stream rate
-d = xg.BlockEnsemble(p, 1, 65, 63)
-n = (1 << 22) + 128
-out = torch.empty((65, n), dtype=torch.uint32, device="cuda")
+# one warp per stream (the direct path): 513 streams (more than the jump
+# paths take), per-stream rate
+d = xg.BlockEnsemble(p, 1, 513, 63)
+n = 1 << 18
+out = torch.empty((513, n), dtype=torch.uint32, device="cuda")
 d.fill_u32(n, out=out)
 ms = timed(lambda: d.fill_u32(n, out=out), 5)
-res["direct one warp (65 streams, n=2^22+128, per stream)"] = {"ms": ms, "rn_per_s": n / (ms / 1e3)}
+res["direct one warp (513 streams x 2^18, per stream)"] = {"ms": ms, "rn_per_s": n / (ms / 1e3)}
 # a batch skip: 2^14 streams jump 2^22 words (generating them: ~25 ms)
 b = xg.BlockEnsemble(p, 1, 1 << 14, 63)
 b.skip(1 << 22)

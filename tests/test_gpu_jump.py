@@ -266,3 +266,22 @@ def test_jump_host_generate_across_staging_tiles(oracle):
     arr = (ctypes.c_void_p * 1)(host_rows[0].ctypes.data)
     assert xg._lib.lib.xg_generate_host_rows(e.handle, 3 * M + 7, arr, None) == 0
     assert np.array_equal(host_rows[0], oracle.stream(4242, n + 3 * M + 7)[n:].astype(np.uint64))
+
+
+@pytest.mark.parametrize("P,n", [(100, (1 << 21) + 777), (65, (1 << 20) + 1), (7, 3 * M + 64), (300, 906752),
+                                 (2, (1 << 18) + 3)])
+def test_jump_many_streams_any_length(oracle, P, n):
+    """2 .. 512 streams of any length >= 2^18: Q segments of 2^j words per
+    stream in one fill (output rows in groups of Q, one stream row apart --
+    the fill kernels' row-group addressing) plus the per-stream remainders on
+    the side stream; odd lengths send the fills to the word-lane kernel."""
+    e = xg.BlockEnsemble(GP32, 500 + P, P, 63)
+    o = oracle.ensemble(500 + P, P)
+    assert np.array_equal(host(e.fill_u32(n)), o.fill_u32(n))
+    assert np.array_equal(host(e.fill_f64(n // 2)).view(np.uint64), o.fill_f64(n // 2).view(np.uint64))
+    k = 32 * (n // 64)
+    assert int(e.mc_pi(k).item()) == int(o.mc_hits(k).sum())
+    assert np.array_equal(host(e.fill_u32(333)), o.fill_u32(333))
+    for g in (0, P - 1):
+        buf, wy = e.block_state(g)
+        assert wy == o.weyl(g) and np.array_equal(np.array(buf, dtype=np.uint64), o.logical_buffer(g))
