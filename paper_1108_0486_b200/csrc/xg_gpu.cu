@@ -474,11 +474,15 @@ int gf2_mul(const uint32_t* A, uint32_t rows, const uint32_t* B, uint32_t* C, ui
     };
     if (rows >= 256) {  // many rows: tables pay for themselves
         ksplit = 4096u / kM4Span;  // the staged span of B; 16 x 4096 partial rows at most
-        const dim3 grid(4, (rows + 8 * 16 - 1) / (8 * 16), ksplit);
+#ifndef XG_M4RM_RW
+#define XG_M4RM_RW 16
+#endif
+        constexpr int RW = XG_M4RM_RW;  // rows per warp: 8 RW rows share each CTA's tables
+        const dim3 grid(4, (rows + 8 * RW - 1) / (8 * RW), ksplit);
         static std::atomic<uint64_t> done{0};
-        const int rc = raise_smem_once(gf2_mul_m4rm_kernel<16>, kM4Smem, done);
+        const int rc = raise_smem_once(gf2_mul_m4rm_kernel<RW>, kM4Smem, done);
         if (rc) return rc;
-        gf2_mul_m4rm_kernel<16><<<grid, 256, kM4Smem, s>>>(A, B, part, rows, 4096u / ksplit, ldb);
+        gf2_mul_m4rm_kernel<RW><<<grid, 256, kM4Smem, s>>>(A, B, part, rows, 4096u / ksplit, ldb);
     } else if (rows >= 64) {
         launch(gf2_mul_partial_kernel<2>, 2);
     } else {
