@@ -617,29 +617,55 @@ void host_raw_words(const xg_params_t& p, std::vector<uint32_t> window, size_t n
 
 // Berlekamp-Massey over GF(2): the shortest connection polynomial c
 // (c[0] = 1, b_n = XOR_{i=1..L} c_i b_{n-i}) of the bit sequence; returns L.
+// Bit-packed: the discrepancy at step i is the parity of C AND (the sequence
+// reversed, shifted so bit k lines up with b_{i-k}) -- one multiword shift
+// and AND per step (8192 bits: ~1 ms).
 unsigned berlekamp_massey_bits(const std::vector<uint8_t>& b, std::vector<uint8_t>& c) {
-    const size_t n = b.size();
-    c.assign(n + 1, 0);
-    std::vector<uint8_t> bb(n + 1, 0), t;
-    c[0] = bb[0] = 1;
+    const size_t n = b.size(), nw = (n + 1 + 63) / 64 + 1;
+    std::vector<uint64_t> rev(nw, 0), C(nw, 0), B(nw, 0), T(nw, 0), t(nw, 0);
+    for (size_t j = 0; j < n; ++j)  // rev bit j = b_{n-1-j}
+        if (b[n - 1 - j]) rev[j / 64] |= 1ull << (j % 64);
+    auto shr = [&](const std::vector<uint64_t>& x, size_t sh, std::vector<uint64_t>& out) {
+        const size_t ws = sh / 64, bs = sh % 64;
+        for (size_t w = 0; w < nw; ++w) {
+            const size_t src = w + ws;
+            uint64_t v = src < nw ? x[src] >> bs : 0;
+            if (bs && src + 1 < nw) v |= x[src + 1] << (64 - bs);
+            out[w] = v;
+        }
+    };
+    auto xor_shl = [&](std::vector<uint64_t>& x, const std::vector<uint64_t>& y, size_t sh) {  // x ^= y << sh
+        const size_t ws = sh / 64, bs = sh % 64;
+        for (size_t w = nw; w-- > ws;) {
+            const size_t src = w - ws;
+            uint64_t v = y[src] << bs;
+            if (bs && src > 0) v |= y[src - 1] >> (64 - bs);
+            x[w] ^= v;
+        }
+    };
+    C[0] = B[0] = 1;
     unsigned L = 0;
     size_t m = 1;
     for (size_t i = 0; i < n; ++i) {
-        uint8_t d = b[i];
-        for (unsigned k = 1; k <= L; ++k) d ^= c[k] & b[i - k];
+        shr(rev, n - 1 - i, t);  // t bit k = b_{i-k} (k <= i), 0 beyond
+        uint64_t acc = 0;
+        for (size_t w = 0; w <= L / 64 && w < nw; ++w) acc ^= C[w] & t[w];
+        const unsigned d = __builtin_popcountll(acc) & 1u;
         if (!d) {
             ++m;
         } else if (2 * L <= i) {
-            t = c;
-            for (size_t k = 0; k + m <= n; ++k) c[k + m] ^= bb[k];
+            T = C;
+            xor_shl(C, B, m);
             L = static_cast<unsigned>(i + 1 - L);
-            bb = t;
+            B = T;
             m = 1;
         } else {
-            for (size_t k = 0; k + m <= n; ++k) c[k + m] ^= bb[k];
+            xor_shl(C, B, m);
             ++m;
         }
     }
+    c.assign(n + 1, 0);
+    for (size_t k = 0; k <= n; ++k) c[k] = static_cast<uint8_t>((C[k / 64] >> (k % 64)) & 1u);
     return L;
 }
 
