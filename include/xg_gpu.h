@@ -116,7 +116,7 @@ int xg_ensemble_info(xg_ensemble_t h, uint32_t* num_streams, uint64_t* base_seed
 
 /* ---- generation (device buffers, asynchronous) --------------------------- */
 
-/* Calls on one stream of >= 2^20 words, or on 2 .. 512 streams of >= 2^18
+/* Calls on one stream of >= 2^20 words, or on 2 .. 700 streams of >= 2^18
  * words each, of a register-window set (w = 32, r = 128, lane_bound >= 32) are
  * generated as up
  * to 1024 segments in parallel, their start states computed by GF(2)

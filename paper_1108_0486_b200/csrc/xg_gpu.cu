@@ -381,7 +381,8 @@ int launch_fill_direct(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint6
 
 constexpr uint64_t kJumpMin = 1ull << 20;  // words: below this one warp is faster
 constexpr uint64_t kJumpSkipMany = 1ull << 22;  // skips of more streams than 64: jump from here
-constexpr uint64_t kJumpManyMin = 1ull << 18;   // 2 .. 512 streams: segments of >= 2^16 words, >= 2 each
+constexpr uint64_t kJumpManyMin = 1ull << 18;   // 2 .. 700 streams: segments of >= 2^16 words, >= 2 each
+constexpr uint32_t kJumpManyMax = 700;          // from ~760 streams one warp each saturates HBM
 constexpr unsigned kJumpMinLog = 16;       // segments of at least 2^16 words
 #ifndef XG_JUMP_MAX_SEG
 #define XG_JUMP_MAX_SEG 1024
@@ -929,8 +930,8 @@ int jump_fill(xg_ensemble* h, uint32_t g, uint64_t words, void* out, unsigned lo
     }
 }
 
-// 2 .. 512 streams, any length >= 2^20: every stream cut into Q segments of
-// J = 2^j words (P Q <= kJumpMaxSeg; Q = words / J, so the remainder
+// 2 .. 700 streams, any length >= 2^18: every stream cut into Q segments of
+// J = 2^j words (P Q <= max(kJumpMaxSeg, 2 P); Q = words / J, so the remainder
 // rem = words - Q J < J), the start windows of all P (Q + 1) segments by
 // doubling over q with the cached powers -- every stream of a level in one
 // product, rows q-major -- then ONE fill of the P Q full segments (rows
@@ -939,7 +940,9 @@ int jump_fill(xg_ensemble* h, uint32_t g, uint64_t words, void* out, unsigned lo
 template <int MODE>
 int jump_fill_many(xg_ensemble* h, uint32_t g0, uint32_t P, uint64_t words, void* out,
                    unsigned long long* hits, cudaStream_t s) {
-    const uint64_t qmax = kJumpMaxSeg / P;  // >= 2
+    // P Q <= kJumpMaxSeg segments; 513 .. 700 streams still get Q = 2 (up to
+    // ~1400 segments: fewer than ~760 warps leave the fill below the HBM rate)
+    const uint64_t qmax = std::max<uint64_t>(2, kJumpMaxSeg / P);
     unsigned j = kJumpMinLog;
     while ((words >> j) > qmax) ++j;
     const uint64_t J = 1ull << j;
@@ -994,7 +997,7 @@ int jump_fill_many(xg_ensemble* h, uint32_t g0, uint32_t P, uint64_t words, void
 // directly:
 //   skip of >= 2^20 words (more than 64 streams: >= 2^22)     -> jump_skip, O(log n)
 //   one stream, >= 2^20 words                                  -> jump_fill (Krylov)
-//   2 .. 512 streams, >= 2^18 words                            -> jump_fill_many
+//   2 .. 700 streams, >= 2^18 words                            -> jump_fill_many
 template <int MODE>
 int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t words, void* out,
                 unsigned long long* hits, cudaStream_t s) {
@@ -1006,7 +1009,7 @@ int launch_fill(xg_ensemble* h, uint32_t g_begin, uint32_t g_count, uint64_t wor
     } else {
         if (g_count == 1) {
             if (words >= kJumpMin) return jump_fill<MODE>(h, g_begin, words, out, hits, s);
-        } else if (2 * g_count <= kJumpMaxSeg) {
+        } else if (g_count <= kJumpManyMax) {
             return jump_fill_many<MODE>(h, g_begin, g_count, words, out, hits, s);
         }
     }

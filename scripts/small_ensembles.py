@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1108_0486_b200 as xg  # noqa: E402
 
 p = xg.xorgensgp32_params()
-for P in (1, 8, 64, 148, 296, 512, 1184, 2048, 4096, 9472, 16384):
+for P in (1, 8, 64, 148, 296, 512, 600, 700, 1184, 2048, 4096, 9472, 16384):
     per = 1 << 20 if P <= 256 else max(1 << 16, (1 << 28) // P)
     per -= per % 128
     e = xg.BlockEnsemble(p, 1, P, 63)

@@ -269,9 +269,9 @@ def test_jump_host_generate_across_staging_tiles(oracle):
 
 
 @pytest.mark.parametrize("P,n", [(100, (1 << 21) + 777), (65, (1 << 20) + 1), (7, 3 * M + 64), (300, 906752),
-                                 (2, (1 << 18) + 3)])
+                                 (2, (1 << 18) + 3), (600, (1 << 18) + 64)])
 def test_jump_many_streams_any_length(oracle, P, n):
-    """2 .. 512 streams of any length >= 2^18: Q segments of 2^j words per
+    """2 .. 700 streams of any length >= 2^18: Q segments of 2^j words per
     stream in one fill (output rows in groups of Q, one stream row apart --
     the fill kernels' row-group addressing) plus the per-stream remainders on
     the side stream; odd lengths send the fills to the word-lane kernel."""
